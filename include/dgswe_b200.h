@@ -1,0 +1,150 @@
+/*
+ * dgswe_b200.h -- C ABI of the B200 (sm_100a, fp64) DG shallow-water
+ * time-stepping path.  Plain pointers and sizes only; every device buffer is
+ * owned by the caller (PyTorch in this repo), the context owns only the
+ * uploaded constant tables, a status word and cached CUDA graphs.
+ *
+ * Each entry point replaces one reference interface
+ * (/root/reference/pkg/src/dgswe/<file>:<line>):
+ *
+ *   dgswe_create / dgswe_destroy   SpatialOperator.__init__ precomputation
+ *                                  (dg.py:174-219, _setup_mass 223-239,
+ *                                  _setup_coords 254-283)
+ *   dgswe_rhs                      SpatialOperator.assemble_rhs (dg.py:504-523)
+ *                                  incl. _halo_exchange 330-346, nodal_eval
+ *                                  348-357, _pointwise_physics 359-372,
+ *                                  _interface_alphas 385-421,
+ *                                  _interface_fluxes 423-453, _contract 455-502
+ *   dgswe_stage                    one RK stage: rhs + the stage update of
+ *                                  rk_step (timestep.py:149-167), fused
+ *   dgswe_axpy                     timestep._axpy (timestep.py:132-141) and the
+ *                                  finite check of rk_step (165-166)
+ *   dgswe_ssprk3                   integrate's step loop (timestep.py:210-229)
+ *                                  for tableau(3) (timestep.py:65-70), as
+ *                                  Shu-Osher stages, CUDA-graph batched
+ *   dgswe_alpha_prepass            global Rusanov alpha (dg.py:389-411)
+ *   dgswe_status                   PositivityError (models.py:143-146) and
+ *                                  DivergenceError (timestep.py:165-166,
+ *                                  220-226) as device status bits
+ *
+ * Layout of every state buffer (fp64):  [nz][nrows][3][nphi][nx]
+ *   variable v in {h, hu, hv}; mode m = a*(p+1)+b (a: lambda degree,
+ *   b: theta degree, basis.py:5-13); longitude index i fastest.
+ *   Buffer row r holds global latitude row row0 + r.  The rows computed are
+ *   [jlo, jhi) (local); a band's halo rows jlo-1 and jhi must hold the
+ *   neighbour band's coefficients whenever they are inside the sphere.
+ *
+ * All calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ * default) except dgswe_status, which synchronises it.  Return 0 on success,
+ * a negative DGSWE_E* code otherwise; dgswe_last_error() describes it.
+ */
+#ifndef DGSWE_B200_H
+#define DGSWE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DGSWE_ABI_VERSION 1
+
+/* status bits (dgswe_status) */
+#define DGSWE_STATUS_POSITIVITY 0x1u  /* h <= 0 (or NaN) at a quadrature node */
+#define DGSWE_STATUS_NONFINITE 0x2u   /* non-finite coefficient after an update */
+#define DGSWE_STATUS_MEAN_NONPOS 0x4u /* cell-mean h <= 0 (check_positivity) */
+
+/* error codes */
+#define DGSWE_OK 0
+#define DGSWE_EINVAL (-1)
+#define DGSWE_ECUDA (-2)
+#define DGSWE_ENOMEM (-3)
+#define DGSWE_EUNSUPPORTED (-4)
+
+/* Rusanov alpha mode (dg.py:47-57) */
+#define DGSWE_ALPHA_LOCAL 0
+#define DGSWE_ALPHA_GLOBAL_PINNED 1
+#define DGSWE_ALPHA_GLOBAL 2
+
+typedef struct dgswe_cfg {
+    int nx, ny, nz, p;        /* global element grid, levels, degree (0..6) */
+    int row0;                 /* global latitude row of buffer row 0 */
+    int nrows;                /* rows in every state buffer */
+    int jlo, jhi;             /* local rows computed by this context */
+    double radius;            /* R (mesh.py:28) */
+    double gravity;           /* g (mesh.py:30) */
+    double h_floor;           /* velocity-recovery floor, 1e-8*h_ref (models.py:159) */
+    double dx, dy;            /* element extents in lambda / theta (mesh.py:66-72) */
+    int alpha_mode;           /* DGSWE_ALPHA_* */
+    double alpha;             /* pinned alpha for DGSWE_ALPHA_GLOBAL_PINNED */
+    int row_chunk;            /* latitude rows per CTA, 0 = automatic */
+} dgswe_cfg;
+
+/* Host tables; copied during dgswe_create, not retained. */
+typedef struct dgswe_tables {
+    const double *leg;        /* (n, n): P_a(x_q), row a      (basis.py:58-66)  */
+    const double *dleg;       /* (n, n): P'_a(x_q), row a     (basis.py:69-81)  */
+    const double *weights;    /* (n): Gauss weights            (basis.py:50-55)  */
+    const double *cos_r_int;  /* (ny, n): cos(theta)/R at interior node latitudes  (dg.py:248,268) */
+    const double *sin_r_int;  /* (ny, n): sin(theta)/R */
+    const double *fcos_int;   /* (ny, n): 2 Omega sin cos */
+    const double *cos_r_edge; /* (ny+1): cos/R at edge latitude y_edges[e] (dg.py:276-282) */
+    const double *cos_edge;   /* (ny+1): cos(y_edges[e]) for the y-direction alpha (models.py:280) */
+    const double *minv;       /* (ny, nphi, nphi): per-row inverse mass (basis.py:159-190) */
+} dgswe_tables;
+
+typedef struct dgswe_ctx dgswe_ctx;
+
+int dgswe_abi_version(void);
+const char *dgswe_last_error(void);
+
+int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *tables, dgswe_ctx **out);
+void dgswe_destroy(dgswe_ctx *ctx);
+
+/* elements of one state buffer (nz * nrows * 3 * nphi * nx) */
+int64_t dgswe_state_elems(const dgswe_ctx *ctx);
+
+/* K = M^-1 (volume - boundary + source)(X) on rows [jlo, jhi). */
+int dgswe_rhs(dgswe_ctx *ctx, const double *X, double *K, void *stream);
+
+/* Y = a*U + b*X + g*RHS(X) on rows [jlo, jhi); U may be NULL when a == 0.
+ * Y must not alias X; Y may alias U.  `tag` is recorded as the step index
+ * of the first status flag raised (dgswe_status). */
+int dgswe_stage(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g,
+                double *Y, int tag, void *stream);
+
+/* Same, restricted to local rows [r0, r1) (for interior/boundary overlap). */
+int dgswe_stage_rows(dgswe_ctx *ctx, double a, const double *U, double b, const double *X,
+                     double g, double *Y, int tag, int r0, int r1, void *stream);
+
+/* y = y + x*coef on rows [jlo, jhi), two roundings (timestep.py:137-141);
+ * check_finite != 0 raises DGSWE_STATUS_NONFINITE for non-finite results. */
+int dgswe_axpy(dgswe_ctx *ctx, double coef, const double *x, double *y, int check_finite,
+               int tag, void *stream);
+
+/* nsteps of Shu-Osher SSPRK3 on u (in place) with scratch w1, w2, batched
+ * into one CUDA graph per (buffers, dt, nsteps).  check_mean != 0 enables
+ * the per-step cell-mean check on h (timestep.py:220-226).  Status tags are
+ * the 0-based step index within this call.  Single-band contexts only. */
+int dgswe_ssprk3(dgswe_ctx *ctx, double *u, double *w1, double *w2, double dt, int nsteps,
+                 int check_mean, void *stream);
+
+/* Global-mode alpha: device max over all traces of X into the context's
+ * alpha buffer (two doubles, x then y).  dgswe_alpha_buffer exposes it so a
+ * multi-GPU caller can all-reduce(MAX) it before dgswe_stage. */
+int dgswe_alpha_prepass(dgswe_ctx *ctx, const double *X, void *stream);
+double *dgswe_alpha_buffer(dgswe_ctx *ctx);
+/* 0: dgswe_stage runs the prepass itself (single GPU); 1: caller does. */
+int dgswe_set_external_alpha(dgswe_ctx *ctx, int external);
+
+/* Reads (and optionally clears) the status word; synchronises `stream`.
+ * first_tag receives the smallest tag that raised a flag (INT32_MAX if none). */
+int dgswe_status(dgswe_ctx *ctx, uint32_t *flags, int32_t *first_tag, int reset, void *stream);
+
+/* Kernel launches issued by this context since creation (instrumentation). */
+int64_t dgswe_launch_count(const dgswe_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DGSWE_B200_H */

@@ -1,0 +1,93 @@
+"""ctypes binding of the C ABI in include/dgswe_b200.h.
+
+The shared library is built in-tree (``paper_2303_11767_b200/libdgswe_b200.so``,
+see :mod:`.build`).  There is no fallback: if the library is missing or the
+GPU is absent every device call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdgswe_b200.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "dgswe_b200.h")
+
+STATUS_POSITIVITY = 0x1
+STATUS_NONFINITE = 0x2
+STATUS_MEAN_NONPOS = 0x4
+
+ALPHA_LOCAL, ALPHA_GLOBAL_PINNED, ALPHA_GLOBAL = 0, 1, 2
+
+_D = ctypes.c_double
+_PD = ctypes.POINTER(ctypes.c_double)
+_VP = ctypes.c_void_p
+_I = ctypes.c_int
+
+
+class Cfg(ctypes.Structure):
+    _fields_ = [
+        ("nx", _I), ("ny", _I), ("nz", _I), ("p", _I),
+        ("row0", _I), ("nrows", _I), ("jlo", _I), ("jhi", _I),
+        ("radius", _D), ("gravity", _D), ("h_floor", _D), ("dx", _D), ("dy", _D),
+        ("alpha_mode", _I), ("alpha", _D), ("row_chunk", _I),
+    ]
+
+
+class Tables(ctypes.Structure):
+    _fields_ = [(name, _PD) for name in (
+        "leg", "dleg", "weights", "cos_r_int", "sin_r_int", "fcos_int",
+        "cos_r_edge", "cos_edge", "minv")]
+
+
+# name -> (restype, argtypes); the single source for the symbol-export test
+SIGNATURES = {
+    "dgswe_abi_version": (_I, []),
+    "dgswe_last_error": (ctypes.c_char_p, []),
+    "dgswe_create": (_I, [ctypes.POINTER(Cfg), ctypes.POINTER(Tables), ctypes.POINTER(_VP)]),
+    "dgswe_destroy": (None, [_VP]),
+    "dgswe_state_elems": (ctypes.c_int64, [_VP]),
+    "dgswe_rhs": (_I, [_VP, _VP, _VP, _VP]),
+    "dgswe_stage": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _VP]),
+    "dgswe_stage_rows": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _I, _I, _VP]),
+    "dgswe_axpy": (_I, [_VP, _D, _VP, _VP, _I, _I, _VP]),
+    "dgswe_ssprk3": (_I, [_VP, _VP, _VP, _VP, _D, _I, _I, _VP]),
+    "dgswe_alpha_prepass": (_I, [_VP, _VP, _VP]),
+    "dgswe_alpha_buffer": (_VP, [_VP]),
+    "dgswe_set_external_alpha": (_I, [_VP, _I]),
+    "dgswe_status": (_I, [_VP, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int32),
+                          _I, _VP]),
+    "dgswe_launch_count": (ctypes.c_int64, [_VP]),
+}
+
+_lib = None
+
+
+class DGSWEError(RuntimeError):
+    """A C-ABI call failed (message from dgswe_last_error)."""
+
+
+def load():
+    """Load (once) the in-tree library; raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DGSWEError(
+                f"{LIB_PATH} not found: build the CUDA library first "
+                "(python -c 'import __graft_entry__ as g; g.build()')")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.dgswe_abi_version() != 1:
+            raise DGSWEError("libdgswe_b200.so ABI version mismatch")
+        _lib = lib
+    return _lib
+
+
+def check(rc: int, what: str):
+    if rc != 0:
+        msg = load().dgswe_last_error()
+        raise DGSWEError(f"{what} failed ({rc}): {msg.decode() if msg else ''}")

@@ -1,0 +1,527 @@
+// dgswe_b200.cu -- C ABI (include/dgswe_b200.h) over the sm_100a fp64 DG
+// shallow-water kernels in dgswe_kernels.cuh.
+//
+// The context owns only constant tables (uploaded once, as the reference
+// precomputes on the host, dg.py:186-219), a status word, the global-alpha
+// buffer and cached CUDA graphs; all state buffers belong to the caller.
+
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/dgswe_b200.h"
+#include "dgswe_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (expr);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(DGSWE_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                         \
+    } while (0)
+
+struct DevStatus {
+    unsigned flags;
+    int first_tag;
+};
+
+// global-mode alpha: max over all traces (dg.py:389-411, models.py:271-280)
+template <int P>
+__global__ void alpha_prepass_kernel(const double *__restrict__ X, long long zstride,
+                                     long long rstride, int nx, int ny, int row0, int jlo, int jhi,
+                                     const double *__restrict__ cos_edge, double inv_r, double gravity,
+                                     double h_floor, double *out)
+{
+    constexpr int N = P + 1;
+    constexpr int NP = N * N;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int jl = jlo + blockIdx.y;
+    if (i >= nx || jl >= jhi) return;
+    const double *base = X + (size_t)blockIdx.z * zstride + (size_t)jl * rstride;
+    const int jg = row0 + jl;
+    double tr[4][3][N];   // L R B T
+    for (int v = 0; v < 3; ++v) {
+        double c[N][N];
+        for (int a = 0; a < N; ++a)
+            for (int b = 0; b < N; ++b) c[a][b] = base[(size_t)(v * NP + a * N + b) * nx + i];
+        for (int q = 0; q < N; ++q) {
+            double l = 0, r = 0, bo = 0, t = 0;
+            for (int a = 0; a < N; ++a) {
+                double ta = 0, sb = 0, st = 0;
+                for (int b = 0; b < N; ++b) {
+                    ta = fma(c[a][b], dgswe::c_tab[P][0][b][q], ta);
+                    sb = fma((b & 1) ? -1.0 : 1.0, c[a][b], sb);
+                    st += c[a][b];
+                }
+                r += ta;
+                l = fma((a & 1) ? -1.0 : 1.0, ta, l);
+                bo = fma(dgswe::c_tab[P][0][a][q], sb, bo);
+                t = fma(dgswe::c_tab[P][0][a][q], st, t);
+            }
+            tr[0][v][q] = l;
+            tr[1][v][q] = r;
+            tr[2][v][q] = bo;
+            tr[3][v][q] = t;
+        }
+    }
+    double ax = 0.0, ay = 0.0;
+    for (int e = 0; e < 4; ++e)
+        for (int q = 0; q < N; ++q) {
+            const double h = tr[e][0][q];
+            const double m = tr[e][e < 2 ? 1 : 2][q];
+            const double a = (fabs(m / fmax(h, h_floor)) + sqrt(gravity * fmax(h, 0.0))) * inv_r;
+            if (e < 2)
+                ax = fmax(ax, a);
+            else
+                ay = fmax(ay, a * cos_edge[jg + (e == 3 ? 1 : 0)]);
+        }
+    atomicMax(reinterpret_cast<unsigned long long *>(out), (unsigned long long)__double_as_longlong(ax));
+    atomicMax(reinterpret_cast<unsigned long long *>(out + 1),
+              (unsigned long long)__double_as_longlong(ay));
+}
+
+// y = y + x*coef with two roundings (timestep.py:137-141)
+__global__ void axpy_kernel(const double *__restrict__ x, double *__restrict__ y, double coef,
+                            long long zstride, long long off, long long count, int check,
+                            DevStatus *st, int tag)
+{
+    const double *xz = x + (size_t)blockIdx.y * zstride + off;
+    double *yz = y + (size_t)blockIdx.y * zstride + off;
+    bool bad = false;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+         k += (long long)gridDim.x * blockDim.x) {
+        const double t = __dmul_rn(xz[k], coef);
+        const double r = __dadd_rn(yz[k], t);
+        yz[k] = r;
+        if (check && !isfinite(r)) bad = true;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) {
+        atomicOr(&st->flags, DGSWE_STATUS_NONFINITE);
+        atomicMin(&st->first_tag, tag);
+    }
+}
+
+}  // namespace
+
+struct GraphKey {
+    double *u, *w1, *w2;
+    double dt;
+    int nsteps, check_mean;
+    bool operator<(const GraphKey &o) const
+    {
+        return std::tie(u, w1, w2, dt, nsteps, check_mean) <
+               std::tie(o.u, o.w1, o.w2, o.dt, o.nsteps, o.check_mean);
+    }
+};
+
+struct dgswe_ctx {
+    dgswe_cfg cfg;
+    int n, nphi, rc;
+    long long rstride, zstride;
+    double *rowtab = nullptr;     // device, ny * row_stride(p)
+    double *cos_edge = nullptr;   // device, ny+1
+    double *alpha = nullptr;      // device, 2 doubles
+    DevStatus *status = nullptr;  // device
+    int external_alpha = 0;
+    long long launches = 0;
+    int device = 0;
+    std::map<GraphKey, cudaGraphExec_t> graphs;
+    // derived scalars
+    double inv_r, inv_r_cx, half_g, bdx, bdy;
+};
+
+namespace {
+
+template <int P>
+int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, cudaStream_t s)
+{
+    using SM = dgswe::Smem<P>;
+    const int rows = r1 - r0;
+    if (rows <= 0) return DGSWE_OK;
+    const size_t smem = (size_t)SM::total(kp.rc) * sizeof(double);
+    static bool attr_set[64] = {};
+    int dev = c->device;
+    if (!attr_set[dev & 63]) {
+        CUDA_TRY(cudaFuncSetAttribute(dgswe::stage_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(SM::total(32) * sizeof(double))));
+        attr_set[dev & 63] = true;
+    }
+    dim3 grid((c->cfg.nx + dgswe::kOwned - 1) / dgswe::kOwned, (rows + kp.rc - 1) / kp.rc, c->cfg.nz);
+    dgswe::stage_kernel<P><<<grid, dgswe::kThreads, smem, s>>>(kp);
+    CUDA_TRY(cudaGetLastError());
+    c->launches += 1;
+    return DGSWE_OK;
+}
+
+int launch_stage(dgswe_ctx *c, double a, const double *U, double b, const double *X, double g,
+                 double *Y, int tag, int r0, int r1, int check_finite, int check_mean,
+                 cudaStream_t s)
+{
+    if (!X || !Y) return fail(DGSWE_EINVAL, "null state pointer");
+    if (X == Y) return fail(DGSWE_EINVAL, "output must not alias the stage input");
+    if (a != 0.0 && !U) return fail(DGSWE_EINVAL, "U is required when a != 0");
+    if (r0 < c->cfg.jlo || r1 > c->cfg.jhi || r0 > r1)
+        return fail(DGSWE_EINVAL, "row range [%d,%d) outside [%d,%d)", r0, r1, c->cfg.jlo, c->cfg.jhi);
+    dgswe::StageParams kp;
+    kp.X = X;
+    kp.U = (a != 0.0) ? U : nullptr;
+    kp.Y = Y;
+    kp.zstride = c->zstride;
+    kp.rstride = c->rstride;
+    kp.nx = c->cfg.nx;
+    kp.ny = c->cfg.ny;
+    kp.row0 = c->cfg.row0;
+    kp.nrows = c->cfg.nrows;
+    kp.j_begin = r0;
+    kp.j_end = r1;
+    kp.rc = c->rc;
+    kp.a = a;
+    kp.b = b;
+    kp.g = g;
+    kp.rowtab = c->rowtab;
+    kp.inv_r = c->inv_r;
+    kp.inv_r_cx = c->inv_r_cx;
+    kp.gravity = c->cfg.gravity;
+    kp.half_g = c->half_g;
+    kp.h_floor = c->cfg.h_floor;
+    kp.bdx = c->bdx;
+    kp.bdy = c->bdy;
+    kp.alpha_mode = c->cfg.alpha_mode;
+    kp.alpha = c->cfg.alpha;
+    kp.alpha_dev = c->alpha;
+    kp.status = &c->status->flags;
+    kp.first_tag = &c->status->first_tag;
+    kp.tag = tag;
+    kp.check_finite = check_finite;
+    kp.check_mean = check_mean;
+    if (c->cfg.alpha_mode == DGSWE_ALPHA_GLOBAL && !c->external_alpha) {
+        int rc = dgswe_alpha_prepass(c, X, s);
+        if (rc) return rc;
+    }
+    switch (c->cfg.p) {
+    case 0: return launch_stage_p<0>(c, kp, r0, r1, s);
+    case 1: return launch_stage_p<1>(c, kp, r0, r1, s);
+    case 2: return launch_stage_p<2>(c, kp, r0, r1, s);
+    case 3: return launch_stage_p<3>(c, kp, r0, r1, s);
+    case 4: return launch_stage_p<4>(c, kp, r0, r1, s);
+    case 5: return launch_stage_p<5>(c, kp, r0, r1, s);
+    case 6: return launch_stage_p<6>(c, kp, r0, r1, s);
+    default: return fail(DGSWE_EUNSUPPORTED, "degree p=%d not supported (0..6)", c->cfg.p);
+    }
+}
+
+template <int P>
+int launch_alpha_p(dgswe_ctx *c, const double *X, cudaStream_t s)
+{
+    const int rows = c->cfg.jhi - c->cfg.jlo;
+    dim3 grid((c->cfg.nx + 127) / 128, rows, c->cfg.nz);
+    alpha_prepass_kernel<P><<<grid, 128, 0, s>>>(X, c->zstride, c->rstride, c->cfg.nx, c->cfg.ny,
+                                                   c->cfg.row0, c->cfg.jlo, c->cfg.jhi, c->cos_edge,
+                                                   c->inv_r, c->cfg.gravity, c->cfg.h_floor, c->alpha);
+    CUDA_TRY(cudaGetLastError());
+    c->launches += 1;
+    return DGSWE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dgswe_abi_version(void) { return DGSWE_ABI_VERSION; }
+
+const char *dgswe_last_error(void) { return g_last_error.c_str(); }
+
+int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
+{
+    if (!cfg || !t || !out) return fail(DGSWE_EINVAL, "null argument");
+    *out = nullptr;
+    const dgswe_cfg &c = *cfg;
+    if (c.p < 0 || c.p > dgswe::kMaxP) return fail(DGSWE_EUNSUPPORTED, "degree p=%d not supported (0..6)", c.p);
+    if (c.nx < 1 || c.ny < 1 || c.nz < 1) return fail(DGSWE_EINVAL, "element counts must be >= 1");
+    if (c.nrows < 1 || c.jlo < 0 || c.jhi > c.nrows || c.jlo >= c.jhi)
+        return fail(DGSWE_EINVAL, "bad local rows: nrows=%d jlo=%d jhi=%d", c.nrows, c.jlo, c.jhi);
+    if (c.row0 + c.jlo < 0 || c.row0 + c.jhi > c.ny) return fail(DGSWE_EINVAL, "band outside the sphere");
+    if (c.row0 + c.jlo > 0 && c.jlo < 1) return fail(DGSWE_EINVAL, "band needs a southern halo row");
+    if (c.row0 + c.jhi < c.ny && c.jhi >= c.nrows) return fail(DGSWE_EINVAL, "band needs a northern halo row");
+    if (c.alpha_mode < 0 || c.alpha_mode > 2) return fail(DGSWE_EINVAL, "bad alpha mode");
+    if (!(c.radius > 0) || !(c.gravity > 0) || !(c.dx > 0) || !(c.dy > 0))
+        return fail(DGSWE_EINVAL, "radius, gravity, dx, dy must be positive");
+    if (!t->leg || !t->dleg || !t->weights || !t->cos_r_int || !t->sin_r_int || !t->fcos_int ||
+        !t->cos_r_edge || !t->cos_edge || !t->minv)
+        return fail(DGSWE_EINVAL, "missing table");
+
+    dgswe_ctx *ctx = new (std::nothrow) dgswe_ctx();
+    if (!ctx) return fail(DGSWE_ENOMEM, "out of host memory");
+    ctx->cfg = c;
+    const int n = c.p + 1;
+    ctx->n = n;
+    ctx->nphi = n * n;
+    ctx->rstride = 3LL * ctx->nphi * c.nx;
+    ctx->zstride = ctx->rstride * c.nrows;
+    cudaGetDevice(&ctx->device);
+
+    // mesh scalars exactly as the reference forms them (mesh.py:66-84)
+    const double determ = c.dx * c.dy / 4.0;
+    ctx->bdx = c.dx / 2.0;
+    ctx->bdy = c.dy / 2.0;
+    const double cx = determ / ctx->bdx;   // volx factor (dg.py:199-200)
+    const double cy = determ / ctx->bdy;   // voly factor (dg.py:201-202)
+    const double cs = determ;              // src factor (dg.py:213)
+    ctx->inv_r = 1.0 / c.radius;
+    ctx->inv_r_cx = ctx->inv_r * cx;
+    ctx->half_g = 0.5 * c.gravity;
+
+    // automatic rows per CTA: aim for >= ~8 CTAs of 96 threads per SM
+    if (c.row_chunk > 0) {
+        ctx->rc = c.row_chunk;
+    } else {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        const long long strips = (c.nx + dgswe::kOwned - 1) / dgswe::kOwned;
+        const long long rows = c.jhi - c.jlo;
+        long long rc = strips * rows * c.nz / ((long long)sms * 8);
+        if (const char *env = getenv("DGSWE_ROW_CHUNK")) rc = atoi(env);
+        ctx->rc = (int)(rc < 2 ? 2 : (rc > 16 ? 16 : rc));
+    }
+    if (ctx->rc > 32) ctx->rc = 32;
+
+    // constant tables for this degree
+    static double tab[4][dgswe::kMaxP + 1][dgswe::kMaxP + 1];
+    memset(tab, 0, sizeof tab);
+    for (int a = 0; a < n; ++a)
+        for (int q = 0; q < n; ++q) {
+            const double P = t->leg[a * n + q], D = t->dleg[a * n + q], w = t->weights[q];
+            tab[0][a][q] = P;
+            tab[1][a][q] = D;
+            tab[2][a][q] = w * P;
+            tab[3][a][q] = w * D;
+        }
+    cudaError_t e = cudaMemcpyToSymbol(dgswe::c_tab, tab, sizeof tab, sizeof tab * c.p);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return fail(DGSWE_ECUDA, "constant upload: %s", cudaGetErrorString(e));
+    }
+
+    // per-row tables (global rows), layout RowLayout<P>
+    const int rs = dgswe::row_stride(c.p);
+    std::vector<double> rt((size_t)c.ny * rs);
+    for (int j = 0; j < c.ny; ++j) {
+        double *r = rt.data() + (size_t)j * rs;
+        for (int q = 0; q < n; ++q) {
+            r[q] = t->cos_r_int[j * n + q] * cy;
+            r[n + q] = t->sin_r_int[j * n + q] * cs;
+            r[2 * n + q] = t->fcos_int[j * n + q] * cs;
+        }
+        r[3 * n] = t->cos_r_edge[j];
+        r[3 * n + 1] = t->cos_edge[j];
+        const double *M = t->minv + (size_t)j * ctx->nphi * ctx->nphi;
+        for (int b = 0; b < n; ++b)
+            for (int bb = 0; bb < n; ++bb) r[3 * n + 2 + b * n + bb] = M[(size_t)b * ctx->nphi + bb];
+    }
+    bool ok = cudaMalloc(&ctx->rowtab, rt.size() * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&ctx->cos_edge, (c.ny + 1) * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&ctx->alpha, 2 * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&ctx->status, sizeof(DevStatus)) == cudaSuccess;
+    if (ok) {
+        DevStatus st0 = {0u, INT_MAX};
+        ok = cudaMemcpy(ctx->rowtab, rt.data(), rt.size() * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess &&
+             cudaMemcpy(ctx->cos_edge, t->cos_edge, (c.ny + 1) * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess &&
+             cudaMemset(ctx->alpha, 0, 2 * sizeof(double)) == cudaSuccess &&
+             cudaMemcpy(ctx->status, &st0, sizeof st0, cudaMemcpyHostToDevice) == cudaSuccess;
+    }
+    if (!ok) {
+        cudaError_t le = cudaGetLastError();
+        dgswe_destroy(ctx);
+        return fail(DGSWE_ECUDA, "device allocation/upload failed: %s", cudaGetErrorString(le));
+    }
+    *out = ctx;
+    return DGSWE_OK;
+}
+
+void dgswe_destroy(dgswe_ctx *ctx)
+{
+    if (!ctx) return;
+    for (auto &kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+    cudaFree(ctx->rowtab);
+    cudaFree(ctx->cos_edge);
+    cudaFree(ctx->alpha);
+    cudaFree(ctx->status);
+    delete ctx;
+}
+
+int64_t dgswe_state_elems(const dgswe_ctx *ctx)
+{
+    return ctx ? (int64_t)ctx->zstride * ctx->cfg.nz : 0;
+}
+
+int dgswe_rhs(dgswe_ctx *ctx, const double *X, double *K, void *stream)
+{
+    if (!ctx) return fail(DGSWE_EINVAL, "null context");
+    return launch_stage(ctx, 0.0, nullptr, 0.0, X, 1.0, K, 0, ctx->cfg.jlo, ctx->cfg.jhi, 0, 0,
+                        (cudaStream_t)stream);
+}
+
+int dgswe_stage(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g,
+                double *Y, int tag, void *stream)
+{
+    if (!ctx) return fail(DGSWE_EINVAL, "null context");
+    return launch_stage(ctx, a, U, b, X, g, Y, tag, ctx->cfg.jlo, ctx->cfg.jhi, 0, 0,
+                        (cudaStream_t)stream);
+}
+
+int dgswe_stage_rows(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g,
+                     double *Y, int tag, int r0, int r1, void *stream)
+{
+    if (!ctx) return fail(DGSWE_EINVAL, "null context");
+    return launch_stage(ctx, a, U, b, X, g, Y, tag, r0, r1, 0, 0, (cudaStream_t)stream);
+}
+
+int dgswe_axpy(dgswe_ctx *ctx, double coef, const double *x, double *y, int check_finite, int tag,
+               void *stream)
+{
+    if (!ctx || !x || !y) return fail(DGSWE_EINVAL, "null argument");
+    const long long off = (long long)ctx->cfg.jlo * ctx->rstride;
+    const long long count = (long long)(ctx->cfg.jhi - ctx->cfg.jlo) * ctx->rstride;
+    long long blocks = (count + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    dim3 grid((unsigned)blocks, ctx->cfg.nz);
+    axpy_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(x, y, coef, ctx->zstride, off, count,
+                                                       check_finite, ctx->status, tag);
+    CUDA_TRY(cudaGetLastError());
+    ctx->launches += 1;
+    return DGSWE_OK;
+}
+
+int dgswe_alpha_prepass(dgswe_ctx *ctx, const double *X, void *stream)
+{
+    if (!ctx || !X) return fail(DGSWE_EINVAL, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    CUDA_TRY(cudaMemsetAsync(ctx->alpha, 0, 2 * sizeof(double), s));
+    switch (ctx->cfg.p) {
+    case 0: return launch_alpha_p<0>(ctx, X, s);
+    case 1: return launch_alpha_p<1>(ctx, X, s);
+    case 2: return launch_alpha_p<2>(ctx, X, s);
+    case 3: return launch_alpha_p<3>(ctx, X, s);
+    case 4: return launch_alpha_p<4>(ctx, X, s);
+    case 5: return launch_alpha_p<5>(ctx, X, s);
+    case 6: return launch_alpha_p<6>(ctx, X, s);
+    default: return fail(DGSWE_EUNSUPPORTED, "degree not supported");
+    }
+}
+
+double *dgswe_alpha_buffer(dgswe_ctx *ctx) { return ctx ? ctx->alpha : nullptr; }
+
+int dgswe_set_external_alpha(dgswe_ctx *ctx, int external)
+{
+    if (!ctx) return fail(DGSWE_EINVAL, "null context");
+    ctx->external_alpha = external ? 1 : 0;
+    return DGSWE_OK;
+}
+
+static int enqueue_ssprk3(dgswe_ctx *ctx, double *u, double *w1, double *w2, double dt, int nsteps,
+                          int check_mean, cudaStream_t s)
+{
+    const int lo = ctx->cfg.jlo, hi = ctx->cfg.jhi;
+    for (int k = 0; k < nsteps; ++k) {
+        // Shu-Osher SSPRK3 == tableau(3) of timestep.py:65-70
+        int rc = launch_stage(ctx, 0.0, nullptr, 1.0, u, dt, w1, k, lo, hi, 0, 0, s);
+        if (!rc) rc = launch_stage(ctx, 0.75, u, 0.25, w1, 0.25 * dt, w2, k, lo, hi, 0, 0, s);
+        if (!rc) rc = launch_stage(ctx, 1.0 / 3.0, u, 2.0 / 3.0, w2, (2.0 / 3.0) * dt, u, k, lo, hi, 1,
+                                   check_mean, s);
+        if (rc) return rc;
+    }
+    return DGSWE_OK;
+}
+
+int dgswe_ssprk3(dgswe_ctx *ctx, double *u, double *w1, double *w2, double dt, int nsteps,
+                 int check_mean, void *stream)
+{
+    if (!ctx || !u || !w1 || !w2) return fail(DGSWE_EINVAL, "null argument");
+    if (nsteps < 0) return fail(DGSWE_EINVAL, "nsteps must be >= 0");
+    if (nsteps == 0) return DGSWE_OK;
+    if (ctx->cfg.jlo != 0 || ctx->cfg.jhi != ctx->cfg.ny || ctx->cfg.row0 != 0)
+        return fail(DGSWE_EINVAL, "dgswe_ssprk3 needs a single-band context; use dgswe_stage per band");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (getenv("DGSWE_NO_GRAPH")) return enqueue_ssprk3(ctx, u, w1, w2, dt, nsteps, check_mean, s);
+    GraphKey key{u, w1, w2, dt, nsteps, check_mean};
+    auto it = ctx->graphs.find(key);
+    if (it == ctx->graphs.end()) {
+        if (ctx->graphs.size() >= 8) {
+            for (auto &kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+            ctx->graphs.clear();
+        }
+        cudaStream_t cap = s;
+        bool own = false;
+        if (cap == nullptr) {   // legacy stream cannot be captured
+            CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+            own = true;
+        }
+        CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        const long long before = ctx->launches;
+        int rc = enqueue_ssprk3(ctx, u, w1, w2, dt, nsteps, check_mean, cap);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(cap, &graph);
+        ctx->launches = before;   // counted at replay
+        if (own) cudaStreamDestroy(cap);
+        if (rc) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        if (e != cudaSuccess) return fail(DGSWE_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+        cudaGraphExec_t exec = nullptr;
+        e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return fail(DGSWE_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+        it = ctx->graphs.emplace(key, exec).first;
+    }
+    CUDA_TRY(cudaGraphLaunch(it->second, s));
+    const int per_stage = 1 + (ctx->cfg.alpha_mode == DGSWE_ALPHA_GLOBAL ? 1 : 0);
+    ctx->launches += 3LL * nsteps * per_stage;
+    return DGSWE_OK;
+}
+
+int dgswe_status(dgswe_ctx *ctx, uint32_t *flags, int32_t *first_tag, int reset, void *stream)
+{
+    if (!ctx) return fail(DGSWE_EINVAL, "null context");
+    cudaStream_t s = (cudaStream_t)stream;
+    DevStatus h;
+    CUDA_TRY(cudaMemcpyAsync(&h, ctx->status, sizeof h, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (flags) *flags = h.flags;
+    if (first_tag) *first_tag = h.first_tag;
+    if (reset) {
+        DevStatus st0 = {0u, INT_MAX};
+        CUDA_TRY(cudaMemcpyAsync(ctx->status, &st0, sizeof st0, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    return DGSWE_OK;
+}
+
+int64_t dgswe_launch_count(const dgswe_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

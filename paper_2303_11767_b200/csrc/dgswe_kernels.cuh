@@ -1,0 +1,512 @@
+// dgswe_kernels.cuh -- fused fp64 DG shallow-water stage kernel for sm_100a.
+//
+// One CTA = 3 warps (warp v owns variable v in {h, hu, hv}) x 32 lanes.
+// Lane l holds longitude element i0-1+l (mod nx) of a 30-element strip:
+// lanes 1..30 own their element, lanes 0 and 31 are the periodic/strip halo
+// whose traces feed the strip's two border faces.  The CTA marches north
+// through a chunk of latitude rows; every y-face is evaluated once per
+// chunk, every x-face once per strip.
+//
+// Per row, per variable and lane (n = p+1, all tensor contractions
+// sum-factorised and held in registers, constants from __constant__):
+//   1. modal -> nodal: t[a][qj] = sum_b c[a][b] P_b(x_qj),
+//      U[qi][qj] = sum_a P_a(x_qi) t[a][qj]; traces L/R from t, T/B from
+//      sum_b c[a][b](+-1)^b                          (dg.py:348-357)
+//   2. nodal values exchanged through shared memory; pointwise flux /
+//      source physics for this warp's variable      (models.py:161-252)
+//   3. face warps: Rusanov flux with local alpha    (dg.py:92-119,385-453)
+//   4. volume + source projection, boundary lifts, per-row inverse mass
+//      (Kronecker block form), fused RK stage update (dg.py:455-502,
+//      timestep.py:132-167)
+//
+// Floating point: FMA contraction and reciprocal-multiply are used; results
+// agree with the reference (exact-order oracle) to ~1e-15 relative per RHS
+// up to the reference's own conditioning (see tests/test_gpu_parity.py).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dgswe {
+
+constexpr int kMaxP = 6;
+constexpr int kLanes = 32;
+constexpr int kOwned = 30;   // owned elements per strip (lanes 1..30)
+constexpr int kWarps = 3;    // one per conserved variable
+constexpr int kThreads = kWarps * kLanes;
+
+// [p][table][a][q]: 0 P_a(x_q), 1 P'_a(x_q), 2 w_q P_a(x_q), 3 w_q P'_a(x_q)
+__constant__ double c_tab[kMaxP + 1][4][kMaxP + 1][kMaxP + 1];
+
+struct StageParams {
+    const double *X;      // stage input (level 0, buffer row 0)
+    const double *U;      // u^n for the combination (may be null when a == 0)
+    double *Y;            // output
+    long long zstride;    // doubles per level
+    long long rstride;    // doubles per buffer row (3 * nphi * nx)
+    int nx, ny, row0, nrows;
+    int j_begin, j_end, rc;   // local rows [j_begin, j_end), rc rows per CTA
+    double a, b, g;       // Y = a U + b X + g RHS(X)
+    const double *rowtab; // per global row, see row_stride()
+    double inv_r;         // 1/R
+    double inv_r_cx;      // (1/R) * determ/bd_det_x
+    double gravity, half_g, h_floor;
+    double bdx, bdy;      // bd_det_x, bd_det_y
+    int alpha_mode;       // 0 local, 1 pinned, 2 global (from alpha_dev)
+    double alpha;
+    const double *alpha_dev;
+    unsigned *status;
+    int *first_tag;
+    int tag;
+    int check_finite;
+    int check_mean;
+};
+
+// per-row table layout (doubles): crc[n] srs[n] fcs[n] cr_b cos_b T[n][n]
+template <int P>
+struct RowLayout {
+    static constexpr int N = P + 1;
+    static constexpr int CRC = 0;
+    static constexpr int SRS = N;
+    static constexpr int FCS = 2 * N;
+    static constexpr int CRB = 3 * N;
+    static constexpr int COSB = 3 * N + 1;
+    static constexpr int T = 3 * N + 2;
+    static constexpr int STRIDE = 3 * N + 2 + N * N;
+};
+
+__host__ __device__ inline int row_stride(int p) { return 3 * (p + 1) + 2 + (p + 1) * (p + 1); }
+
+#define LEG(a, q) c_tab[P][0][a][q]
+#define WP(a, q) c_tab[P][2][a][q]
+#define WD(a, q) c_tab[P][3][a][q]
+
+template <int P>
+struct Smem {
+    static constexpr int N = P + 1;
+    static constexpr int NP = N * N;
+    // offsets in doubles
+    static constexpr int U = 0;                          // [3][NP][32]
+    static constexpr int XL = U + 3 * NP * kLanes;       // [3][N][32]
+    static constexpr int XR = XL + 3 * N * kLanes;
+    static constexpr int TT = XR + 3 * N * kLanes;       // top traces of current row
+    static constexpr int BB = TT + 3 * N * kLanes;       // bottom traces of next row
+    static constexpr int FX = BB + 3 * N * kLanes;       // x-face flux, right face of lane
+    static constexpr int FY0 = FX + 3 * N * kLanes;      // y-face flux buffers
+    static constexpr int FY1 = FY0 + 3 * N * kLanes;
+    static constexpr int ROW = FY1 + 3 * N * kLanes;     // row tables
+    static __host__ __device__ constexpr int total(int rc) {
+        return ROW + (rc + 1) * RowLayout<P>::STRIDE;
+    }
+};
+
+__device__ __forceinline__ double sgn(int k) { return (k & 1) ? -1.0 : 1.0; }
+
+template <int P>
+__device__ __forceinline__ void load_tile(double (&c)[P + 1][P + 1], const double *__restrict__ src,
+                                          int nx, int i)
+{
+    constexpr int N = P + 1;
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int b = 0; b < N; ++b) c[a][b] = __ldg(src + (size_t)(a * N + b) * nx + i);
+}
+
+// bottom (sign -1) or top (sign +1) trace at the n edge nodes from modes
+template <int P, bool TOP>
+__device__ __forceinline__ void ytrace(const double (&c)[P + 1][P + 1], double (&tr)[P + 1])
+{
+    constexpr int N = P + 1;
+    double s[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+        double acc = c[a][0];
+#pragma unroll
+        for (int b = 1; b < N; ++b) acc = TOP ? acc + c[a][b] : fma(sgn(b), c[a][b], acc);
+        s[a] = acc;
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < N; ++a) acc = fma(LEG(a, q), s[a], acc);
+        tr[q] = acc;
+    }
+}
+
+// Interior nodal values and L/R/T traces of one variable -> shared memory.
+template <int P>
+__device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], double *sU, double *sXL,
+                                             double *sXR, double *sT, int lane, bool check)
+{
+    constexpr int N = P + 1;
+    unsigned bad = 0;
+    double t[N][N];
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            double acc = 0.0;
+#pragma unroll
+            for (int b = 0; b < N; ++b) acc = fma(c[a][b], LEG(b, q), acc);
+            t[a][q] = acc;
+        }
+#pragma unroll
+    for (int qi = 0; qi < N; ++qi)
+#pragma unroll
+        for (int qj = 0; qj < N; ++qj) {
+            double acc = 0.0;
+#pragma unroll
+            for (int a = 0; a < N; ++a) acc = fma(LEG(a, qi), t[a][qj], acc);
+            sU[(qi * N + qj) * kLanes + lane] = acc;
+            if (check) bad |= !(acc > 0.0);
+        }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+        double l = t[0][q], r = t[0][q];
+#pragma unroll
+        for (int a = 1; a < N; ++a) {
+            r += t[a][q];
+            l = fma(sgn(a), t[a][q], l);
+        }
+        sXL[q * kLanes + lane] = l;
+        sXR[q * kLanes + lane] = r;
+        if (check) bad |= !(l > 0.0) | !(r > 0.0);
+    }
+    double tt[N];
+    ytrace<P, true>(c, tt);
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+        sT[q * kLanes + lane] = tt[q];
+        if (check) bad |= !(tt[q] > 0.0);
+    }
+    return bad;
+}
+
+// Rusanov flux over one face: "in" = lower/left element, "out" = upper/right.
+// DIR 0: x-face, physical flux F, alpha = (|u|+c)/R.
+// DIR 1: y-face, physical flux G = cos/R * (...), alpha = cos (|v|+c)/R.
+template <int P, int DIR>
+__device__ __forceinline__ void face_flux(const double *sIn, int lin, const double *sOut, int lout,
+                                          double *sF, int lane, const StageParams &kp,
+                                          double cr_e, double cos_e, double alpha_glob)
+{
+    constexpr int N = P + 1;
+    double rin[N], rout[N];
+    double amax = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const double hi = sIn[(0 * N + k) * kLanes + lin];
+        const double mi = sIn[((DIR == 0 ? 1 : 2) * N + k) * kLanes + lin];
+        const double ho = sOut[(0 * N + k) * kLanes + lout];
+        const double mo = sOut[((DIR == 0 ? 1 : 2) * N + k) * kLanes + lout];
+        rin[k] = 1.0 / fmax(hi, kp.h_floor);
+        rout[k] = 1.0 / fmax(ho, kp.h_floor);
+        const double ci = sqrt(kp.gravity * fmax(hi, 0.0));
+        const double co = sqrt(kp.gravity * fmax(ho, 0.0));
+        double ai = (fabs(mi * rin[k]) + ci) * kp.inv_r;
+        double ao = (fabs(mo * rout[k]) + co) * kp.inv_r;
+        if (DIR == 1) {
+            ai *= cos_e;
+            ao *= cos_e;
+        }
+        amax = fmax(amax, fmax(ai, ao));
+    }
+    const double alpha = (kp.alpha_mode == 0) ? amax : alpha_glob;
+    const double ha = 0.5 * alpha;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const double hi = sIn[(0 * N + k) * kLanes + lin];
+        const double ui = sIn[(1 * N + k) * kLanes + lin];
+        const double vi = sIn[(2 * N + k) * kLanes + lin];
+        const double ho = sOut[(0 * N + k) * kLanes + lout];
+        const double uo = sOut[(1 * N + k) * kLanes + lout];
+        const double vo = sOut[(2 * N + k) * kLanes + lout];
+        const double gi = hi * hi * kp.half_g, go = ho * ho * kp.half_g;
+        double fi0, fi1, fi2, fo0, fo1, fo2, sc;
+        if (DIR == 0) {
+            const double ui_ = ui * rin[k], vi_ = vi * rin[k];
+            const double uo_ = uo * rout[k], vo_ = vo * rout[k];
+            fi0 = ui; fi1 = fma(ui, ui_, gi); fi2 = ui * vi_;
+            fo0 = uo; fo1 = fma(uo, uo_, go); fo2 = uo * vo_;
+            sc = kp.inv_r;
+        } else {
+            const double vi_ = vi * rin[k], vo_ = vo * rout[k];
+            fi0 = vi; fi1 = ui * vi_; fi2 = fma(vi, vi_, gi);
+            fo0 = vo; fo1 = uo * vo_; fo2 = fma(vo, vo_, go);
+            sc = cr_e;
+        }
+        const double hs = 0.5 * sc;
+        sF[(0 * N + k) * kLanes + lane] = fma(hs, fi0 + fo0, -ha * (ho - hi));
+        sF[(1 * N + k) * kLanes + lane] = fma(hs, fi1 + fo1, -ha * (uo - ui));
+        sF[(2 * N + k) * kLanes + lane] = fma(hs, fi2 + fo2, -ha * (vo - vi));
+    }
+}
+
+// Volume + source projection of variable V at the current row.
+// vol[a][b] = sum_q (cx dphi/dxi F + cy dphi/deta G + cs phi S)[q]
+template <int P, int V>
+__device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], const double *sU, const double *row,
+                                       int lane, const StageParams &kp)
+{
+    constexpr int N = P + 1;
+    constexpr int NP = N * N;
+    using RL = RowLayout<P>;
+    double rF[N][N], rG[N][N];   // [qi][b]
+#pragma unroll
+    for (int qi = 0; qi < N; ++qi) {
+        double F[N], G[N], S[N];
+#pragma unroll
+        for (int qj = 0; qj < N; ++qj) {
+            const int q = qi * N + qj;
+            const double h = sU[(0 * NP + q) * kLanes + lane];
+            const double hu = sU[(1 * NP + q) * kLanes + lane];
+            const double hv = sU[(2 * NP + q) * kLanes + lane];
+            const double crc = row[RL::CRC + qj];
+            if (V == 0) {
+                F[qj] = hu * kp.inv_r_cx;
+                G[qj] = hv * crc;
+                S[qj] = 0.0;
+            } else {
+                const double r = 1.0 / fmax(h, kp.h_floor);
+                const double u = hu * r, v = hv * r;
+                const double gh2 = h * h * kp.half_g;
+                const double t = fma(u, row[RL::SRS + qj], row[RL::FCS + qj]);
+                if (V == 1) {
+                    F[qj] = fma(hu, u, gh2) * kp.inv_r_cx;
+                    G[qj] = hu * v * crc;
+                    S[qj] = t * hv;
+                } else {
+                    F[qj] = hu * v * kp.inv_r_cx;
+                    G[qj] = fma(hv, v, gh2) * crc;
+                    S[qj] = -fma(gh2, row[RL::SRS + qj], t * hu);
+                }
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < N; ++b) {
+            double f = 0.0, g = 0.0;
+#pragma unroll
+            for (int qj = 0; qj < N; ++qj) {
+                f = fma(WP(b, qj), F[qj], f);
+                g = fma(WD(b, qj), G[qj], g);
+                if (V != 0) g = fma(WP(b, qj), S[qj], g);
+            }
+            rF[qi][b] = f;
+            rG[qi][b] = g;
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int b = 0; b < N; ++b) {
+            double acc = 0.0;
+#pragma unroll
+            for (int qi = 0; qi < N; ++qi) {
+                acc = fma(WD(a, qi), rF[qi][b], acc);
+                acc = fma(WP(a, qi), rG[qi][b], acc);
+            }
+            vol[a][b] = acc;
+        }
+}
+
+// Boundary lifts, inverse mass, stage combination and store for variable V.
+template <int P, int V>
+__device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const double *sFX,
+                                             const double *sFtop, const double *sFbot, bool has_top,
+                                             bool has_bot, const double *row, int lane, bool owned,
+                                             const double *__restrict__ Xv, const double *Uv,
+                                             double *Yv, int nx, int i,
+                                             const StageParams &kp)
+{
+    constexpr int N = P + 1;
+    using RL = RowLayout<P>;
+    const int ll = lane > 0 ? lane - 1 : 0;
+    double eR[N], eL[N], eT[N], eB[N];
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+        double r = 0.0, l = 0.0, t = 0.0, bo = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            r = fma(WP(b, k), sFX[(V * N + k) * kLanes + lane], r);
+            l = fma(WP(b, k), sFX[(V * N + k) * kLanes + ll], l);
+            if (has_top) t = fma(WP(b, k), sFtop[(V * N + k) * kLanes + lane], t);
+            if (has_bot) bo = fma(WP(b, k), sFbot[(V * N + k) * kLanes + lane], bo);
+        }
+        eR[b] = r * kp.bdy;
+        eL[b] = l * kp.bdy;
+        eT[b] = t * kp.bdx;
+        eB[b] = bo * kp.bdx;
+    }
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int b = 0; b < N; ++b)
+            vol[a][b] += (fma(sgn(a), eL[b], -eR[b]) + fma(sgn(b), eB[a], -eT[a]));
+    unsigned bad = 0;
+    const double *T = row + RL::T;
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+        const double ga = kp.g * (double)(2 * a + 1);
+#pragma unroll
+        for (int b = 0; b < N; ++b) {
+            double k = 0.0;
+#pragma unroll
+            for (int bb = 0; bb < N; ++bb) k = fma(T[b * N + bb], vol[a][bb], k);
+            const size_t off = (size_t)(a * N + b) * nx + i;
+            double y = ga * k;
+            if (kp.b != 0.0) y = fma(kp.b, __ldg(Xv + off), y);
+            if (kp.a != 0.0) y = fma(kp.a, Uv[off], y);
+            if (owned) {
+                Yv[off] = y;
+                if (kp.check_finite && !isfinite(y)) bad |= 2u;
+                if (V == 0 && kp.check_mean && a == 0 && b == 0 && !(y > 0.0)) bad |= 4u;
+            }
+        }
+    }
+    return bad;
+}
+
+template <int P>
+__global__ void __launch_bounds__(kThreads) stage_kernel(StageParams kp)
+{
+    constexpr int N = P + 1;
+    constexpr int NP = N * N;
+    using SM = Smem<P>;
+    using RL = RowLayout<P>;
+    extern __shared__ double smem[];
+    const int v = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nx = kp.nx;
+    const int i0 = blockIdx.x * kOwned;
+    int i = (i0 - 1 + lane) % nx;
+    if (i < 0) i += nx;
+    const int nown = min(kOwned, nx - i0);
+    const bool owned = lane >= 1 && lane <= nown;
+    const int jb = kp.j_begin + blockIdx.y * kp.rc;
+    const int je = min(jb + kp.rc, kp.j_end);
+    if (jb >= je) return;
+
+    double *sU = smem + SM::U;
+    double *sXL = smem + SM::XL;
+    double *sXR = smem + SM::XR;
+    double *sT = smem + SM::TT;
+    double *sB = smem + SM::BB;
+    double *sFX = smem + SM::FX;
+    double *sFa = smem + SM::FY0;
+    double *sFb = smem + SM::FY1;
+    double *sRow = smem + SM::ROW;
+
+    // row tables for global rows [row0+jb, min(row0+je, ny-1)]
+    const int gfirst = kp.row0 + jb;
+    const int glast = min(kp.row0 + je, kp.ny - 1);
+    for (int idx = threadIdx.x; idx < (glast - gfirst + 1) * RL::STRIDE; idx += kThreads)
+        sRow[idx] = kp.rowtab[(size_t)gfirst * RL::STRIDE + idx];
+
+    const double *Xz = kp.X + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx;
+    const double *Uz = kp.U ? kp.U + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx : nullptr;
+    double *Yz = kp.Y + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx;
+    const bool chk = (v == 0);
+    unsigned bad = 0;
+
+    double alpha_x = kp.alpha, alpha_y = kp.alpha;
+    if (kp.alpha_mode == 2) {
+        alpha_x = kp.alpha_dev[0];
+        alpha_y = kp.alpha_dev[1];
+    }
+
+    // prologue: bottom face of the chunk's first row
+    double cn[N][N];
+    const bool below = gfirst > 0;
+    if (below) {
+        load_tile<P>(cn, Xz + (size_t)(jb - 1) * kp.rstride, nx, i);
+        double tt[N];
+        ytrace<P, true>(cn, tt);
+#pragma unroll
+        for (int q = 0; q < N; ++q) sT[(v * N + q) * kLanes + lane] = tt[q];
+    }
+    load_tile<P>(cn, Xz + (size_t)jb * kp.rstride, nx, i);
+    {
+        double bt[N];
+        ytrace<P, false>(cn, bt);
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            sB[(v * N + q) * kLanes + lane] = bt[q];
+            if (chk) bad |= !(bt[q] > 0.0);
+        }
+    }
+    __syncthreads();
+    if (below && v == 1) {
+        const double *r = sRow;   // row jb: its bottom edge is the face latitude
+        face_flux<P, 1>(sT, lane, sB, lane, sFb, lane, kp, r[RL::CRB], r[RL::COSB], alpha_y);
+    }
+    __syncthreads();
+
+    for (int jl = jb; jl < je; ++jl) {
+        const int jg = kp.row0 + jl;
+        const bool has_top = jg + 1 < kp.ny;
+        const bool has_bot = jg > 0;
+        const double *row = sRow + (size_t)(jl - jb) * RL::STRIDE;
+        double c[N][N];
+#pragma unroll
+        for (int a = 0; a < N; ++a)
+#pragma unroll
+            for (int b = 0; b < N; ++b) c[a][b] = cn[a][b];
+        if (has_top) load_tile<P>(cn, Xz + (size_t)(jl + 1) * kp.rstride, nx, i);
+
+        bad |= eval_row<P>(c, sU + v * NP * kLanes, sXL + v * N * kLanes, sXR + v * N * kLanes,
+                           sT + v * N * kLanes, lane, chk);
+        if (has_top) {
+            double bt[N];
+            ytrace<P, false>(cn, bt);
+#pragma unroll
+            for (int q = 0; q < N; ++q) {
+                sB[(v * N + q) * kLanes + lane] = bt[q];
+                if (chk) bad |= !(bt[q] > 0.0);
+            }
+        }
+        __syncthreads();
+
+        double vol[N][N];
+        if (v == 0) {
+            face_flux<P, 0>(sXR, lane, sXL, min(lane + 1, 31), sFX, lane, kp, 0.0, 0.0, alpha_x);
+            volume<P, 0>(vol, sU, row, lane, kp);
+        } else if (v == 1) {
+            if (has_top) {
+                const double *rn = row + RL::STRIDE;   // row above: bottom edge = face
+                face_flux<P, 1>(sT, lane, sB, lane, sFa, lane, kp, rn[RL::CRB], rn[RL::COSB], alpha_y);
+            }
+            volume<P, 1>(vol, sU, row, lane, kp);
+        } else {
+            volume<P, 2>(vol, sU, row, lane, kp);
+        }
+        __syncthreads();
+
+        const size_t roff = (size_t)jl * kp.rstride;
+        if (v == 0)
+            bad |= finalize<P, 0>(vol, sFX, sFa, sFb, has_top, has_bot, row, lane, owned, Xz + roff,
+                                  Uz ? Uz + roff : nullptr, Yz + roff, nx, i, kp);
+        else if (v == 1)
+            bad |= finalize<P, 1>(vol, sFX, sFa, sFb, has_top, has_bot, row, lane, owned, Xz + roff,
+                                  Uz ? Uz + roff : nullptr, Yz + roff, nx, i, kp);
+        else
+            bad |= finalize<P, 2>(vol, sFX, sFa, sFb, has_top, has_bot, row, lane, owned, Xz + roff,
+                                  Uz ? Uz + roff : nullptr, Yz + roff, nx, i, kp);
+        double *tmp = sFa;
+        sFa = sFb;
+        sFb = tmp;
+    }
+
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (bad && lane == 0) {
+        atomicOr(kp.status, bad);
+        atomicMin(kp.first_tag, kp.tag);
+    }
+}
+
+#undef LEG
+#undef WP
+#undef WD
+
+}  // namespace dgswe

@@ -1,0 +1,337 @@
+"""Device-resident DG operator with the reference's solver API.
+
+``SpatialOperator`` and ``State`` mirror /root/reference/pkg/src/dgswe/
+dg.py:47-89 and 166-543 (constructor, attributes, ``zero_state``,
+``state_from_coeffs``, ``project_state``, ``assemble_rhs``,
+``max_physical_speed``); the right-hand side itself is one fused CUDA launch
+through the C ABI (include/dgswe_b200.h, ``dgswe_rhs``).
+
+Device layout of a state: one fp64 tensor ``data[z, j, v, m, i]``
+(level, latitude row, variable, mode, longitude) -- structure of arrays
+with longitude fastest so a warp's 32 lanes read 32 consecutive elements.
+There is no halo ring: the periodic longitude wrap is an index wrap inside
+the kernel (replaces ``_halo_exchange``, dg.py:330-346).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .geometry import (Mesh, build_vander, gauss_legendre, node_latitudes, project_initial,
+                       sphere_row_mass_matrices)
+from .physics import PositivityError, SphereSWEModel
+
+VAR_NAMES = ("h", "hu", "hv")
+
+
+@dataclass(frozen=True)
+class RusanovParams:
+    """Per-interface local alpha (default) or one global alpha per
+    direction, optionally pinned (dg.py:47-57)."""
+
+    mode: str = "local"
+    alpha: float | None = None
+
+    def __post_init__(self):
+        if self.mode not in ("local", "global"):
+            raise ValueError(f"mode must be 'local' or 'global', got {self.mode!r}")
+
+
+def _to_device_layout(stack: np.ndarray) -> np.ndarray:
+    """(3, nx, ny, nz, nphi) reference interior layout -> (nz, ny, 3, nphi, nx)."""
+    return np.ascontiguousarray(np.transpose(stack, (3, 2, 0, 4, 1)))
+
+
+def _to_reference_layout(data: torch.Tensor) -> np.ndarray:
+    """(nz, ny, 3, nphi, nx) device tensor -> (3, nx, ny, nz, nphi) host."""
+    return np.ascontiguousarray(data.detach().cpu().numpy().transpose(2, 4, 1, 0, 3))
+
+
+class _VarView:
+    """Host view object standing in for a reference ``Field`` (``.data`` is
+    the halo-padded (nx+2, ny+2, nz, nphi) array, copied from the device)."""
+
+    def __init__(self, state: "State", v: int):
+        self._s, self._v = state, v
+
+    @property
+    def data(self) -> np.ndarray:
+        s = self._s
+        inner = s.interior_coeffs(s.names[self._v])
+        out = np.zeros((s.nx + 2, s.ny + 2, s.nz, s.nphi))
+        out[1:-1, 1:-1] = inner
+        out[0, 1:-1] = inner[-1]
+        out[-1, 1:-1] = inner[0]
+        return out
+
+
+class State:
+    """Modal coefficients of (h, hu, hv) on the device.
+
+    ``interior_coeffs(name)`` returns a host copy shaped like the
+    reference's (nx, ny, nz, nphi) view; writes to it do not reach the
+    device (use :meth:`set_interior_coeffs`).
+    """
+
+    def __init__(self, data: torch.Tensor, nx: int, ny: int, nz: int, nphi: int):
+        if data.dtype != torch.float64 or not data.is_cuda:
+            raise TypeError("State data must be a CUDA float64 tensor")
+        if tuple(data.shape) != (nz, ny, 3, nphi, nx) or not data.is_contiguous():
+            raise ValueError(f"State data must be contiguous (nz, ny, 3, nphi, nx), got "
+                             f"{tuple(data.shape)}")
+        self.data = data
+        self.names = VAR_NAMES
+        self.nx, self.ny, self.nz, self.nphi = nx, ny, nz, nphi
+
+    @property
+    def fields(self) -> dict:
+        return {n: _VarView(self, v) for v, n in enumerate(self.names)}
+
+    @property
+    def interior(self):
+        return (self.nx, self.ny, self.nz)
+
+    def interior_coeffs(self, name: str) -> np.ndarray:
+        v = self.names.index(name)
+        return np.ascontiguousarray(
+            self.data[:, :, v].detach().cpu().numpy().transpose(3, 1, 0, 2))
+
+    def set_interior_coeffs(self, name: str, arr) -> None:
+        v = self.names.index(name)
+        a = np.broadcast_to(np.asarray(arr, dtype=np.float64), (self.nx, self.ny, self.nz, self.nphi))
+        self.data[:, :, v].copy_(torch.from_numpy(np.ascontiguousarray(a.transpose(2, 1, 3, 0))))
+
+    def to_numpy(self) -> np.ndarray:
+        """(3, nx, ny, nz, nphi) host copy in the reference's interior layout."""
+        return _to_reference_layout(self.data)
+
+    def copy(self) -> "State":
+        return State(self.data.clone(), self.nx, self.ny, self.nz, self.nphi)
+
+    def max_abs(self) -> float:
+        return float(self.data.abs().max().item())
+
+
+class _Context:
+    """Owns one dgswe_ctx (C ABI) for a band of latitude rows."""
+
+    def __init__(self, mesh: Mesh, p: int, model: SphereSWEModel, rusanov: RusanovParams, nz: int,
+                 quad, vander, Minv, row0=0, nrows=None, jlo=None, jhi=None, row_chunk=0):
+        lib = _lib.load()
+        ny = mesh.ny
+        nrows = ny if nrows is None else nrows
+        jlo = 0 if jlo is None else jlo
+        jhi = nrows if jhi is None else jhi
+        const = model.constants
+        th = node_latitudes(mesh, quad.nodes)                 # (ny, n)
+        R = const.radius
+        arrs = {
+            "leg": vander.leg, "dleg": vander.dleg, "weights": quad.weights,
+            "cos_r_int": np.cos(th) / R, "sin_r_int": np.sin(th) / R,
+            "fcos_int": 2.0 * const.omega * np.sin(th) * np.cos(th),
+            "cos_r_edge": np.cos(mesh.y_edges) / R, "cos_edge": np.cos(mesh.y_edges),
+            "minv": Minv,
+        }
+        keep = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in arrs.items()}
+        tabs = _lib.Tables(**{k: v.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+                              for k, v in keep.items()})
+        if rusanov.mode == "local":
+            mode, alpha = _lib.ALPHA_LOCAL, 0.0
+        elif rusanov.alpha is not None:
+            mode, alpha = _lib.ALPHA_GLOBAL_PINNED, float(rusanov.alpha)
+        else:
+            mode, alpha = _lib.ALPHA_GLOBAL, 0.0
+        cfg = _lib.Cfg(nx=mesh.nx, ny=ny, nz=nz, p=p, row0=row0, nrows=nrows, jlo=jlo, jhi=jhi,
+                       radius=R, gravity=model.gravity, h_floor=model.h_floor,
+                       dx=mesh.dx, dy=mesh.dy, alpha_mode=mode, alpha=alpha,
+                       row_chunk=int(row_chunk))
+        handle = ctypes.c_void_p()
+        _lib.check(lib.dgswe_create(ctypes.byref(cfg), ctypes.byref(tabs), ctypes.byref(handle)),
+                   "dgswe_create")
+        self.lib, self.h = lib, handle
+        self.row0, self.nrows, self.jlo, self.jhi = row0, nrows, jlo, jhi
+        self.device = torch.cuda.current_device()
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            try:
+                self.lib.dgswe_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    @staticmethod
+    def stream():
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def status(self, reset=True):
+        flags = ctypes.c_uint32(0)
+        tag = ctypes.c_int32(0)
+        _lib.check(self.lib.dgswe_status(self.h, ctypes.byref(flags), ctypes.byref(tag),
+                                         int(reset), self.stream()), "dgswe_status")
+        return flags.value, tag.value
+
+    def launches(self) -> int:
+        return int(self.lib.dgswe_launch_count(self.h))
+
+
+def _ptr(t: torch.Tensor | None):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+class _NullTimer:
+    def begin(self, phase):
+        pass
+
+    def end(self, phase):
+        pass
+
+
+class SpatialOperator:
+    """Precomputed DG discretisation of the spherical SWE on one mesh, with
+    the right-hand side evaluated by the fused sm_100a kernel.
+
+    Quadrature: p+1 Gauss points per direction for interior and edges,
+    weights and Jacobians folded into the device contraction constants.
+    """
+
+    def __init__(self, mesh: Mesh, p: int, model: SphereSWEModel, rusanov: RusanovParams | None = None,
+                 nz: int = 1, timers=None, device=None, row_chunk: int = 0):
+        if not getattr(model, "is_spherical", False) or mesh.kind != "latlon":
+            raise ValueError("model/mesh geometry mismatch (only the lat-lon sphere is supported)")
+        if not torch.cuda.is_available():
+            raise RuntimeError("SpatialOperator needs a CUDA device (no CPU fallback)")
+        self.mesh, self.p, self.model = mesh, int(p), model
+        self.rusanov = rusanov or RusanovParams()
+        self.nz = int(nz)
+        self.timers = timers or _NullTimer()
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else \
+            torch.device(device)
+        self.quad = gauss_legendre(self.p + 1)
+        self.vander = build_vander(self.p, self.quad)
+        self.nphi, self.n1, self.nq = self.vander.nphi, self.vander.n_1d, self.vander.n_q
+        self.halo_shape = (mesh.nx + 2, mesh.ny + 2, self.nz)
+        self.M_rows, self.Minv_rows = sphere_row_mass_matrices(self.p, mesh, self.quad)
+        self.M_planar = None
+        with torch.cuda.device(self.device):
+            self._ctx = _Context(mesh, self.p, model, self.rusanov, self.nz, self.quad, self.vander,
+                                 self.Minv_rows, row_chunk=row_chunk)
+        self._phi_dev = None
+        self._scratch = {}
+
+    # -- state construction -------------------------------------------------
+
+    @property
+    def state_shape(self):
+        return (self.nz, self.mesh.ny, 3, self.nphi, self.mesh.nx)
+
+    def zero_state(self) -> State:
+        d = torch.zeros(self.state_shape, dtype=torch.float64, device=self.device)
+        return State(d, self.mesh.nx, self.mesh.ny, self.nz, self.nphi)
+
+    def state_from_coeffs(self, coeffs: dict) -> State:
+        """Per-variable (nx, ny, nphi) (or (nx, ny, nz, nphi)) arrays."""
+        stack = np.zeros((3, self.mesh.nx, self.mesh.ny, self.nz, self.nphi))
+        for name, arr in coeffs.items():
+            a = np.asarray(arr, dtype=np.float64)
+            stack[VAR_NAMES.index(name)] = a[:, :, None, :] if a.ndim == 3 else a
+        return self.state_from_array(stack)
+
+    def state_from_array(self, stack: np.ndarray) -> State:
+        """(3, nx, ny, nz, nphi) host array in the reference's interior layout."""
+        d = torch.from_numpy(_to_device_layout(np.asarray(stack, dtype=np.float64)))
+        return State(d.to(self.device), self.mesh.nx, self.mesh.ny, self.nz, self.nphi)
+
+    def state_from_reference(self, ref_state) -> State:
+        """Adopt a reference ``dgswe.dg.State`` (interior coefficients)."""
+        return self.state_from_array(np.stack([ref_state.interior_coeffs(n) for n in VAR_NAMES]))
+
+    def project_state(self, ic_funcs: dict) -> State:
+        return self.state_from_coeffs({name: project_initial(f, self.mesh, self.vander)
+                                       for name, f in ic_funcs.items()})
+
+    # -- device entry points ------------------------------------------------
+
+    def _check(self, state: State):
+        if tuple(state.data.shape) != self.state_shape:
+            raise ValueError(f"state shape {tuple(state.data.shape)} != operator {self.state_shape}")
+
+    def raise_on_status(self, flags: int):
+        if flags & _lib.STATUS_POSITIVITY:
+            raise PositivityError("non-positive water height at a quadrature node")
+
+    def assemble_rhs(self, state: State, out: State | None = None, check: bool = True) -> State:
+        """Full right-hand side M^-1 (volume - boundary + source); raises
+        PositivityError like the reference when ``check`` (one device sync)."""
+        self._check(state)
+        if out is None:
+            out = self.zero_state()
+        self._check(out)
+        self.timers.begin("main")
+        c = self._ctx
+        _lib.check(c.lib.dgswe_rhs(c.h, _ptr(state.data), _ptr(out.data), c.stream()), "dgswe_rhs")
+        self.timers.end("main")
+        if check:
+            flags, _ = c.status(reset=True)
+            self.raise_on_status(flags)
+        return out
+
+    def stage(self, a: float, U: State | None, b: float, X: State, g: float, Y: State, tag: int = 0):
+        """Y = a U + b X + g RHS(X) in one launch (no sync)."""
+        c = self._ctx
+        _lib.check(c.lib.dgswe_stage(c.h, float(a), _ptr(U.data if U is not None else None),
+                                     float(b), _ptr(X.data), float(g), _ptr(Y.data), int(tag),
+                                     c.stream()), "dgswe_stage")
+
+    def axpy(self, coef: float, x: State, y: State, check_finite: bool = False, tag: int = 0):
+        """y += x*coef with the reference's two roundings (timestep.py:137-141)."""
+        c = self._ctx
+        _lib.check(c.lib.dgswe_axpy(c.h, float(coef), _ptr(x.data), _ptr(y.data),
+                                    int(check_finite), int(tag), c.stream()), "dgswe_axpy")
+
+    def ssprk3_steps(self, state: State, dt: float, nsteps: int, check_mean: bool = False):
+        """nsteps fused Shu-Osher SSPRK3 steps in place (one CUDA graph)."""
+        self._check(state)
+        key = state.data.data_ptr()
+        ws = self._scratch.get(key)
+        if ws is None:
+            ws = (torch.empty_like(state.data), torch.empty_like(state.data))
+            self._scratch = {key: ws}
+        c = self._ctx
+        _lib.check(c.lib.dgswe_ssprk3(c.h, _ptr(state.data), _ptr(ws[0]), _ptr(ws[1]), float(dt),
+                                      int(nsteps), int(check_mean), c.stream()), "dgswe_ssprk3")
+
+    def status(self, reset: bool = True):
+        return self._ctx.status(reset)
+
+    def launch_count(self) -> int:
+        return self._ctx.launches()
+
+    # -- host-side helpers (diagnostics / step control) ---------------------
+
+    def interior_nodal_values(self, state: State) -> dict:
+        """(nx, ny, nz, nq) nodal values per variable."""
+        if self._phi_dev is None:
+            self._phi_dev = torch.from_numpy(self.vander.phi).to(self.device)
+        U = torch.einsum("qm,zjvmi->vijzq", self._phi_dev, state.data)
+        return {n: U[v].cpu().numpy() for v, n in enumerate(VAR_NAMES)}
+
+    def interior_theta(self):
+        return None
+
+    def max_physical_speed(self, state: State) -> float:
+        """max over interior nodes of max(|u|,|v|) + sqrt(g h) (models.py:282-285)."""
+        if self._phi_dev is None:
+            self._phi_dev = torch.from_numpy(self.vander.phi).to(self.device)
+        U = torch.einsum("qm,zjvmi->vzjqi", self._phi_dev, state.data)
+        h = U[0]
+        hf = torch.clamp_min(h, self.model.h_floor)
+        c = torch.sqrt(self.model.gravity * torch.clamp_min(h, 0.0))
+        vel = torch.maximum((U[1] / hf).abs(), (U[2] / hf).abs())
+        return float((vel + c).max().item())

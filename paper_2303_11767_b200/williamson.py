@@ -1,0 +1,136 @@
+"""Williamson shallow-water test cases and run configurations.
+
+API of /root/reference/pkg/src/dgswe/cases.py (``CaseConfig``,
+``default_config``, ``build_case``, ``RunSetup``, ``ic_williamson_tc2``,
+``ic_williamson_tc6``) for the two spherical cases of the reference.
+Williamson et al. (1992) equations: TC2 (90)-(95) with alpha = 0,
+TC6 (142)-(149).  The planar cases (advection, geostrophic adjustment) are
+outside the spherical hot path and raise NotImplementedError.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from .geometry import EARTH, PhysicalConstants, build_latlon_mesh
+from .physics import swe_sphere_model
+
+DAY = 86400.0
+TC2_U0 = 2.0 * math.pi * EARTH.radius / (12.0 * DAY)
+TC2_GH0 = 2.94e4
+TC6_OMEGA = 7.848e-6
+TC6_K = 7.848e-6
+TC6_H0 = 8.0e3
+TC6_R = 4
+
+CASE_IDS = ("advection_sine", "geostrophic_adjustment", "williamson_tc2", "williamson_tc6")
+SPHERE_CASES = ("williamson_tc2", "williamson_tc6")
+
+
+@dataclass(frozen=True)
+class CaseConfig:
+    case: str
+    nx: int
+    ny: int
+    p: int
+    rk: int
+    t_final: float
+    dt: float | None = None
+    courant: float | None = None
+    nz: int = 1
+    alpha_mode: str = "local"
+    alpha: float | None = None
+
+    def override(self, **kwargs) -> "CaseConfig":
+        return replace(self, **{k: v for k, v in kwargs.items() if v is not None})
+
+
+_DEFAULTS = {
+    "advection_sine": dict(nx=20, ny=20, p=2, rk=4, t_final=1.0, courant=0.2),
+    "geostrophic_adjustment": dict(nx=50, ny=50, p=3, rk=4, t_final=36000.0, dt=100.0),
+    "williamson_tc2": dict(nx=20, ny=20, p=3, rk=4, t_final=2.0 * DAY, courant=0.2),
+    "williamson_tc6": dict(nx=40, ny=20, p=3, rk=4, t_final=8.0 * DAY, dt=4.0),
+}
+
+
+def default_config(case: str) -> CaseConfig:
+    if case not in _DEFAULTS:
+        raise ValueError(f"unknown case {case!r}; choose from {CASE_IDS}")
+    return CaseConfig(case=case, **_DEFAULTS[case])
+
+
+def ic_williamson_tc2(constants: PhysicalConstants = EARTH):
+    """Steady zonal geostrophic flow: u = u0 cos(theta), v = 0,
+    g h = g h0 - (R Omega u0 + u0^2/2) sin^2(theta)."""
+    g = constants.gravity
+    u0 = TC2_U0
+    k = constants.radius * constants.omega * u0 + 0.5 * u0 * u0
+
+    def height(lam, th):
+        return (TC2_GH0 - k * np.sin(th) ** 2) / g + 0.0 * lam
+
+    return ({"h": height,
+             "hu": lambda lam, th: height(lam, th) * u0 * np.cos(th),
+             "hv": lambda lam, th: np.zeros(np.broadcast(lam, th).shape)},
+            height)
+
+
+def tc6_fields(constants: PhysicalConstants = EARTH):
+    """Wavenumber-4 Rossby-Haurwitz height and winds."""
+    a, g, Om = constants.radius, constants.gravity, constants.omega
+    w, K, R = TC6_OMEGA, TC6_K, TC6_R
+
+    def winds(lam, th):
+        c = np.cos(th)
+        u = a * w * c + a * K * c ** (R - 1) * (R * np.sin(th) ** 2 - c**2) * np.cos(R * lam)
+        v = -a * K * R * c ** (R - 1) * np.sin(th) * np.sin(R * lam)
+        return u, v
+
+    def height(lam, th):
+        c = np.cos(th)
+        A = 0.5 * w * (2.0 * Om + w) * c**2 + 0.25 * K**2 * c ** (2 * R) * (
+            (R + 1) * c**2 + (2 * R**2 - R - 2) - 2.0 * R**2 * c ** (-2))
+        B = (2.0 * (Om + w) * K) / ((R + 1) * (R + 2)) * c**R * (
+            (R**2 + 2 * R + 2) - (R + 1) ** 2 * c**2)
+        C = 0.25 * K**2 * c ** (2 * R) * ((R + 1) * c**2 - (R + 2))
+        return TC6_H0 + (a * a / g) * (A + B * np.cos(R * lam) + C * np.cos(2 * R * lam))
+
+    return height, winds
+
+
+def ic_williamson_tc6(constants: PhysicalConstants = EARTH):
+    height, winds = tc6_fields(constants)
+    return {"h": height,
+            "hu": lambda lam, th: height(lam, th) * winds(lam, th)[0],
+            "hv": lambda lam, th: height(lam, th) * winds(lam, th)[1]}
+
+
+@dataclass
+class RunSetup:
+    config: CaseConfig
+    mesh: object
+    model: object
+    ic: dict
+    exact: object = None
+    constants: PhysicalConstants = EARTH
+
+
+def build_case(config: CaseConfig, constants: PhysicalConstants = EARTH) -> RunSetup:
+    case = config.case
+    if case == "williamson_tc2":
+        ic, height = ic_williamson_tc2(constants)
+        setup = RunSetup(config, build_latlon_mesh(config.nx, config.ny, constants.radius),
+                         swe_sphere_model(constants, h_ref=TC2_GH0 / constants.gravity), ic,
+                         None, constants)
+        setup.exact = lambda t: height
+        return setup
+    if case == "williamson_tc6":
+        return RunSetup(config, build_latlon_mesh(config.nx, config.ny, constants.radius),
+                        swe_sphere_model(constants, h_ref=TC6_H0), ic_williamson_tc6(constants),
+                        None, constants)
+    if case in CASE_IDS:
+        raise NotImplementedError(f"{case!r} is a planar case, outside the spherical hot path")
+    raise ValueError(f"unknown case {case!r}; choose from {CASE_IDS}")
