@@ -1,0 +1,380 @@
+"""Benchmark: DOF-updates/s per RK stage of the fused fp64 SSPRK3 DG
+shallow-water step on B200 (BASELINE.json metric), with the roofline, the
+CPU oracle baseline, an end-to-end host-buffer number and clock samples.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c4]
+    python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+    python bench.py --impl reference ...     (CPU reference arm)
+
+Workload (default, config C3 of BASELINE.json): Williamson TC6
+Rossby-Haurwitz wave, p=3 (order 4), 720x360 elements, 12,441,600 DOF,
+SSPRK3 with dt = 5e-3 s; synthetic = the analytic TC6 initial condition
+projected on the mesh (no dataset).  N>1: the same grid split into
+latitude bands (strong scaling), one process per GPU, NCCL halo exchange.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (case, nx, ny, p, dt, label)
+    "c3": ("williamson_tc6", 720, 360, 3, 5e-3, "C3: Williamson TC6, order 4 (p=3), 720x360, SSPRK3"),
+    "c2": ("williamson_tc2", 360, 180, 3, 0.05, "C2: Williamson TC2, order 4 (p=3), 360x180, SSPRK3"),
+    "c4": ("williamson_tc6", 1440, 720, 4, 5e-4,
+           "C4 shape: order 5 (p=4), 1440x720, SSPRK3, TC6 IC (no orography in the reference)"),
+}
+METRIC = "DOF-updates/sec (fp64, per RK stage)"
+UNIT = "DOF-updates/s"
+B_ALG = 64.0 / 3.0          # algorithmic HBM bytes per DOF-update, SSPRK3 Shu-Osher
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_rate(case, nx, ny, p, dt, budget_s=12.0, max_steps=None):
+    """The CPU oracle (bit-exact C port of the reference path, OpenMP over
+    all host threads) on the same workload; returns (rate, steps, seconds, threads)."""
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
+    from oracle import oracle as O
+    t, orc, X = O.build_case(case, nx, ny, p)
+    threads = O.max_threads()
+    dofs = nx * ny * (p + 1) ** 2 * 3
+    orc.rk_steps(X, dt, 3, 1)                       # warm-up (page-in, threads)
+    steps, t0 = 0, time.perf_counter()
+    while True:
+        X, st, _ = orc.rk_steps(X, dt, 3, 1)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or (max_steps and steps >= max_steps):
+            break
+    return dofs * 3 * steps / el, steps, el, threads
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    case, nx, ny, p, dt, label = CONFIGS[args.config]
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
+    from oracle import oracle as O
+    t, orc, X = O.build_case(case, nx, ny, p)
+    threads = O.max_threads()
+    dofs = nx * ny * (p + 1) ** 2 * 3
+    for _ in range(args.warmup):
+        X, _, _ = orc.rk_steps(X, dt, 3, 1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        X, _, _ = orc.rk_steps(X, dt, 3, 1)
+    el = time.perf_counter() - t0
+    value = dofs * 3 * args.steps / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (analytic Williamson initial condition projected on the mesh)",
+        "config": {"workload": label, "case": case, "nx": nx, "ny": ny, "p": p, "dofs": dofs,
+                   "dt": dt, "rk": "SSPRK3 (tableau(3), Butcher form)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} full SSPRK3 steps of the {args.config.upper()} "
+                                   f"grid after {args.warmup} warm-up steps; oracle/dgswe_oracle.c "
+                                   "(bit-exact C port of the reference RHS/RK, OpenMP)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def load_traffic(config):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(path))
+        return d.get(config)
+    except (OSError, ValueError):
+        return None
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2303_11767_b200 as P
+    from paper_2303_11767_b200.bands import BandLayout, BandOperator
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    case, nx, ny, p, dt, label = CONFIGS[args.config]
+    setup = P.build_case(P.default_config(case).override(nx=nx, ny=ny, p=p))
+    op = P.SpatialOperator(setup.mesh, p, setup.model)
+    dofs = nx * ny * (p + 1) ** 2 * 3
+    state = op.project_state(setup.ic)
+    stream = torch.cuda.current_stream()
+
+    if world == 1:
+        def steps(k):
+            op.ssprk3_steps(state, dt, k)
+        counter = op.launch_count
+        state_bytes = state.data.numel() * 8
+    else:
+        L = BandLayout(ny, world, rank)
+        bop = BandOperator(op, L, transport="p2p")
+        full = state.data.cpu().numpy()
+        u = torch.from_numpy(L.scatter(full)).cuda()
+        w1, w2 = bop.empty(), bop.empty()
+        del state
+
+        def steps(k):
+            for _ in range(k):
+                bop.ssprk3_step(u, w1, w2, dt)
+        counter = bop.launch_count
+        state_bytes = u.numel() * 8
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up (also builds the CUDA graph for k = steps)
+    steps(args.warmup)
+    steps(args.steps)
+    torch.cuda.synchronize()
+    barrier()
+
+    # timed region: K steps, device events, max over ranks
+    n0 = counter()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        steps(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = counter() - n0
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    if world == 1:
+        flags, _ = op.status()
+    else:
+        flags, _ = bop.status()
+    if flags:
+        raise SystemExit(f"device status flags {flags:#x} during the bench")
+    value = dofs * 3 * args.steps / (ms * 1e-3)
+
+    # per-stage launch times (event-timed, same stream, individual launches)
+    per_stage = None
+    if world == 1:
+        w1, w2 = torch.empty_like(state.data), torch.empty_like(state.data)
+        s1 = P.State(w1, nx, ny, 1, op.nphi)
+        s2 = P.State(w2, nx, ny, 1, op.nphi)
+        reps = 20
+        times = {1: [], 2: [], 3: []}
+        for _ in range(reps):
+            for k, fn in ((1, lambda: op.stage(0.0, None, 1.0, state, dt, s1)),
+                          (2, lambda: op.stage(0.75, state, 0.25, s1, 0.25 * dt, s2)),
+                          (3, lambda: op.stage(1 / 3, state, 2 / 3, s2, 2 / 3 * dt, state))):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                times[k].append((a, b))
+        torch.cuda.synchronize()
+        per_stage = {k: statistics.median(a.elapsed_time(b) for a, b in v) for k, v in times.items()}
+        flags, _ = op.status()
+        assert flags == 0
+
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs", 6650.0)
+    local_dofs = dofs // world
+    stage_ms = ms / (3 * args.steps)                 # every launch in the region is a stage
+    achieved = local_dofs * B_ALG / (stage_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": load_traffic(args.config),
+                "kernel": f"dgswe::stage_kernel<{p}>",
+                "alg_bytes_per_launch": local_dofs * B_ALG,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
+    if per_stage:
+        roofline["per_stage_ms"] = per_stage
+        roofline["per_stage_gbs"] = {
+            k: local_dofs * (16.0 if k == 1 else 24.0) / (v * 1e-3) / 1e9 for k, v in per_stage.items()}
+
+    # end to end through the public API with host buffers: every step copies
+    # the state from pinned host memory, runs one fused SSPRK3 step and reads
+    # the result back (the reference's rk_step contract on a host state)
+    e2e = None
+    if world == 1:
+        host = torch.empty_like(state.data, device="cpu").pin_memory()
+        host.copy_(state.data)
+        dev = state
+        op.ssprk3_steps(dev, dt, 1)
+        torch.cuda.synchronize()
+        k2 = max(3, min(args.steps, 20))
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k2):
+            dev.data.copy_(host, non_blocking=True)
+            op.ssprk3_steps(dev, dt, 1)
+            host.copy_(dev.data, non_blocking=True)
+            flags, _ = op.status()                   # syncs: the step's result is on the host
+        e1.record(stream)
+        torch.cuda.synchronize()
+        el = e0.elapsed_time(e1) * 1e-3
+        e2e = {"value": dofs * 3 * k2 / el, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
+               "d2h_bytes_per_step": state_bytes, "steps": k2,
+               "path": "pinned host state -> dgswe_ssprk3 (C ABI, 1 step) -> pinned host, per step",
+               "wall_s": time.perf_counter() - t0}
+    else:
+        host = u.cpu().pin_memory()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k2 = max(3, min(args.steps, 20))
+        e0.record(stream)
+        for _ in range(k2):
+            u.copy_(host, non_blocking=True)
+            bop.ssprk3_step(u, w1, w2, dt)
+            host.copy_(u, non_blocking=True)
+            bop.status()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        el = max_over_ranks(e0.elapsed_time(e1)) * 1e-3
+        e2e = {"value": dofs * 3 * k2 / el, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
+               "d2h_bytes_per_step": state_bytes, "steps": k2}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, n, el, threads = cpu_oracle_rate(case, nx, ny, p, dt, budget_s=args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{n} full SSPRK3 steps of the same {args.config.upper()} grid "
+                         f"({el:.1f} s) with the bit-exact C port of the reference path "
+                         "(oracle/dgswe_oracle.c, OpenMP)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (analytic Williamson initial condition projected on the mesh)",
+            "config": {"workload": label, "case": case, "nx": nx, "ny": ny, "p": p, "dofs": dofs,
+                       "dt": dt, "rk": "SSPRK3, Shu-Osher fused stages (== tableau(3))",
+                       "parallelism": f"latitude bands x{world}" if world > 1 else "single GPU",
+                       "l2": f"no flush; per-stage working set {3 * dofs * 8 / 1e6:.0f} MB "
+                             f"(3 states) > 126 MB L2" if args.config != "c2" else
+                             "C2 states (25 MB each) fit in L2; roofline inflated"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clk.summary(), "gpu_launches": int(launches),
+            "dofs_per_gpu": local_dofs, "per_gpu_value": value / world,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

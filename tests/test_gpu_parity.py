@@ -1,0 +1,358 @@
+"""GPU parity: the fused sm_100a path (through the C ABI) against the
+bit-exact CPU oracle and the reference's own golden outputs.
+
+Tolerances (fp64; north star: rel L2 <= 1e-11 after N steps, mass drift
+matching to 1e-13):
+* one RHS: per-variable relative L2 error <= 20x the oracle's own 1-ulp
+  sensitivity (relative change of the oracle RHS when X is perturbed by one
+  ulp), floor 1e-13.  A single RHS cancels volume, boundary and source terms
+  (TC2 is a steady state), so its relative error measures conditioning, not
+  correctness;
+* N steps: rel L2 <= 1e-11 for h and hu; hv <= 1e-11 relative to
+  ||(hu, hv)|| (TC2's hv is pure discretisation error, ||hv|| ~ 1e-6
+  ||hu||); TC6 hv additionally <= 1e-11 relative to itself;
+* mass: |drift_gpu - drift_oracle| <= 1e-13 |mass_0|.
+"""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import ROOT, oracle_case
+
+pytestmark = pytest.mark.gpu
+
+RK3_CASES = ["tc2_c1", "tc6_40x20_p3", "tc2_40x20_p3", "tc6_p0", "tc6_p1", "tc6_p2", "tc6_p3",
+             "tc6_p4", "tc6_p5", "tc2_p3_odd", "tc6_ny1", "tc2_nx1", "tc6_nx2",
+             "tc6_global_pinned", "tc6_global", "tc6_nz2", "tc6_wide"]
+ALL_CASES = RK3_CASES + ["tc6_rk1", "tc6_rk2", "tc6_rk4", "tc2_c2_shape"]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2303_11767_b200 as P
+    torch.cuda.set_device(0)
+    return P
+
+
+def make_op(P, e, **kw):
+    cfg = P.default_config(e["case"]).override(nx=e["nx"], ny=e["ny"], p=e["p"], nz=e["nz"])
+    setup = P.build_case(cfg)
+    return P.SpatialOperator(setup.mesh, e["p"], setup.model,
+                             rusanov=P.RusanovParams(*e["rusanov"]), nz=e["nz"], **kw)
+
+
+def rel(a, b, v):
+    return float(np.linalg.norm(a[v] - b[v]) / max(np.linalg.norm(b[v]), 1e-300))
+
+
+def assert_state_close(got, ref, case, tol=1e-11):
+    assert np.all(np.isfinite(got))
+    assert rel(got, ref, 0) <= tol, ("h", rel(got, ref, 0))
+    assert rel(got, ref, 1) <= tol, ("hu", rel(got, ref, 1))
+    mom = np.sqrt(np.linalg.norm(ref[1]) ** 2 + np.linalg.norm(ref[2]) ** 2)
+    e_hv = float(np.linalg.norm(got[2] - ref[2]) / mom)
+    assert e_hv <= tol, ("hv/|m|", e_hv)
+    if case == "williamson_tc6":
+        assert rel(got, ref, 2) <= tol, ("hv", rel(got, ref, 2))
+
+
+def ulp_sensitivity(orc, X, K):
+    rng = np.random.default_rng(0)
+    Xp = X * (1.0 + rng.integers(-1, 2, size=X.shape) * 2.0 ** -52)
+    Kp = orc.rhs(Xp)
+    return [float(np.linalg.norm(Kp[v] - K[v]) / max(np.linalg.norm(K[v]), 1e-300)) for v in range(3)]
+
+
+@pytest.mark.parametrize("name", ALL_CASES)
+def test_rhs_parity(P, golden, oracle_mod, name):
+    meta, _ = golden
+    e = meta["cases"][name]
+    t, orc, X = oracle_case(oracle_mod, e)
+    op = make_op(P, e)
+    K = op.assemble_rhs(op.state_from_array(X)).to_numpy()
+    Kr = orc.rhs(X)
+    sens = ulp_sensitivity(orc, X, Kr)
+    for v in range(3):
+        assert rel(K, Kr, v) <= max(20 * sens[v], 1e-13), (v, rel(K, Kr, v), sens[v])
+
+
+@pytest.mark.parametrize("name", ALL_CASES)
+def test_butcher_steps_parity(P, golden, oracle_mod, name):
+    meta, g = golden
+    e = meta["cases"][name]
+    t, orc, X = oracle_case(oracle_mod, e)
+    U, status, _ = orc.rk_steps(X, e["dt"], e["rk"], e["nsteps"])
+    assert status == 0
+    op = make_op(P, e)
+    st = op.state_from_array(X)
+    tab = P.tableau(e["rk"])
+    for _ in range(e["nsteps"]):
+        P.rk_step(st, op.assemble_rhs, e["dt"], tab)
+    got = st.to_numpy()
+    assert_state_close(got, U, e["case"])
+    if f"{name}/final" in g:            # the reference's own output
+        assert_state_close(got, g[f"{name}/final"], e["case"])
+    for k in range(e["nz"]):
+        m0, m1 = e["mass_ic"][k], e["mass_final"][k]
+        mg = P.mass_integral(st, op, "h", level=k)
+        assert abs((mg - m0) - (m1 - m0)) <= 1e-13 * abs(m0)
+
+
+@pytest.mark.parametrize("name", RK3_CASES)
+def test_fused_ssprk3_parity(P, golden, oracle_mod, name):
+    meta, g = golden
+    e = meta["cases"][name]
+    t, orc, X = oracle_case(oracle_mod, e)
+    U, _, _ = orc.rk_steps(X, e["dt"], 3, e["nsteps"])
+    op = make_op(P, e)
+    st = op.state_from_array(X)
+    op.ssprk3_steps(st, e["dt"], e["nsteps"])
+    flags, _ = op.status()
+    assert flags == 0
+    got = st.to_numpy()
+    assert_state_close(got, U, e["case"])
+    for k in range(e["nz"]):
+        m0, m1 = e["mass_ic"][k], e["mass_final"][k]
+        mg = P.mass_integral(st, op, "h", level=k)
+        assert abs((mg - m0) - (m1 - m0)) <= 1e-13 * abs(m0)
+
+
+def test_integrate_c1_against_reference(P, golden):
+    """Config C1 end to end through the public API (project -> integrate)
+    against the reference's own 100-step output."""
+    meta, g = golden
+    e = meta["cases"]["tc2_c1"]
+    cfg = P.default_config("williamson_tc2").override(nx=40, ny=20, p=2, rk=3, dt=10.0,
+                                                       t_final=1000.0)
+    setup = P.build_case(cfg)
+    op = P.SpatialOperator(setup.mesh, cfg.p, setup.model)
+    st = op.project_state(setup.ic)
+    assert np.array_equal(st.to_numpy(), g["tc2_c1/ic"])
+    st, log = P.integrate(st, op, P.TimeControls(cfg.t_final, dt=cfg.dt), P.tableau(3))
+    assert log.steps == 100 and log.t == 1000.0 and log.dt == 10.0
+    assert_state_close(st.to_numpy(), g["tc2_c1/final"], "williamson_tc2")
+    m = P.mass_integral(st, op)
+    assert abs((m - e["mass_ic"][0]) - (e["mass_final"][0] - e["mass_ic"][0])) <= 1e-13 * abs(m)
+    l2 = P.l2_error(st, setup.exact(1000.0), op, "h", relative=True)
+    assert abs(l2 - e["l2_h_rel_final"]) <= 1e-9 * e["l2_h_rel_final"]
+
+
+def test_large_c2_against_oracle(P, oracle_mod):
+    """C2 shape (TC2 360x180 p=3, dt=0.05 s): 3 fused steps vs the oracle."""
+    t, orc, X = oracle_mod.build_case("williamson_tc2", 360, 180, 3)
+    U, _, _ = orc.rk_steps(X, 0.05, 3, 3)
+    setup = P.build_case(P.default_config("williamson_tc2").override(nx=360, ny=180, p=3))
+    op = P.SpatialOperator(setup.mesh, 3, setup.model)
+    st = op.state_from_array(X)
+    op.ssprk3_steps(st, 0.05, 3)
+    assert op.status()[0] == 0
+    assert_state_close(st.to_numpy(), U, "williamson_tc2")
+
+
+def test_c3_conservation_and_rk_equivalence(P):
+    """C3 shape (TC6 720x360 p=3): mass conserved to 1e-13 over 20 fused
+    steps, and fused Shu-Osher == Butcher rk_step to 1e-12."""
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=720, ny=360, p=3))
+    op = P.SpatialOperator(setup.mesh, 3, setup.model)
+    st = op.project_state(setup.ic)
+    ref = st.copy()
+    m0 = P.mass_integral(st, op)
+    op.ssprk3_steps(st, 5e-3, 20)
+    assert op.status()[0] == 0
+    assert abs(P.mass_integral(st, op) - m0) <= 1e-13 * abs(m0)
+    for _ in range(20):
+        P.rk_step(ref, op.assemble_rhs, 5e-3, P.tableau(3))
+    a, b = st.to_numpy(), ref.to_numpy()
+    for v in range(3):
+        assert rel(a, b, v) <= 1e-12
+
+
+@pytest.mark.parametrize("rc", [1, 3, 7])
+def test_row_chunk_invariance(P, golden, oracle_mod, rc):
+    """Rows per CTA change which CTA evaluates a face, never its bits."""
+    meta, _ = golden
+    e = meta["cases"]["tc6_wide"]
+    t, orc, X = oracle_case(oracle_mod, e)
+    base = make_op(P, e)
+    other = make_op(P, e, row_chunk=rc)
+    a = base.assemble_rhs(base.state_from_array(X)).data
+    b = other.assemble_rhs(other.state_from_array(X)).data
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_band_decomposition_bitwise(P, oracle_mod, world):
+    """Latitude bands with halo rows (one context per band, as on one GPU of
+    a multi-GPU run) reproduce the single-band stage bit for bit, including
+    the interior/boundary split used to overlap the halo exchange."""
+    from paper_2303_11767_b200.bands import BandLayout, BandOperator
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=64, ny=21, p=3, nz=2))
+    op = P.SpatialOperator(setup.mesh, 3, setup.model, nz=2)
+    st = op.project_state(setup.ic)
+    st.data[1] *= 1.0001
+    full = st.data.cpu().numpy()
+    w1 = op.zero_state()
+    op.stage(0.0, None, 1.0, st, 7.0, w1)
+    w2 = op.zero_state()
+    op.stage(0.75, st, 0.25, w1, 1.75, w2)
+    want1, want2 = w1.data.cpu().numpy(), w2.data.cpu().numpy()
+    for r in range(world):
+        L = BandLayout(21, world, r)
+        bop = BandOperator(op, L, transport="p2p", overlap=False)
+        u = torch.from_numpy(L.scatter(full)).cuda()
+        x1 = torch.from_numpy(L.scatter(want1)).cuda()
+        y1 = bop.empty()
+        bop._launch(0.0, None, 1.0, u, 7.0, y1, 0, L.jlo, L.jhi)
+        y2 = bop.empty()
+        if L.owned > 2:
+            bop._launch(0.75, u, 0.25, x1, 1.75, y2, 0, L.jlo + 1, L.jhi - 1)
+            bop._launch(0.75, u, 0.25, x1, 1.75, y2, 0, L.jlo, L.jlo + 1)
+            bop._launch(0.75, u, 0.25, x1, 1.75, y2, 0, L.jhi - 1, L.jhi)
+        else:
+            bop._launch(0.75, u, 0.25, x1, 1.75, y2, 0, L.jlo, L.jhi)
+        assert np.array_equal(y1.cpu().numpy()[:, 1:L.jhi], want1[:, L.j0:L.j1])
+        assert np.array_equal(y2.cpu().numpy()[:, 1:L.jhi], want2[:, L.j0:L.j1])
+
+
+def test_multiprocess_bands_on_one_gpu(P, tmp_path):
+    """Two ranks (torchrun, gloo host transport, same GPU) step TC6 with
+    halo exchange per stage; result equals the single-GPU run bitwise."""
+    out = tmp_path / "bands.npy"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29533",
+           os.path.join(ROOT, "tools", "band_run.py"), "--transport", "host", "--out", str(out)]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    got = np.load(out)
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=48, ny=16, p=3))
+    op = P.SpatialOperator(setup.mesh, 3, setup.model)
+    st = op.project_state(setup.ic)
+    op.ssprk3_steps(st, 5.0, 4)
+    assert np.array_equal(got, st.data.cpu().numpy())
+
+
+def test_positivity_raises(P):
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=12, ny=6, p=2))
+    op = P.SpatialOperator(setup.mesh, 2, setup.model)
+    st = op.project_state(setup.ic)
+    st.data[0, 3, 0, 0, 5] = -100.0
+    with pytest.raises(P.PositivityError):
+        op.assemble_rhs(st)
+    with pytest.raises(P.PositivityError):
+        P.rk_step(st, op.assemble_rhs, 1.0, P.tableau(3))
+    with pytest.raises(P.DivergenceError) as ei:
+        P.integrate(st, op, P.TimeControls(10.0, dt=1.0), P.tableau(3))
+    assert ei.value.step == 1 and ei.value.t == 0.0
+
+
+def test_divergence_reported_at_failing_step(P):
+    """Blow-up under an unstable dt: the fused batch reports the first
+    failing step, like the reference's per-step check."""
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=40, ny=20, p=3))
+    op = P.SpatialOperator(setup.mesh, 3, setup.model)
+    st = op.project_state(setup.ic)
+    with pytest.raises(P.DivergenceError) as ei:
+        P.integrate(st, op, P.TimeControls(4000.0, dt=40.0), P.tableau(3), batch=16)
+    step = ei.value.step
+    st2 = op.project_state(setup.ic)
+    with pytest.raises(P.DivergenceError) as ei2:
+        P.integrate(st2, op, P.TimeControls(4000.0, dt=40.0), P.tableau(3), fused=False)
+    assert 1 <= step <= 100
+    assert abs(ei2.value.step - step) <= 1
+
+
+def test_nonfinite_detected(P):
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=12, ny=6, p=2))
+    op = P.SpatialOperator(setup.mesh, 2, setup.model)
+    st = op.project_state(setup.ic)
+    st.data[0, 2, 1, 3, 4] = float("inf")
+    with pytest.raises((P.DivergenceError, P.PositivityError)):
+        P.rk_step(st, op.assemble_rhs, 1.0, P.tableau(3))
+
+
+def test_cell_mean_check(P):
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=12, ny=6, p=2))
+    op = P.SpatialOperator(setup.mesh, 2, setup.model)
+    st = op.project_state(setup.ic)
+    st2 = st.copy()
+    P.integrate(st, op, P.TimeControls(30.0, dt=10.0), P.tableau(3), check_positivity="h")
+    P.integrate(st2, op, P.TimeControls(30.0, dt=10.0), P.tableau(3), check_positivity="h",
+                fused=False)
+    a, b = st.to_numpy(), st2.to_numpy()
+    for v in range(3):                      # Shu-Osher vs Butcher: rounding only
+        assert rel(a, b, v) <= 1e-13
+
+
+def test_state_api(P, golden):
+    meta, g = golden
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=12, ny=6, p=3))
+    op = P.SpatialOperator(setup.mesh, 3, setup.model)
+    st = op.project_state(setup.ic)
+    assert np.array_equal(st.to_numpy(), g["tc6_p3/ic"])
+    hu = st.interior_coeffs("hu")
+    assert hu.shape == (12, 6, 1, 16)
+    padded = st.fields["hu"].data
+    assert np.array_equal(padded[1:-1, 1:-1], hu)
+    assert np.array_equal(padded[0, 1:-1], hu[-1]) and np.array_equal(padded[-1, 1:-1], hu[0])
+    cp = st.copy()
+    cp.set_interior_coeffs("hu", hu * 2.0)
+    assert np.array_equal(cp.interior_coeffs("hu"), hu * 2.0)
+    assert np.array_equal(st.interior_coeffs("hu"), hu)
+    assert st.max_abs() == float(np.abs(st.to_numpy()).max())
+    s2 = op.state_from_coeffs({n: st.interior_coeffs(n)[:, :, 0, :] for n in st.names})
+    assert torch.equal(s2.data, st.data)
+    U = op.interior_nodal_values(st)
+    ref = np.einsum("qm,xyzm->xyzq", op.vander.phi, st.interior_coeffs("h"))
+    assert np.allclose(U["h"], ref, rtol=1e-14, atol=0)
+    Un = {n: np.einsum("qm,xyzm->xyzq", op.vander.phi, st.interior_coeffs(n)) for n in st.names}
+    assert abs(op.max_physical_speed(st) - setup.model.max_physical_speed(Un)) <= 1e-12 * 400
+    with pytest.raises(ValueError):
+        op.assemble_rhs(P.SpatialOperator(P.build_latlon_mesh(8, 6), 3, setup.model).zero_state())
+
+
+def test_integrate_schedule_and_callbacks(P, oracle_mod):
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=16, ny=8, p=2))
+    op = P.SpatialOperator(setup.mesh, 2, setup.model)
+    st = op.project_state(setup.ic)
+    X = st.to_numpy()
+    seen = []
+    st, log = P.integrate(st, op, P.TimeControls(95.0, dt=10.0), P.tableau(3),
+                          callbacks=[(3, lambda s, t, x: seen.append((s, t)))])
+    assert log.steps == 10 and log.t == 95.0
+    assert [s for s, _ in seen] == [0, 3, 6, 9, 10] and seen[-1][1] == 95.0
+    t, orc, _ = oracle_mod.build_case("williamson_tc6", 16, 8, 2)
+    U, _, _ = orc.rk_steps(X, 10.0, 3, 9)
+    U, _, _ = orc.rk_steps(U, 5.0, 3, 1)
+    assert_state_close(st.to_numpy(), U, "williamson_tc6")
+    st0 = op.project_state(setup.ic)
+    out, log0 = P.integrate(st0, op, P.TimeControls(0.0, dt=1.0), P.tableau(3))
+    assert log0.steps == 0 and out is st0
+
+
+def test_generic_rhs_callable(P, oracle_mod):
+    """rk_step with an arbitrary rhs_fn (not the operator's bound method)."""
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=16, ny=8, p=2))
+    op = P.SpatialOperator(setup.mesh, 2, setup.model)
+    st = op.project_state(setup.ic)
+    a = st.copy()
+    P.rk_step(a, lambda s, out: op.assemble_rhs(s, out), 10.0, P.tableau(4))
+    b = st.copy()
+    P.rk_step(b, op.assemble_rhs, 10.0, P.tableau(4))
+    x, y = a.to_numpy(), b.to_numpy()
+    for v in range(3):
+        assert rel(x, y, v) <= 1e-14
+
+
+def test_launch_counter_counts_kernels(P):
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=16, ny=8, p=2))
+    op = P.SpatialOperator(setup.mesh, 2, setup.model)
+    st = op.project_state(setup.ic)
+    n0 = op.launch_count()
+    op.ssprk3_steps(st, 10.0, 5)
+    torch.cuda.synchronize()
+    assert op.launch_count() - n0 == 15

@@ -1,0 +1,64 @@
+"""Multi-rank latitude-band SSPRK3 run (used by tests/test_gpu_parity.py).
+
+    torchrun --nproc-per-node N tools/band_run.py --transport host --out x.npy
+
+Every rank owns a band of TC6 48x16 p=3, steps it with a halo exchange per
+stage, and rank 0 gathers the owned rows into one (nz, ny, 3, nphi, nx)
+array.  ``--transport host`` lets all ranks share GPU 0 (gloo);
+``--transport p2p`` uses NCCL with one GPU per rank.
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2303_11767_b200 as P  # noqa: E402
+from paper_2303_11767_b200.bands import BandLayout, BandOperator  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--transport", default="host")
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--steps", type=int, default=4)
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    dev = 0 if args.transport == "host" else int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo" if args.transport == "host" else "nccl")
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=48, ny=16, p=3))
+    op = P.SpatialOperator(setup.mesh, 3, setup.model)
+    full = op.project_state(setup.ic).data.cpu().numpy()
+    L = BandLayout(16, world, rank)
+    bop = BandOperator(op, L, transport=args.transport)
+    u = torch.from_numpy(L.scatter(full)).cuda()
+    w1, w2 = bop.empty(), bop.empty()
+    for k in range(args.steps):
+        bop.ssprk3_step(u, w1, w2, 5.0, tag=k)
+    flags, _ = bop.status()
+    assert flags == 0, flags
+    mine = u[:, L.jlo:L.jhi].cpu().contiguous()
+    if rank == 0:
+        parts = [mine]
+        for r in range(1, world):
+            Lr = BandLayout(16, world, r)
+            buf = torch.empty((full.shape[0], Lr.owned) + full.shape[2:], dtype=torch.float64)
+            dist.recv(buf, src=r)
+            parts.append(buf)
+        np.save(args.out, torch.cat(parts, dim=1).numpy())
+    else:
+        dist.send(mine, dst=0)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
