@@ -7,21 +7,26 @@
 // through a chunk of latitude rows; every y-face is evaluated once per
 // chunk, every x-face once per strip.
 //
+// Memory pipeline: each lane streams its own element's coefficients with
+// cp.async (LDGSTS) into a two-row shared-memory ring, two rows ahead of
+// use, and the u^n tile of the current row one phase ahead; every lane
+// reads back only the words it copied, so no CTA barrier guards the ring.
+//
 // Per row, per variable and lane (n = p+1, all tensor contractions
-// sum-factorised and held in registers, constants from __constant__):
+// sum-factorised; constant tables in __constant__):
 //   1. modal -> nodal: t[a][qj] = sum_b c[a][b] P_b(x_qj),
 //      U[qi][qj] = sum_a P_a(x_qi) t[a][qj]; traces L/R from t, T/B from
 //      sum_b c[a][b](+-1)^b                          (dg.py:348-357)
 //   2. nodal values exchanged through shared memory; pointwise flux /
 //      source physics for this warp's variable      (models.py:161-252)
 //   3. face warps: Rusanov flux with local alpha    (dg.py:92-119,385-453)
-//   4. volume + source projection, boundary lifts, per-row inverse mass
-//      (Kronecker block form), fused RK stage update (dg.py:455-502,
-//      timestep.py:132-167)
+//   4. volume + source projection streamed over qi, boundary lifts,
+//      per-row inverse mass (Kronecker block form), fused RK stage update
+//      (dg.py:455-502, timestep.py:132-167)
 //
-// Floating point: FMA contraction and reciprocal-multiply are used; results
-// agree with the reference (exact-order oracle) to ~1e-15 relative per RHS
-// up to the reference's own conditioning (see tests/test_gpu_parity.py).
+// Floating point: FMA contraction and a Newton-refined reciprocal are used;
+// results agree with the reference's exact-order oracle to ~1e-15 relative
+// per step (tests/test_gpu_parity.py).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -47,7 +52,7 @@ struct StageParams {
     int nx, ny, row0, nrows;
     int j_begin, j_end, rc;   // local rows [j_begin, j_end), rc rows per CTA
     double a, b, g;       // Y = a U + b X + g RHS(X)
-    const double *rowtab; // per global row, see row_stride()
+    const double *rowtab; // per global row, see RowLayout
     double inv_r;         // 1/R
     double inv_r_cx;      // (1/R) * determ/bd_det_x
     double gravity, half_g, h_floor;
@@ -85,16 +90,21 @@ template <int P>
 struct Smem {
     static constexpr int N = P + 1;
     static constexpr int NP = N * N;
+    static constexpr int TILE = 3 * NP * kLanes;         // one row of coefficients, all vars
+    static constexpr int TR = 3 * N * kLanes;            // one trace / face-flux set
     // offsets in doubles
-    static constexpr int U = 0;                          // [3][NP][32]
-    static constexpr int XL = U + 3 * NP * kLanes;       // [3][N][32]
-    static constexpr int XR = XL + 3 * N * kLanes;
-    static constexpr int TT = XR + 3 * N * kLanes;       // top traces of current row
-    static constexpr int BB = TT + 3 * N * kLanes;       // bottom traces of next row
-    static constexpr int FX = BB + 3 * N * kLanes;       // x-face flux, right face of lane
-    static constexpr int FY0 = FX + 3 * N * kLanes;      // y-face flux buffers
-    static constexpr int FY1 = FY0 + 3 * N * kLanes;
-    static constexpr int ROW = FY1 + 3 * N * kLanes;     // row tables
+    static constexpr int XR0 = 0;                        // coefficient ring slot 0
+    static constexpr int XR1 = XR0 + TILE;               // slot 1
+    static constexpr int UN = XR1 + TILE;                // u^n tile of the current row
+    static constexpr int U = UN + TILE;                  // nodal values [3][NP][32]
+    static constexpr int XL = U + TILE;                  // [3][N][32]
+    static constexpr int XRT = XL + TR;
+    static constexpr int TT = XRT + TR;                  // top traces of current row
+    static constexpr int BB = TT + TR;                   // bottom traces of next row
+    static constexpr int FX = BB + TR;                   // x-face flux, right face of lane
+    static constexpr int FY0 = FX + TR;                  // y-face flux buffers
+    static constexpr int FY1 = FY0 + TR;
+    static constexpr int ROW = FY1 + TR;                 // row tables
     static __host__ __device__ constexpr int total(int rc) {
         return ROW + (rc + 1) * RowLayout<P>::STRIDE;
     }
@@ -102,15 +112,33 @@ struct Smem {
 
 __device__ __forceinline__ double sgn(int k) { return (k & 1) ? -1.0 : 1.0; }
 
-template <int P>
-__device__ __forceinline__ void load_tile(double (&c)[P + 1][P + 1], const double *__restrict__ src,
-                                          int nx, int i)
+// 1/x: MUFU seed + two Newton steps (<= 1 ulp for normal x)
+__device__ __forceinline__ double rcp64(double x)
 {
-    constexpr int N = P + 1;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+__device__ __forceinline__ void cp_async8(double *dst, const double *src)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// this lane's element, one variable: NP words, mode-major, lane-minor
+template <int P>
+__device__ __forceinline__ void tile_fetch(double *dst, const double *src, int nx, int i, int lane)
+{
+    constexpr int NP = (P + 1) * (P + 1);
 #pragma unroll
-    for (int a = 0; a < N; ++a)
-#pragma unroll
-        for (int b = 0; b < N; ++b) c[a][b] = __ldg(src + (size_t)(a * N + b) * nx + i);
+    for (int m = 0; m < NP; ++m) cp_async8(dst + m * kLanes + lane, src + (size_t)m * nx + i);
 }
 
 // bottom (sign -1) or top (sign +1) trace at the n edge nodes from modes
@@ -135,6 +163,16 @@ __device__ __forceinline__ void ytrace(const double (&c)[P + 1][P + 1], double (
     }
 }
 
+template <int P>
+__device__ __forceinline__ void tile_read(double (&c)[P + 1][P + 1], const double *s, int lane)
+{
+    constexpr int N = P + 1;
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int b = 0; b < N; ++b) c[a][b] = s[(a * N + b) * kLanes + lane];
+}
+
 // Interior nodal values and L/R/T traces of one variable -> shared memory.
 template <int P>
 __device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], double *sU, double *sXL,
@@ -151,16 +189,6 @@ __device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], do
 #pragma unroll
             for (int b = 0; b < N; ++b) acc = fma(c[a][b], LEG(b, q), acc);
             t[a][q] = acc;
-        }
-#pragma unroll
-    for (int qi = 0; qi < N; ++qi)
-#pragma unroll
-        for (int qj = 0; qj < N; ++qj) {
-            double acc = 0.0;
-#pragma unroll
-            for (int a = 0; a < N; ++a) acc = fma(LEG(a, qi), t[a][qj], acc);
-            sU[(qi * N + qj) * kLanes + lane] = acc;
-            if (check) bad |= !(acc > 0.0);
         }
 #pragma unroll
     for (int q = 0; q < N; ++q) {
@@ -181,6 +209,20 @@ __device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], do
         sT[q * kLanes + lane] = tt[q];
         if (check) bad |= !(tt[q] > 0.0);
     }
+#pragma unroll 1
+    for (int qi = 0; qi < N; ++qi) {
+        double pa[N];
+#pragma unroll
+        for (int a = 0; a < N; ++a) pa[a] = LEG(a, qi);
+#pragma unroll
+        for (int qj = 0; qj < N; ++qj) {
+            double acc = 0.0;
+#pragma unroll
+            for (int a = 0; a < N; ++a) acc = fma(pa[a], t[a][qj], acc);
+            sU[(qi * N + qj) * kLanes + lane] = acc;
+            if (check) bad |= !(acc > 0.0);
+        }
+    }
     return bad;
 }
 
@@ -193,28 +235,26 @@ __device__ __forceinline__ void face_flux(const double *sIn, int lin, const doub
                                           double cr_e, double cos_e, double alpha_glob)
 {
     constexpr int N = P + 1;
+    constexpr int M = DIR == 0 ? 1 : 2;   // normal momentum
     double rin[N], rout[N];
     double amax = 0.0;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         const double hi = sIn[(0 * N + k) * kLanes + lin];
-        const double mi = sIn[((DIR == 0 ? 1 : 2) * N + k) * kLanes + lin];
+        const double mi = sIn[(M * N + k) * kLanes + lin];
         const double ho = sOut[(0 * N + k) * kLanes + lout];
-        const double mo = sOut[((DIR == 0 ? 1 : 2) * N + k) * kLanes + lout];
-        rin[k] = 1.0 / fmax(hi, kp.h_floor);
-        rout[k] = 1.0 / fmax(ho, kp.h_floor);
+        const double mo = sOut[(M * N + k) * kLanes + lout];
+        rin[k] = rcp64(fmax(hi, kp.h_floor));
+        rout[k] = rcp64(fmax(ho, kp.h_floor));
         const double ci = sqrt(kp.gravity * fmax(hi, 0.0));
         const double co = sqrt(kp.gravity * fmax(ho, 0.0));
-        double ai = (fabs(mi * rin[k]) + ci) * kp.inv_r;
-        double ao = (fabs(mo * rout[k]) + co) * kp.inv_r;
-        if (DIR == 1) {
-            ai *= cos_e;
-            ao *= cos_e;
-        }
-        amax = fmax(amax, fmax(ai, ao));
+        amax = fmax(amax, fmax(fabs(mi * rin[k]) + ci, fabs(mo * rout[k]) + co));
     }
-    const double alpha = (kp.alpha_mode == 0) ? amax : alpha_glob;
+    double alpha = amax * kp.inv_r;
+    if (DIR == 1) alpha *= cos_e;
+    if (kp.alpha_mode != 0) alpha = alpha_glob;
     const double ha = 0.5 * alpha;
+    const double hs = 0.5 * (DIR == 0 ? kp.inv_r : cr_e);
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         const double hi = sIn[(0 * N + k) * kLanes + lin];
@@ -224,37 +264,38 @@ __device__ __forceinline__ void face_flux(const double *sIn, int lin, const doub
         const double uo = sOut[(1 * N + k) * kLanes + lout];
         const double vo = sOut[(2 * N + k) * kLanes + lout];
         const double gi = hi * hi * kp.half_g, go = ho * ho * kp.half_g;
-        double fi0, fi1, fi2, fo0, fo1, fo2, sc;
+        double fi0, fi1, fi2, fo0, fo1, fo2;
         if (DIR == 0) {
             const double ui_ = ui * rin[k], vi_ = vi * rin[k];
             const double uo_ = uo * rout[k], vo_ = vo * rout[k];
             fi0 = ui; fi1 = fma(ui, ui_, gi); fi2 = ui * vi_;
             fo0 = uo; fo1 = fma(uo, uo_, go); fo2 = uo * vo_;
-            sc = kp.inv_r;
         } else {
             const double vi_ = vi * rin[k], vo_ = vo * rout[k];
             fi0 = vi; fi1 = ui * vi_; fi2 = fma(vi, vi_, gi);
             fo0 = vo; fo1 = uo * vo_; fo2 = fma(vo, vo_, go);
-            sc = cr_e;
         }
-        const double hs = 0.5 * sc;
         sF[(0 * N + k) * kLanes + lane] = fma(hs, fi0 + fo0, -ha * (ho - hi));
         sF[(1 * N + k) * kLanes + lane] = fma(hs, fi1 + fo1, -ha * (uo - ui));
         sF[(2 * N + k) * kLanes + lane] = fma(hs, fi2 + fo2, -ha * (vo - vi));
     }
 }
 
-// Volume + source projection of variable V at the current row.
+// Volume + source projection of variable v at the current row, streamed
+// over the xi node index qi:
 // vol[a][b] = sum_q (cx dphi/dxi F + cy dphi/deta G + cs phi S)[q]
-template <int P, int V>
-__device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], const double *sU, const double *row,
-                                       int lane, const StageParams &kp)
+template <int P>
+__device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const double *sU,
+                                       const double *row, int lane, const StageParams &kp)
 {
     constexpr int N = P + 1;
     constexpr int NP = N * N;
     using RL = RowLayout<P>;
-    double rF[N][N], rG[N][N];   // [qi][b]
 #pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int b = 0; b < N; ++b) vol[a][b] = 0.0;
+#pragma unroll 1
     for (int qi = 0; qi < N; ++qi) {
         double F[N], G[N], S[N];
 #pragma unroll
@@ -264,25 +305,31 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], const double
             const double hu = sU[(1 * NP + q) * kLanes + lane];
             const double hv = sU[(2 * NP + q) * kLanes + lane];
             const double crc = row[RL::CRC + qj];
-            if (V == 0) {
+            if (v == 0) {
                 F[qj] = hu * kp.inv_r_cx;
                 G[qj] = hv * crc;
                 S[qj] = 0.0;
             } else {
-                const double r = 1.0 / fmax(h, kp.h_floor);
-                const double u = hu * r, v = hv * r;
+                const double r = rcp64(fmax(h, kp.h_floor));
+                const double u = hu * r, w = hv * r;
                 const double gh2 = h * h * kp.half_g;
                 const double t = fma(u, row[RL::SRS + qj], row[RL::FCS + qj]);
-                if (V == 1) {
+                if (v == 1) {
                     F[qj] = fma(hu, u, gh2) * kp.inv_r_cx;
-                    G[qj] = hu * v * crc;
+                    G[qj] = hu * w * crc;
                     S[qj] = t * hv;
                 } else {
-                    F[qj] = hu * v * kp.inv_r_cx;
-                    G[qj] = fma(hv, v, gh2) * crc;
+                    F[qj] = hu * w * kp.inv_r_cx;
+                    G[qj] = fma(hv, w, gh2) * crc;
                     S[qj] = -fma(gh2, row[RL::SRS + qj], t * hu);
                 }
             }
+        }
+        double pd[N], pp[N];
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            pd[a] = WD(a, qi);
+            pp[a] = WP(a, qi);
         }
 #pragma unroll
         for (int b = 0; b < N; ++b) {
@@ -291,77 +338,68 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], const double
             for (int qj = 0; qj < N; ++qj) {
                 f = fma(WP(b, qj), F[qj], f);
                 g = fma(WD(b, qj), G[qj], g);
-                if (V != 0) g = fma(WP(b, qj), S[qj], g);
+                g = fma(WP(b, qj), S[qj], g);
             }
-            rF[qi][b] = f;
-            rG[qi][b] = g;
+#pragma unroll
+            for (int a = 0; a < N; ++a) vol[a][b] = fma(pd[a], f, fma(pp[a], g, vol[a][b]));
         }
     }
-#pragma unroll
-    for (int a = 0; a < N; ++a)
-#pragma unroll
-        for (int b = 0; b < N; ++b) {
-            double acc = 0.0;
-#pragma unroll
-            for (int qi = 0; qi < N; ++qi) {
-                acc = fma(WD(a, qi), rF[qi][b], acc);
-                acc = fma(WP(a, qi), rG[qi][b], acc);
-            }
-            vol[a][b] = acc;
-        }
 }
 
-// Boundary lifts, inverse mass, stage combination and store for variable V.
-template <int P, int V>
-__device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const double *sFX,
-                                             const double *sFtop, const double *sFbot, bool has_top,
-                                             bool has_bot, const double *row, int lane, bool owned,
-                                             const double *__restrict__ Xv, const double *Uv,
-                                             double *Yv, int nx, int i,
+// Boundary lifts, inverse mass, stage combination and store for variable v.
+template <int P>
+__device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const double (&c)[P + 1][P + 1],
+                                             int v, const double *sFX, const double *sFtop,
+                                             const double *sFbot, bool has_top, bool has_bot,
+                                             const double *row, const double *sUn, int lane,
+                                             bool owned, double *Yv, int nx, int i,
                                              const StageParams &kp)
 {
     constexpr int N = P + 1;
     using RL = RowLayout<P>;
     const int ll = lane > 0 ? lane - 1 : 0;
-    double eR[N], eL[N], eT[N], eB[N];
+    double xe[N], xo[N], ye[N], yo[N];
 #pragma unroll
     for (int b = 0; b < N; ++b) {
         double r = 0.0, l = 0.0, t = 0.0, bo = 0.0;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-            r = fma(WP(b, k), sFX[(V * N + k) * kLanes + lane], r);
-            l = fma(WP(b, k), sFX[(V * N + k) * kLanes + ll], l);
-            if (has_top) t = fma(WP(b, k), sFtop[(V * N + k) * kLanes + lane], t);
-            if (has_bot) bo = fma(WP(b, k), sFbot[(V * N + k) * kLanes + lane], bo);
+            r = fma(WP(b, k), sFX[(v * N + k) * kLanes + lane], r);
+            l = fma(WP(b, k), sFX[(v * N + k) * kLanes + ll], l);
+            t = fma(WP(b, k), has_top ? sFtop[(v * N + k) * kLanes + lane] : 0.0, t);
+            bo = fma(WP(b, k), has_bot ? sFbot[(v * N + k) * kLanes + lane] : 0.0, bo);
         }
-        eR[b] = r * kp.bdy;
-        eL[b] = l * kp.bdy;
-        eT[b] = t * kp.bdx;
-        eB[b] = bo * kp.bdx;
+        // even / odd parity of the broadcast index
+        xe[b] = (l - r) * kp.bdy;
+        xo[b] = (-l - r) * kp.bdy;
+        ye[b] = (bo - t) * kp.bdx;
+        yo[b] = (-bo - t) * kp.bdx;
     }
-#pragma unroll
-    for (int a = 0; a < N; ++a)
-#pragma unroll
-        for (int b = 0; b < N; ++b)
-            vol[a][b] += (fma(sgn(a), eL[b], -eR[b]) + fma(sgn(b), eB[a], -eT[a]));
-    unsigned bad = 0;
     const double *T = row + RL::T;
+    double Tm[N][N];
+#pragma unroll
+    for (int b = 0; b < N; ++b)
+#pragma unroll
+        for (int bb = 0; bb < N; ++bb) Tm[b][bb] = T[b * N + bb];
+    unsigned bad = 0;
 #pragma unroll
     for (int a = 0; a < N; ++a) {
+        double w[N];
+#pragma unroll
+        for (int b = 0; b < N; ++b) w[b] = vol[a][b] + ((a & 1) ? xo[b] : xe[b]) + ((b & 1) ? yo[a] : ye[a]);
         const double ga = kp.g * (double)(2 * a + 1);
 #pragma unroll
         for (int b = 0; b < N; ++b) {
             double k = 0.0;
 #pragma unroll
-            for (int bb = 0; bb < N; ++bb) k = fma(T[b * N + bb], vol[a][bb], k);
-            const size_t off = (size_t)(a * N + b) * nx + i;
+            for (int bb = 0; bb < N; ++bb) k = fma(Tm[b][bb], w[bb], k);
             double y = ga * k;
-            if (kp.b != 0.0) y = fma(kp.b, __ldg(Xv + off), y);
-            if (kp.a != 0.0) y = fma(kp.a, Uv[off], y);
+            if (kp.b != 0.0) y = fma(kp.b, c[a][b], y);
+            if (kp.a != 0.0) y = fma(kp.a, sUn[(a * N + b) * kLanes + lane], y);
             if (owned) {
-                Yv[off] = y;
+                Yv[(size_t)(a * N + b) * nx + i] = y;
                 if (kp.check_finite && !isfinite(y)) bad |= 2u;
-                if (V == 0 && kp.check_mean && a == 0 && b == 0 && !(y > 0.0)) bad |= 4u;
+                if (v == 0 && kp.check_mean && a == 0 && b == 0 && !(y > 0.0)) bad |= 4u;
             }
         }
     }
@@ -369,7 +407,7 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
 }
 
 template <int P>
-__global__ void __launch_bounds__(kThreads) stage_kernel(StageParams kp)
+__global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(StageParams kp)
 {
     constexpr int N = P + 1;
     constexpr int NP = N * N;
@@ -388,9 +426,11 @@ __global__ void __launch_bounds__(kThreads) stage_kernel(StageParams kp)
     const int je = min(jb + kp.rc, kp.j_end);
     if (jb >= je) return;
 
+    double *ring[2] = {smem + SM::XR0 + v * NP * kLanes, smem + SM::XR1 + v * NP * kLanes};
+    double *sUn = smem + SM::UN + v * NP * kLanes;
     double *sU = smem + SM::U;
     double *sXL = smem + SM::XL;
-    double *sXR = smem + SM::XR;
+    double *sXR = smem + SM::XRT;
     double *sT = smem + SM::TT;
     double *sB = smem + SM::BB;
     double *sFX = smem + SM::FX;
@@ -398,17 +438,27 @@ __global__ void __launch_bounds__(kThreads) stage_kernel(StageParams kp)
     double *sFb = smem + SM::FY1;
     double *sRow = smem + SM::ROW;
 
+    const double *Xz = kp.X + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx;
+    const double *Uz = kp.U ? kp.U + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx : nullptr;
+    double *Yz = kp.Y + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx;
+    const bool chk = (v == 0);
+    const bool use_u = (kp.a != 0.0);
+    unsigned bad = 0;
+
+    // rows whose coefficients exist: local r with global row0+r in [0, ny)
+    const int r_last = min(kp.nrows - 1, kp.ny - 1 - kp.row0);
+
+    // prologue: start streaming rows jb and jb+1
+    tile_fetch<P>(ring[0], Xz + (size_t)jb * kp.rstride, nx, i, lane);
+    cp_commit();
+    if (jb + 1 <= min(je, r_last)) tile_fetch<P>(ring[1], Xz + (size_t)(jb + 1) * kp.rstride, nx, i, lane);
+    cp_commit();
+
     // row tables for global rows [row0+jb, min(row0+je, ny-1)]
     const int gfirst = kp.row0 + jb;
     const int glast = min(kp.row0 + je, kp.ny - 1);
     for (int idx = threadIdx.x; idx < (glast - gfirst + 1) * RL::STRIDE; idx += kThreads)
         sRow[idx] = kp.rowtab[(size_t)gfirst * RL::STRIDE + idx];
-
-    const double *Xz = kp.X + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx;
-    const double *Uz = kp.U ? kp.U + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx : nullptr;
-    double *Yz = kp.Y + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx;
-    const bool chk = (v == 0);
-    unsigned bad = 0;
 
     double alpha_x = kp.alpha, alpha_y = kp.alpha;
     if (kp.alpha_mode == 2) {
@@ -416,20 +466,25 @@ __global__ void __launch_bounds__(kThreads) stage_kernel(StageParams kp)
         alpha_y = kp.alpha_dev[1];
     }
 
-    // prologue: bottom face of the chunk's first row
-    double cn[N][N];
+    // bottom face of the chunk's first row
     const bool below = gfirst > 0;
+    double c[N][N];
     if (below) {
-        load_tile<P>(cn, Xz + (size_t)(jb - 1) * kp.rstride, nx, i);
+        const double *src = Xz + (size_t)(jb - 1) * kp.rstride;
+#pragma unroll
+        for (int a = 0; a < N; ++a)
+#pragma unroll
+            for (int b = 0; b < N; ++b) c[a][b] = __ldg(src + (size_t)(a * N + b) * nx + i);
         double tt[N];
-        ytrace<P, true>(cn, tt);
+        ytrace<P, true>(c, tt);
 #pragma unroll
         for (int q = 0; q < N; ++q) sT[(v * N + q) * kLanes + lane] = tt[q];
     }
-    load_tile<P>(cn, Xz + (size_t)jb * kp.rstride, nx, i);
+    cp_wait<1>();
     {
+        tile_read<P>(c, ring[0], lane);
         double bt[N];
-        ytrace<P, false>(cn, bt);
+        ytrace<P, false>(c, bt);
 #pragma unroll
         for (int q = 0; q < N; ++q) {
             sB[(v * N + q) * kLanes + lane] = bt[q];
@@ -437,27 +492,31 @@ __global__ void __launch_bounds__(kThreads) stage_kernel(StageParams kp)
         }
     }
     __syncthreads();
-    if (below && v == 1) {
-        const double *r = sRow;   // row jb: its bottom edge is the face latitude
-        face_flux<P, 1>(sT, lane, sB, lane, sFb, lane, kp, r[RL::CRB], r[RL::COSB], alpha_y);
-    }
+    if (below && v == 1)
+        face_flux<P, 1>(sT, lane, sB, lane, sFb, lane, kp, sRow[RL::CRB], sRow[RL::COSB], alpha_y);
     __syncthreads();
 
     for (int jl = jb; jl < je; ++jl) {
+        const int slot = (jl - jb) & 1;
         const int jg = kp.row0 + jl;
         const bool has_top = jg + 1 < kp.ny;
         const bool has_bot = jg > 0;
         const double *row = sRow + (size_t)(jl - jb) * RL::STRIDE;
-        double c[N][N];
-#pragma unroll
-        for (int a = 0; a < N; ++a)
-#pragma unroll
-            for (int b = 0; b < N; ++b) c[a][b] = cn[a][b];
-        if (has_top) load_tile<P>(cn, Xz + (size_t)(jl + 1) * kp.rstride, nx, i);
+
+        if (use_u) tile_fetch<P>(sUn, Uz + (size_t)jl * kp.rstride, nx, i, lane);
+        cp_commit();                                   // group U(jl)
+        tile_read<P>(c, ring[slot], lane);             // X(jl), landed one row ago
+        __syncwarp();
+        if (jl + 2 <= min(je, r_last))
+            tile_fetch<P>(ring[slot], Xz + (size_t)(jl + 2) * kp.rstride, nx, i, lane);
+        cp_commit();                                   // group X(jl+2)
 
         bad |= eval_row<P>(c, sU + v * NP * kLanes, sXL + v * N * kLanes, sXR + v * N * kLanes,
                            sT + v * N * kLanes, lane, chk);
+        cp_wait<2>();                                  // X(jl+1) landed
         if (has_top) {
+            double cn[N][N];
+            tile_read<P>(cn, ring[slot ^ 1], lane);
             double bt[N];
             ytrace<P, false>(cn, bt);
 #pragma unroll
@@ -468,35 +527,24 @@ __global__ void __launch_bounds__(kThreads) stage_kernel(StageParams kp)
         }
         __syncthreads();
 
-        double vol[N][N];
         if (v == 0) {
             face_flux<P, 0>(sXR, lane, sXL, min(lane + 1, 31), sFX, lane, kp, 0.0, 0.0, alpha_x);
-            volume<P, 0>(vol, sU, row, lane, kp);
-        } else if (v == 1) {
-            if (has_top) {
-                const double *rn = row + RL::STRIDE;   // row above: bottom edge = face
-                face_flux<P, 1>(sT, lane, sB, lane, sFa, lane, kp, rn[RL::CRB], rn[RL::COSB], alpha_y);
-            }
-            volume<P, 1>(vol, sU, row, lane, kp);
-        } else {
-            volume<P, 2>(vol, sU, row, lane, kp);
+        } else if (v == 1 && has_top) {
+            const double *rn = row + RL::STRIDE;   // row above: its bottom edge is the face
+            face_flux<P, 1>(sT, lane, sB, lane, sFa, lane, kp, rn[RL::CRB], rn[RL::COSB], alpha_y);
         }
+        double vol[N][N];
+        volume<P>(vol, v, sU, row, lane, kp);
+        cp_wait<1>();                                  // U(jl) landed
         __syncthreads();
 
-        const size_t roff = (size_t)jl * kp.rstride;
-        if (v == 0)
-            bad |= finalize<P, 0>(vol, sFX, sFa, sFb, has_top, has_bot, row, lane, owned, Xz + roff,
-                                  Uz ? Uz + roff : nullptr, Yz + roff, nx, i, kp);
-        else if (v == 1)
-            bad |= finalize<P, 1>(vol, sFX, sFa, sFb, has_top, has_bot, row, lane, owned, Xz + roff,
-                                  Uz ? Uz + roff : nullptr, Yz + roff, nx, i, kp);
-        else
-            bad |= finalize<P, 2>(vol, sFX, sFa, sFb, has_top, has_bot, row, lane, owned, Xz + roff,
-                                  Uz ? Uz + roff : nullptr, Yz + roff, nx, i, kp);
+        bad |= finalize<P>(vol, c, v, sFX, sFa, sFb, has_top, has_bot, row, sUn, lane, owned,
+                           Yz + (size_t)jl * kp.rstride, nx, i, kp);
         double *tmp = sFa;
         sFa = sFb;
         sFb = tmp;
     }
+    cp_wait<0>();
 
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && lane == 0) {
