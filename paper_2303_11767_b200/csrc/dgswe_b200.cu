@@ -209,6 +209,7 @@ int launch_stage(dgswe_ctx *c, double a, const double *U, double b, const double
     kp.gravity = c->cfg.gravity;
     kp.half_g = c->half_g;
     kp.h_floor = c->cfg.h_floor;
+    kp.sqrt_g = sqrt(c->cfg.gravity);
     kp.bdx = c->bdx;
     kp.bdy = c->bdy;
     kp.alpha_mode = c->cfg.alpha_mode;

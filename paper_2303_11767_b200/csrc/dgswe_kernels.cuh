@@ -1,6 +1,7 @@
 // dgswe_kernels.cuh -- fused fp64 DG shallow-water stage kernel for sm_100a.
 //
-// One CTA = 3 warps (warp v owns variable v in {h, hu, hv}) x 32 lanes.
+// One CTA = 4 warps x 32 lanes: warp v < 3 owns variable v in {h, hu, hv},
+// warp 3 evaluates the Rusanov fluxes of the row's x- and y-faces.
 // Lane l holds longitude element i0-1+l (mod nx) of a 30-element strip:
 // lanes 1..30 own their element, lanes 0 and 31 are the periodic/strip halo
 // whose traces feed the strip's two border faces.  The CTA marches north
@@ -37,7 +38,8 @@ namespace dgswe {
 constexpr int kMaxP = 6;
 constexpr int kLanes = 32;
 constexpr int kOwned = 30;   // owned elements per strip (lanes 1..30)
-constexpr int kWarps = 3;    // one per conserved variable
+constexpr int kVarWarps = 3; // one per conserved variable
+constexpr int kWarps = 4;    // + one face warp (Rusanov fluxes)
 constexpr int kThreads = kWarps * kLanes;
 
 // [p][table][a][q]: 0 P_a(x_q), 1 P'_a(x_q), 2 w_q P_a(x_q), 3 w_q P'_a(x_q)
@@ -55,7 +57,7 @@ struct StageParams {
     const double *rowtab; // per global row, see RowLayout
     double inv_r;         // 1/R
     double inv_r_cx;      // (1/R) * determ/bd_det_x
-    double gravity, half_g, h_floor;
+    double gravity, half_g, h_floor, sqrt_g;
     double bdx, bdy;      // bd_det_x, bd_det_y
     int alpha_mode;       // 0 local, 1 pinned, 2 global (from alpha_dev)
     double alpha;
@@ -95,9 +97,8 @@ struct Smem {
     // offsets in doubles
     static constexpr int XR0 = 0;                        // coefficient ring slot 0
     static constexpr int XR1 = XR0 + TILE;               // slot 1
-    static constexpr int UN = XR1 + TILE;                // u^n tile of the current row
-    static constexpr int U = UN + TILE;                  // nodal values [3][NP][32]
-    static constexpr int XL = U + TILE;                  // [3][N][32]
+    static constexpr int U = XR1 + TILE;                 // nodal [4][NP][32]: gh2 hu hv 1/hf
+    static constexpr int XL = U + 4 * NP * kLanes;       // [3][N][32]
     static constexpr int XRT = XL + TR;
     static constexpr int TT = XRT + TR;                  // top traces of current row
     static constexpr int BB = TT + TR;                   // bottom traces of next row
@@ -121,6 +122,32 @@ __device__ __forceinline__ double rcp64(double x)
     r = fma(r, e, r);
     e = fma(-x, r, 1.0);
     return fma(r, e, r);
+}
+
+// 1/sqrt(x): MUFU seed + two Newton steps (x > 0, normal)
+__device__ __forceinline__ double rsqrt64(double x)
+{
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    double e = fma(-hx * y, y, 0.5);
+    y = fma(y, e, y);
+    e = fma(-hx * y, y, 0.5);
+    return fma(y, e, y);
+}
+
+// 1/max(h, floor) and sqrt(g max(h, 0)) of one trace node from one rsqrt
+__device__ __forceinline__ void inv_and_celerity(double h, double h_floor, double sqrt_g, double g,
+                                                 double &r, double &c)
+{
+    if (h >= h_floor) {
+        const double y = rsqrt64(h);
+        r = y * y;
+        c = sqrt_g * (h * y);
+    } else {                       // below the velocity floor (never in practice)
+        r = 1.0 / h_floor;
+        c = sqrt(g * fmax(h, 0.0));
+    }
 }
 
 __device__ __forceinline__ void cp_async8(double *dst, const double *src)
@@ -156,9 +183,9 @@ __device__ __forceinline__ void ytrace(const double (&c)[P + 1][P + 1], double (
     }
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-        double acc = 0.0;
+        double acc = LEG(0, q) * s[0];
 #pragma unroll
-        for (int a = 0; a < N; ++a) acc = fma(LEG(a, q), s[a], acc);
+        for (int a = 1; a < N; ++a) acc = fma(LEG(a, q), s[a], acc);
         tr[q] = acc;
     }
 }
@@ -176,18 +203,20 @@ __device__ __forceinline__ void tile_read(double (&c)[P + 1][P + 1], const doubl
 // Interior nodal values and L/R/T traces of one variable -> shared memory.
 template <int P>
 __device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], double *sU, double *sXL,
-                                             double *sXR, double *sT, int lane, bool check)
+                                             double *sXR, double *sT, int lane, bool check,
+                                             double half_g, double h_floor)
 {
     constexpr int N = P + 1;
+    constexpr int NP = N * N;
     unsigned bad = 0;
     double t[N][N];
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
         for (int q = 0; q < N; ++q) {
-            double acc = 0.0;
+            double acc = c[a][0] * LEG(0, q);
 #pragma unroll
-            for (int b = 0; b < N; ++b) acc = fma(c[a][b], LEG(b, q), acc);
+            for (int b = 1; b < N; ++b) acc = fma(c[a][b], LEG(b, q), acc);
             t[a][q] = acc;
         }
 #pragma unroll
@@ -216,11 +245,17 @@ __device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], do
         for (int a = 0; a < N; ++a) pa[a] = LEG(a, qi);
 #pragma unroll
         for (int qj = 0; qj < N; ++qj) {
-            double acc = 0.0;
+            double acc = pa[0] * t[0][qj];
 #pragma unroll
-            for (int a = 0; a < N; ++a) acc = fma(pa[a], t[a][qj], acc);
-            sU[(qi * N + qj) * kLanes + lane] = acc;
-            if (check) bad |= !(acc > 0.0);
+            for (int a = 1; a < N; ++a) acc = fma(pa[a], t[a][qj], acc);
+            if (check) {
+                // h warp: publish g h^2/2 and 1/max(h, floor) for the momentum warps
+                bad |= !(acc > 0.0);
+                sU[(qi * N + qj) * kLanes + lane] = acc * acc * half_g;
+                sU[(3 * NP + qi * N + qj) * kLanes + lane] = rcp64(fmax(acc, h_floor));
+            } else {
+                sU[(qi * N + qj) * kLanes + lane] = acc;
+            }
         }
     }
     return bad;
@@ -244,10 +279,9 @@ __device__ __forceinline__ void face_flux(const double *sIn, int lin, const doub
         const double mi = sIn[(M * N + k) * kLanes + lin];
         const double ho = sOut[(0 * N + k) * kLanes + lout];
         const double mo = sOut[(M * N + k) * kLanes + lout];
-        rin[k] = rcp64(fmax(hi, kp.h_floor));
-        rout[k] = rcp64(fmax(ho, kp.h_floor));
-        const double ci = sqrt(kp.gravity * fmax(hi, 0.0));
-        const double co = sqrt(kp.gravity * fmax(ho, 0.0));
+        double ci, co;
+        inv_and_celerity(hi, kp.h_floor, kp.sqrt_g, kp.gravity, rin[k], ci);
+        inv_and_celerity(ho, kp.h_floor, kp.sqrt_g, kp.gravity, rout[k], co);
         amax = fmax(amax, fmax(fabs(mi * rin[k]) + ci, fabs(mo * rout[k]) + co));
     }
     double alpha = amax * kp.inv_r;
@@ -301,7 +335,6 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
 #pragma unroll
         for (int qj = 0; qj < N; ++qj) {
             const int q = qi * N + qj;
-            const double h = sU[(0 * NP + q) * kLanes + lane];
             const double hu = sU[(1 * NP + q) * kLanes + lane];
             const double hv = sU[(2 * NP + q) * kLanes + lane];
             const double crc = row[RL::CRC + qj];
@@ -310,9 +343,9 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
                 G[qj] = hv * crc;
                 S[qj] = 0.0;
             } else {
-                const double r = rcp64(fmax(h, kp.h_floor));
+                const double gh2 = sU[(0 * NP + q) * kLanes + lane];
+                const double r = sU[(3 * NP + q) * kLanes + lane];
                 const double u = hu * r, w = hv * r;
-                const double gh2 = h * h * kp.half_g;
                 const double t = fma(u, row[RL::SRS + qj], row[RL::FCS + qj]);
                 if (v == 1) {
                     F[qj] = fma(hu, u, gh2) * kp.inv_r_cx;
@@ -331,17 +364,31 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
             pd[a] = WD(a, qi);
             pp[a] = WP(a, qi);
         }
+        if (v == 0) {
 #pragma unroll
-        for (int b = 0; b < N; ++b) {
-            double f = 0.0, g = 0.0;
+            for (int b = 0; b < N; ++b) {
+                double f = WP(b, 0) * F[0], g = WD(b, 0) * G[0];
 #pragma unroll
-            for (int qj = 0; qj < N; ++qj) {
-                f = fma(WP(b, qj), F[qj], f);
-                g = fma(WD(b, qj), G[qj], g);
-                g = fma(WP(b, qj), S[qj], g);
+                for (int qj = 1; qj < N; ++qj) {
+                    f = fma(WP(b, qj), F[qj], f);
+                    g = fma(WD(b, qj), G[qj], g);
+                }
+#pragma unroll
+                for (int a = 0; a < N; ++a) vol[a][b] = fma(pd[a], f, fma(pp[a], g, vol[a][b]));
             }
+        } else {
 #pragma unroll
-            for (int a = 0; a < N; ++a) vol[a][b] = fma(pd[a], f, fma(pp[a], g, vol[a][b]));
+            for (int b = 0; b < N; ++b) {
+                double f = WP(b, 0) * F[0], g = fma(WD(b, 0), G[0], WP(b, 0) * S[0]);
+#pragma unroll
+                for (int qj = 1; qj < N; ++qj) {
+                    f = fma(WP(b, qj), F[qj], f);
+                    g = fma(WD(b, qj), G[qj], g);
+                    g = fma(WP(b, qj), S[qj], g);
+                }
+#pragma unroll
+                for (int a = 0; a < N; ++a) vol[a][b] = fma(pd[a], f, fma(pp[a], g, vol[a][b]));
+            }
         }
     }
 }
@@ -349,11 +396,11 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
 // Boundary lifts, inverse mass, stage combination and store for variable v.
 template <int P>
 __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const double (&c)[P + 1][P + 1],
-                                             int v, const double *sFX, const double *sFtop,
+                                             const double (&un)[P + 1][P + 1], int v,
+                                             const double *sFX, const double *sFtop,
                                              const double *sFbot, bool has_top, bool has_bot,
-                                             const double *row, const double *sUn, int lane,
-                                             bool owned, double *Yv, int nx, int i,
-                                             const StageParams &kp)
+                                             const double *row, int lane, bool owned, double *Yv,
+                                             int nx, int i, const StageParams &kp)
 {
     constexpr int N = P + 1;
     using RL = RowLayout<P>;
@@ -361,14 +408,20 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
     double xe[N], xo[N], ye[N], yo[N];
 #pragma unroll
     for (int b = 0; b < N; ++b) {
-        double r = 0.0, l = 0.0, t = 0.0, bo = 0.0;
+        const int o = (v * N) * kLanes;
+        double r = WP(b, 0) * sFX[o + lane];
+        double l = WP(b, 0) * sFX[o + ll];
+        double t = WP(b, 0) * sFtop[o + lane];
+        double bo = WP(b, 0) * sFbot[o + lane];
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            r = fma(WP(b, k), sFX[(v * N + k) * kLanes + lane], r);
-            l = fma(WP(b, k), sFX[(v * N + k) * kLanes + ll], l);
-            t = fma(WP(b, k), has_top ? sFtop[(v * N + k) * kLanes + lane] : 0.0, t);
-            bo = fma(WP(b, k), has_bot ? sFbot[(v * N + k) * kLanes + lane] : 0.0, bo);
+        for (int k = 1; k < N; ++k) {
+            r = fma(WP(b, k), sFX[o + k * kLanes + lane], r);
+            l = fma(WP(b, k), sFX[o + k * kLanes + ll], l);
+            t = fma(WP(b, k), sFtop[o + k * kLanes + lane], t);
+            bo = fma(WP(b, k), sFbot[o + k * kLanes + lane], bo);
         }
+        t = has_top ? t : 0.0;        // pole faces carry no flux (dg.py:483-495)
+        bo = has_bot ? bo : 0.0;
         // even / odd parity of the broadcast index
         xe[b] = (l - r) * kp.bdy;
         xo[b] = (-l - r) * kp.bdy;
@@ -390,12 +443,12 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
         const double ga = kp.g * (double)(2 * a + 1);
 #pragma unroll
         for (int b = 0; b < N; ++b) {
-            double k = 0.0;
+            double k = Tm[b][0] * w[0];
 #pragma unroll
-            for (int bb = 0; bb < N; ++bb) k = fma(Tm[b][bb], w[bb], k);
+            for (int bb = 1; bb < N; ++bb) k = fma(Tm[b][bb], w[bb], k);
             double y = ga * k;
             if (kp.b != 0.0) y = fma(kp.b, c[a][b], y);
-            if (kp.a != 0.0) y = fma(kp.a, sUn[(a * N + b) * kLanes + lane], y);
+            if (kp.a != 0.0) y = fma(kp.a, un[a][b], y);
             if (owned) {
                 Yv[(size_t)(a * N + b) * nx + i] = y;
                 if (kp.check_finite && !isfinite(y)) bad |= 2u;
@@ -414,7 +467,9 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
     using SM = Smem<P>;
     using RL = RowLayout<P>;
     extern __shared__ double smem[];
-    const int v = threadIdx.x >> 5;
+    const int warp = threadIdx.x >> 5;
+    const int v = warp < kVarWarps ? warp : 0;     // face warp borrows var 0's addressing
+    const bool face_warp = warp == kVarWarps;
     const int lane = threadIdx.x & 31;
     const int nx = kp.nx;
     const int i0 = blockIdx.x * kOwned;
@@ -426,8 +481,8 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
     const int je = min(jb + kp.rc, kp.j_end);
     if (jb >= je) return;
 
-    double *ring[2] = {smem + SM::XR0 + v * NP * kLanes, smem + SM::XR1 + v * NP * kLanes};
-    double *sUn = smem + SM::UN + v * NP * kLanes;
+    // this warp's variable in ring slot s: smem + ring0 + s * TILE
+    double *const ring0 = smem + SM::XR0 + v * NP * kLanes;
     double *sU = smem + SM::U;
     double *sXL = smem + SM::XL;
     double *sXR = smem + SM::XRT;
@@ -449,10 +504,13 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
     const int r_last = min(kp.nrows - 1, kp.ny - 1 - kp.row0);
 
     // prologue: start streaming rows jb and jb+1
-    tile_fetch<P>(ring[0], Xz + (size_t)jb * kp.rstride, nx, i, lane);
-    cp_commit();
-    if (jb + 1 <= min(je, r_last)) tile_fetch<P>(ring[1], Xz + (size_t)(jb + 1) * kp.rstride, nx, i, lane);
-    cp_commit();
+    if (!face_warp) {
+        tile_fetch<P>(ring0, Xz + (size_t)jb * kp.rstride, nx, i, lane);
+        cp_commit();
+        if (jb + 1 <= min(je, r_last))
+            tile_fetch<P>(ring0 + SM::TILE, Xz + (size_t)(jb + 1) * kp.rstride, nx, i, lane);
+        cp_commit();
+    }
 
     // row tables for global rows [row0+jb, min(row0+je, ny-1)]
     const int gfirst = kp.row0 + jb;
@@ -469,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
     // bottom face of the chunk's first row
     const bool below = gfirst > 0;
     double c[N][N];
-    if (below) {
+    if (below && !face_warp) {
         const double *src = Xz + (size_t)(jb - 1) * kp.rstride;
 #pragma unroll
         for (int a = 0; a < N; ++a)
@@ -480,9 +538,9 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
 #pragma unroll
         for (int q = 0; q < N; ++q) sT[(v * N + q) * kLanes + lane] = tt[q];
     }
-    cp_wait<1>();
-    {
-        tile_read<P>(c, ring[0], lane);
+    if (!face_warp) {
+        cp_wait<1>();
+        tile_read<P>(c, ring0, lane);
         double bt[N];
         ytrace<P, false>(c, bt);
 #pragma unroll
@@ -492,59 +550,72 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
         }
     }
     __syncthreads();
-    if (below && v == 1)
+    if (below && face_warp)
         face_flux<P, 1>(sT, lane, sB, lane, sFb, lane, kp, sRow[RL::CRB], sRow[RL::COSB], alpha_y);
     __syncthreads();
 
     for (int jl = jb; jl < je; ++jl) {
         const int slot = (jl - jb) & 1;
+        double *const cur = ring0 + slot * SM::TILE;
+        double *const nxt = ring0 + (slot ^ 1) * SM::TILE;
         const int jg = kp.row0 + jl;
         const bool has_top = jg + 1 < kp.ny;
         const bool has_bot = jg > 0;
         const double *row = sRow + (size_t)(jl - jb) * RL::STRIDE;
 
-        if (use_u) tile_fetch<P>(sUn, Uz + (size_t)jl * kp.rstride, nx, i, lane);
-        cp_commit();                                   // group U(jl)
-        tile_read<P>(c, ring[slot], lane);             // X(jl), landed one row ago
-        __syncwarp();
-        if (jl + 2 <= min(je, r_last))
-            tile_fetch<P>(ring[slot], Xz + (size_t)(jl + 2) * kp.rstride, nx, i, lane);
-        cp_commit();                                   // group X(jl+2)
+        if (!face_warp) {
+            tile_read<P>(c, cur, lane);                // X(jl), landed one row ago
+            __syncwarp();
+            if (jl + 2 <= min(je, r_last))
+                tile_fetch<P>(cur, Xz + (size_t)(jl + 2) * kp.rstride, nx, i, lane);
+            cp_commit();                               // group X(jl+2)
 
-        bad |= eval_row<P>(c, sU + v * NP * kLanes, sXL + v * N * kLanes, sXR + v * N * kLanes,
-                           sT + v * N * kLanes, lane, chk);
-        cp_wait<2>();                                  // X(jl+1) landed
-        if (has_top) {
-            double cn[N][N];
-            tile_read<P>(cn, ring[slot ^ 1], lane);
-            double bt[N];
-            ytrace<P, false>(cn, bt);
+            bad |= eval_row<P>(c, sU + v * NP * kLanes, sXL + v * N * kLanes, sXR + v * N * kLanes,
+                               sT + v * N * kLanes, lane, chk, kp.half_g, kp.h_floor);
+            cp_wait<1>();                              // X(jl+1) landed
+            if (has_top) {
+                double cn[N][N];
+                tile_read<P>(cn, nxt, lane);
+                double bt[N];
+                ytrace<P, false>(cn, bt);
 #pragma unroll
-            for (int q = 0; q < N; ++q) {
-                sB[(v * N + q) * kLanes + lane] = bt[q];
-                if (chk) bad |= !(bt[q] > 0.0);
+                for (int q = 0; q < N; ++q) {
+                    sB[(v * N + q) * kLanes + lane] = bt[q];
+                    if (chk) bad |= !(bt[q] > 0.0);
+                }
             }
         }
         __syncthreads();
 
-        if (v == 0) {
+        if (face_warp) {
             face_flux<P, 0>(sXR, lane, sXL, min(lane + 1, 31), sFX, lane, kp, 0.0, 0.0, alpha_x);
-        } else if (v == 1 && has_top) {
-            const double *rn = row + RL::STRIDE;   // row above: its bottom edge is the face
-            face_flux<P, 1>(sT, lane, sB, lane, sFa, lane, kp, rn[RL::CRB], rn[RL::COSB], alpha_y);
+            if (has_top) {
+                const double *rn = row + RL::STRIDE;   // row above: its bottom edge is the face
+                face_flux<P, 1>(sT, lane, sB, lane, sFa, lane, kp, rn[RL::CRB], rn[RL::COSB],
+                                alpha_y);
+            }
+            __syncthreads();
+        } else {
+            // u^n of this row: plain loads (U may alias Y), consumed in finalize
+            double un[N][N];
+            if (use_u) {
+                const double *src = Uz + (size_t)jl * kp.rstride;
+#pragma unroll
+                for (int a = 0; a < N; ++a)
+#pragma unroll
+                    for (int b = 0; b < N; ++b) un[a][b] = src[(size_t)(a * N + b) * nx + i];
+            }
+            double vol[N][N];
+            volume<P>(vol, v, sU, row, lane, kp);
+            __syncthreads();
+            bad |= finalize<P>(vol, c, un, v, sFX, sFa, sFb, has_top, has_bot, row, lane, owned,
+                               Yz + (size_t)jl * kp.rstride, nx, i, kp);
         }
-        double vol[N][N];
-        volume<P>(vol, v, sU, row, lane, kp);
-        cp_wait<1>();                                  // U(jl) landed
-        __syncthreads();
-
-        bad |= finalize<P>(vol, c, v, sFX, sFa, sFb, has_top, has_bot, row, sUn, lane, owned,
-                           Yz + (size_t)jl * kp.rstride, nx, i, kp);
         double *tmp = sFa;
         sFa = sFb;
         sFb = tmp;
     }
-    cp_wait<0>();
+    if (!face_warp) cp_wait<0>();
 
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && lane == 0) {
