@@ -150,6 +150,7 @@ struct dgswe_ctx {
     int external_alpha = 0;
     long long launches = 0;
     int device = 0;
+    int sms = 148;
     std::map<GraphKey, cudaGraphExec_t> graphs;
     // derived scalars
     double inv_r, inv_r_cx, half_g, bdx, bdy;
@@ -163,16 +164,40 @@ int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, c
     using SM = dgswe::Smem<P>;
     const int rows = r1 - r0;
     if (rows <= 0) return DGSWE_OK;
-    const size_t smem = (size_t)SM::total(kp.rc) * sizeof(double);
-    static bool attr_set[64] = {};
-    int dev = c->device;
-    if (!attr_set[dev & 63]) {
-        CUDA_TRY(cudaFuncSetAttribute(dgswe::stage_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(SM::total(32) * sizeof(double))));
-        attr_set[dev & 63] = true;
+    const size_t smem = (size_t)SM::TOTAL * sizeof(double);
+    static int occ[64][2] = {};     // resident CTAs per SM, per device and variant
+    const int dev = c->device & 63;
+    const int variant = kp.U ? 1 : 0;
+    if (!occ[dev][variant]) {
+        CUDA_TRY(cudaFuncSetAttribute(dgswe::stage_kernel<P, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(cudaFuncSetAttribute(dgswe::stage_kernel<P, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int o1 = 0, o0 = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, dgswe::stage_kernel<P, true>,
+                                                               dgswe::kThreads, smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o0, dgswe::stage_kernel<P, false>,
+                                                               dgswe::kThreads, smem));
+        occ[dev][1] = o1 > 0 ? o1 : 1;
+        occ[dev][0] = o0 > 0 ? o0 : 1;
     }
-    dim3 grid((c->cfg.nx + dgswe::kOwned - 1) / dgswe::kOwned, (rows + kp.rc - 1) / kp.rc, c->cfg.nz);
-    dgswe::stage_kernel<P><<<grid, dgswe::kThreads, smem, s>>>(kp);
+    // one wave: split every (strip, level) column of rows into as many
+    // contiguous chunks as the resident CTA slots allow
+    const int strips = (c->cfg.nx + dgswe::kOwned - 1) / dgswe::kOwned;
+    int rc = kp.rc;
+    if (rc <= 0) {
+        const long long slots = (long long)c->sms * occ[dev][variant];
+        long long chunks = slots / ((long long)strips * c->cfg.nz);
+        if (chunks < 1) chunks = 1;
+        rc = (int)((rows + chunks - 1) / chunks);
+    }
+    dgswe::StageParams kq = kp;
+    kq.rc = rc;
+    dim3 grid(strips, (rows + rc - 1) / rc, c->cfg.nz);
+    if (kq.U)
+        dgswe::stage_kernel<P, true><<<grid, dgswe::kThreads, smem, s>>>(kq);
+    else
+        dgswe::stage_kernel<P, false><<<grid, dgswe::kThreads, smem, s>>>(kq);
     CUDA_TRY(cudaGetLastError());
     c->launches += 1;
     return DGSWE_OK;
@@ -297,19 +322,10 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
     ctx->inv_r_cx = ctx->inv_r * cx;
     ctx->half_g = 0.5 * c.gravity;
 
-    // automatic rows per CTA: aim for >= ~8 CTAs of 96 threads per SM
-    if (c.row_chunk > 0) {
-        ctx->rc = c.row_chunk;
-    } else {
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-        const long long strips = (c.nx + dgswe::kOwned - 1) / dgswe::kOwned;
-        const long long rows = c.jhi - c.jlo;
-        long long rc = strips * rows * c.nz / ((long long)sms * 8);
-        if (const char *env = getenv("DGSWE_ROW_CHUNK")) rc = atoi(env);
-        ctx->rc = (int)(rc < 2 ? 2 : (rc > 16 ? 16 : rc));
-    }
-    if (ctx->rc > 32) ctx->rc = 32;
+    // rows per CTA: fixed, or 0 = sized at launch so the grid is one wave
+    cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    ctx->rc = c.row_chunk > 0 ? c.row_chunk : 0;
+    if (const char *env = getenv("DGSWE_ROW_CHUNK")) ctx->rc = atoi(env);
 
     // constant tables for this degree
     static double tab[4][dgswe::kMaxP + 1][dgswe::kMaxP + 1];

@@ -105,10 +105,8 @@ struct Smem {
     static constexpr int FX = BB + TR;                   // x-face flux, right face of lane
     static constexpr int FY0 = FX + TR;                  // y-face flux buffers
     static constexpr int FY1 = FY0 + TR;
-    static constexpr int ROW = FY1 + TR;                 // row tables
-    static __host__ __device__ constexpr int total(int rc) {
-        return ROW + (rc + 1) * RowLayout<P>::STRIDE;
-    }
+    static constexpr int ROW = FY1 + TR;                 // row-table ring, 3 rows
+    static constexpr int TOTAL = ROW + 3 * RowLayout<P>::STRIDE;
 };
 
 __device__ __forceinline__ double sgn(int k) { return (k & 1) ? -1.0 : 1.0; }
@@ -136,18 +134,15 @@ __device__ __forceinline__ double rsqrt64(double x)
     return fma(y, e, y);
 }
 
-// 1/max(h, floor) and sqrt(g max(h, 0)) of one trace node from one rsqrt
-__device__ __forceinline__ void inv_and_celerity(double h, double h_floor, double sqrt_g, double g,
-                                                 double &r, double &c)
+// 1/hf and sqrt(g hf) with hf = max(h, floor) from one rsqrt; equals the
+// reference's sqrt(g max(h, 0)) whenever h >= floor (callers fix the rest)
+__device__ __forceinline__ void inv_and_celerity(double h, double h_floor, double sqrt_g, double &r,
+                                                 double &c)
 {
-    if (h >= h_floor) {
-        const double y = rsqrt64(h);
-        r = y * y;
-        c = sqrt_g * (h * y);
-    } else {                       // below the velocity floor (never in practice)
-        r = 1.0 / h_floor;
-        c = sqrt(g * fmax(h, 0.0));
-    }
+    const double hf = fmax(h, h_floor);
+    const double y = rsqrt64(hf);
+    r = y * y;
+    c = sqrt_g * (hf * y);
 }
 
 __device__ __forceinline__ void cp_async8(double *dst, const double *src)
@@ -273,6 +268,7 @@ __device__ __forceinline__ void face_flux(const double *sIn, int lin, const doub
     constexpr int M = DIR == 0 ? 1 : 2;   // normal momentum
     double rin[N], rout[N];
     double amax = 0.0;
+    bool low = false;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         const double hi = sIn[(0 * N + k) * kLanes + lin];
@@ -280,9 +276,22 @@ __device__ __forceinline__ void face_flux(const double *sIn, int lin, const doub
         const double ho = sOut[(0 * N + k) * kLanes + lout];
         const double mo = sOut[(M * N + k) * kLanes + lout];
         double ci, co;
-        inv_and_celerity(hi, kp.h_floor, kp.sqrt_g, kp.gravity, rin[k], ci);
-        inv_and_celerity(ho, kp.h_floor, kp.sqrt_g, kp.gravity, rout[k], co);
+        inv_and_celerity(hi, kp.h_floor, kp.sqrt_g, rin[k], ci);
+        inv_and_celerity(ho, kp.h_floor, kp.sqrt_g, rout[k], co);
+        low |= (hi < kp.h_floor) | (ho < kp.h_floor);
         amax = fmax(amax, fmax(fabs(mi * rin[k]) + ci, fabs(mo * rout[k]) + co));
+    }
+    if (__any_sync(0xffffffffu, low)) {      // h below the velocity floor: exact celerity
+        amax = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            const double hi = sIn[(0 * N + k) * kLanes + lin];
+            const double mi = sIn[(M * N + k) * kLanes + lin];
+            const double ho = sOut[(0 * N + k) * kLanes + lout];
+            const double mo = sOut[(M * N + k) * kLanes + lout];
+            amax = fmax(amax, fmax(fabs(mi * rin[k]) + sqrt(kp.gravity * fmax(hi, 0.0)),
+                                   fabs(mo * rout[k]) + sqrt(kp.gravity * fmax(ho, 0.0))));
+        }
     }
     double alpha = amax * kp.inv_r;
     if (DIR == 1) alpha *= cos_e;
@@ -394,7 +403,7 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
 }
 
 // Boundary lifts, inverse mass, stage combination and store for variable v.
-template <int P>
+template <int P, bool HAS_U>
 __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const double (&c)[P + 1][P + 1],
                                              const double (&un)[P + 1][P + 1], int v,
                                              const double *sFX, const double *sFtop,
@@ -434,7 +443,8 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
     for (int b = 0; b < N; ++b)
 #pragma unroll
         for (int bb = 0; bb < N; ++bb) Tm[b][bb] = T[b * N + bb];
-    unsigned bad = 0;
+    double fin = 0.0;                 // NaN iff some output is not finite
+    double mean = 1.0;
 #pragma unroll
     for (int a = 0; a < N; ++a) {
         double w[N];
@@ -446,20 +456,22 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
             double k = Tm[b][0] * w[0];
 #pragma unroll
             for (int bb = 1; bb < N; ++bb) k = fma(Tm[b][bb], w[bb], k);
-            double y = ga * k;
-            if (kp.b != 0.0) y = fma(kp.b, c[a][b], y);
-            if (kp.a != 0.0) y = fma(kp.a, un[a][b], y);
-            if (owned) {
-                Yv[(size_t)(a * N + b) * nx + i] = y;
-                if (kp.check_finite && !isfinite(y)) bad |= 2u;
-                if (v == 0 && kp.check_mean && a == 0 && b == 0 && !(y > 0.0)) bad |= 4u;
-            }
+            double y = fma(kp.b, c[a][b], ga * k);
+            if (HAS_U) y = fma(kp.a, un[a][b], y);
+            if (owned) Yv[(size_t)(a * N + b) * nx + i] = y;
+            fin += y - y;
+            if (a == 0 && b == 0) mean = y;
         }
+    }
+    unsigned bad = 0;
+    if (owned) {
+        bad |= (kp.check_finite && !(fin == fin)) ? 2u : 0u;
+        bad |= (v == 0 && kp.check_mean && !(mean > 0.0)) ? 4u : 0u;
     }
     return bad;
 }
 
-template <int P>
+template <int P, bool HAS_U>
 __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(StageParams kp)
 {
     constexpr int N = P + 1;
@@ -497,7 +509,6 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
     const double *Uz = kp.U ? kp.U + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx : nullptr;
     double *Yz = kp.Y + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx;
     const bool chk = (v == 0);
-    const bool use_u = (kp.a != 0.0);
     unsigned bad = 0;
 
     // rows whose coefficients exist: local r with global row0+r in [0, ny)
@@ -512,11 +523,14 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
         cp_commit();
     }
 
-    // row tables for global rows [row0+jb, min(row0+je, ny-1)]
+    // row-table ring: slot (r - jb) % 3 holds local row r (rows jb, jb+1 now,
+    // row jl+2 staged by the face warp during iteration jl)
     const int gfirst = kp.row0 + jb;
-    const int glast = min(kp.row0 + je, kp.ny - 1);
-    for (int idx = threadIdx.x; idx < (glast - gfirst + 1) * RL::STRIDE; idx += kThreads)
-        sRow[idx] = kp.rowtab[(size_t)gfirst * RL::STRIDE + idx];
+    {
+        const int nload = min(2, kp.ny - gfirst);
+        for (int idx = threadIdx.x; idx < nload * RL::STRIDE; idx += kThreads)
+            sRow[idx] = kp.rowtab[(size_t)gfirst * RL::STRIDE + idx];
+    }
 
     double alpha_x = kp.alpha, alpha_y = kp.alpha;
     if (kp.alpha_mode == 2) {
@@ -561,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
         const int jg = kp.row0 + jl;
         const bool has_top = jg + 1 < kp.ny;
         const bool has_bot = jg > 0;
-        const double *row = sRow + (size_t)(jl - jb) * RL::STRIDE;
+        const double *row = sRow + ((jl - jb) % 3) * RL::STRIDE;
 
         if (!face_warp) {
             tile_read<P>(c, cur, lane);                // X(jl), landed one row ago
@@ -590,15 +604,22 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
         if (face_warp) {
             face_flux<P, 0>(sXR, lane, sXL, min(lane + 1, 31), sFX, lane, kp, 0.0, 0.0, alpha_x);
             if (has_top) {
-                const double *rn = row + RL::STRIDE;   // row above: its bottom edge is the face
+                // row above: its bottom edge is the face
+                const double *rn = sRow + ((jl + 1 - jb) % 3) * RL::STRIDE;
                 face_flux<P, 1>(sT, lane, sB, lane, sFa, lane, kp, rn[RL::CRB], rn[RL::COSB],
                                 alpha_y);
+            }
+            // stage the table of row jl+2 (its slot held row jl-1, no longer read)
+            if (jl + 2 < je + 1 && jg + 2 < kp.ny) {
+                double *dst = sRow + ((jl + 2 - jb) % 3) * RL::STRIDE;
+                const double *src = kp.rowtab + (size_t)(jg + 2) * RL::STRIDE;
+                for (int idx = lane; idx < RL::STRIDE; idx += kLanes) dst[idx] = src[idx];
             }
             __syncthreads();
         } else {
             // u^n of this row: plain loads (U may alias Y), consumed in finalize
             double un[N][N];
-            if (use_u) {
+            if (HAS_U) {
                 const double *src = Uz + (size_t)jl * kp.rstride;
 #pragma unroll
                 for (int a = 0; a < N; ++a)
@@ -608,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
             double vol[N][N];
             volume<P>(vol, v, sU, row, lane, kp);
             __syncthreads();
-            bad |= finalize<P>(vol, c, un, v, sFX, sFa, sFb, has_top, has_bot, row, lane, owned,
+            bad |= finalize<P, HAS_U>(vol, c, un, v, sFX, sFa, sFb, has_top, has_bot, row, lane, owned,
                                Yz + (size_t)jl * kp.rstride, nx, i, kp);
         }
         double *tmp = sFa;
