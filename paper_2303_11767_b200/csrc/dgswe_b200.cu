@@ -151,6 +151,7 @@ struct dgswe_ctx {
     long long launches = 0;
     int device = 0;
     int sms = 148;
+    int smem_pad = 0;             // experiment knob: extra dynamic smem per CTA
     std::map<GraphKey, cudaGraphExec_t> graphs;
     // derived scalars
     double inv_r, inv_r_cx, half_g, bdx, bdy;
@@ -164,8 +165,13 @@ int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, c
     using SM = dgswe::Smem<P>;
     const int rows = r1 - r0;
     if (rows <= 0) return DGSWE_OK;
-    const size_t smem = (size_t)SM::TOTAL * sizeof(double);
+    const size_t smem = (size_t)SM::TOTAL * sizeof(double) + (size_t)c->smem_pad;
     static int occ[64][2] = {};     // resident CTAs per SM, per device and variant
+    static size_t occ_smem[64] = {};
+    if (occ_smem[c->device & 63] != smem) {
+        occ[c->device & 63][0] = occ[c->device & 63][1] = 0;
+        occ_smem[c->device & 63] = smem;
+    }
     const int dev = c->device & 63;
     const int variant = kp.U ? 1 : 0;
     if (!occ[dev][variant]) {
@@ -326,6 +332,7 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
     cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, ctx->device);
     ctx->rc = c.row_chunk > 0 ? c.row_chunk : 0;
     if (const char *env = getenv("DGSWE_ROW_CHUNK")) ctx->rc = atoi(env);
+    if (const char *env = getenv("DGSWE_SMEM_PAD")) ctx->smem_pad = atoi(env);
 
     // constant tables for this degree
     static double tab[4][dgswe::kMaxP + 1][dgswe::kMaxP + 1];

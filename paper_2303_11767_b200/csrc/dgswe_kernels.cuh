@@ -97,12 +97,11 @@ struct Smem {
     // offsets in doubles
     static constexpr int XR0 = 0;                        // coefficient ring slot 0
     static constexpr int XR1 = XR0 + TILE;               // slot 1
-    static constexpr int U = XR1 + TILE;                 // nodal [4][NP][32]: gh2 hu hv 1/hf
-    static constexpr int XL = U + 4 * NP * kLanes;       // [3][N][32]
+    static constexpr int U = XR1 + TILE;                 // nodal values [3][NP][32]
+    static constexpr int XL = U + TILE;                  // [3][N][32]
     static constexpr int XRT = XL + TR;
     static constexpr int TT = XRT + TR;                  // top traces of current row
-    static constexpr int BB = TT + TR;                   // bottom traces of next row
-    static constexpr int FX = BB + TR;                   // x-face flux, right face of lane
+    static constexpr int FX = TT + TR;                   // x-face flux, right face of lane
     static constexpr int FY0 = FX + TR;                  // y-face flux buffers
     static constexpr int FY1 = FY0 + TR;
     static constexpr int ROW = FY1 + TR;                 // row-table ring, 3 rows
@@ -198,11 +197,9 @@ __device__ __forceinline__ void tile_read(double (&c)[P + 1][P + 1], const doubl
 // Interior nodal values and L/R/T traces of one variable -> shared memory.
 template <int P>
 __device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], double *sU, double *sXL,
-                                             double *sXR, double *sT, int lane, bool check,
-                                             double half_g, double h_floor)
+                                             double *sXR, double *sT, int lane, bool check)
 {
     constexpr int N = P + 1;
-    constexpr int NP = N * N;
     unsigned bad = 0;
     double t[N][N];
 #pragma unroll
@@ -243,24 +240,19 @@ __device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], do
             double acc = pa[0] * t[0][qj];
 #pragma unroll
             for (int a = 1; a < N; ++a) acc = fma(pa[a], t[a][qj], acc);
-            if (check) {
-                // h warp: publish g h^2/2 and 1/max(h, floor) for the momentum warps
-                bad |= !(acc > 0.0);
-                sU[(qi * N + qj) * kLanes + lane] = acc * acc * half_g;
-                sU[(3 * NP + qi * N + qj) * kLanes + lane] = rcp64(fmax(acc, h_floor));
-            } else {
-                sU[(qi * N + qj) * kLanes + lane] = acc;
-            }
+            sU[(qi * N + qj) * kLanes + lane] = acc;
+            if (check) bad |= !(acc > 0.0);
         }
     }
     return bad;
 }
 
-// Rusanov flux over one face: "in" = lower/left element, "out" = upper/right.
+// Rusanov flux over one face from register traces: "in" = lower/left
+// element, "out" = upper/right element, [var][node].
 // DIR 0: x-face, physical flux F, alpha = (|u|+c)/R.
 // DIR 1: y-face, physical flux G = cos/R * (...), alpha = cos (|v|+c)/R.
 template <int P, int DIR>
-__device__ __forceinline__ void face_flux(const double *sIn, int lin, const double *sOut, int lout,
+__device__ __forceinline__ void face_flux(const double (&in)[3][P + 1], const double (&out)[3][P + 1],
                                           double *sF, int lane, const StageParams &kp,
                                           double cr_e, double cos_e, double alpha_glob)
 {
@@ -271,27 +263,18 @@ __device__ __forceinline__ void face_flux(const double *sIn, int lin, const doub
     bool low = false;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-        const double hi = sIn[(0 * N + k) * kLanes + lin];
-        const double mi = sIn[(M * N + k) * kLanes + lin];
-        const double ho = sOut[(0 * N + k) * kLanes + lout];
-        const double mo = sOut[(M * N + k) * kLanes + lout];
         double ci, co;
-        inv_and_celerity(hi, kp.h_floor, kp.sqrt_g, rin[k], ci);
-        inv_and_celerity(ho, kp.h_floor, kp.sqrt_g, rout[k], co);
-        low |= (hi < kp.h_floor) | (ho < kp.h_floor);
-        amax = fmax(amax, fmax(fabs(mi * rin[k]) + ci, fabs(mo * rout[k]) + co));
+        inv_and_celerity(in[0][k], kp.h_floor, kp.sqrt_g, rin[k], ci);
+        inv_and_celerity(out[0][k], kp.h_floor, kp.sqrt_g, rout[k], co);
+        low |= (in[0][k] < kp.h_floor) | (out[0][k] < kp.h_floor);
+        amax = fmax(amax, fmax(fabs(in[M][k] * rin[k]) + ci, fabs(out[M][k] * rout[k]) + co));
     }
     if (__any_sync(0xffffffffu, low)) {      // h below the velocity floor: exact celerity
         amax = 0.0;
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            const double hi = sIn[(0 * N + k) * kLanes + lin];
-            const double mi = sIn[(M * N + k) * kLanes + lin];
-            const double ho = sOut[(0 * N + k) * kLanes + lout];
-            const double mo = sOut[(M * N + k) * kLanes + lout];
-            amax = fmax(amax, fmax(fabs(mi * rin[k]) + sqrt(kp.gravity * fmax(hi, 0.0)),
-                                   fabs(mo * rout[k]) + sqrt(kp.gravity * fmax(ho, 0.0))));
-        }
+        for (int k = 0; k < N; ++k)
+            amax = fmax(amax, fmax(fabs(in[M][k] * rin[k]) + sqrt(kp.gravity * fmax(in[0][k], 0.0)),
+                                   fabs(out[M][k] * rout[k]) + sqrt(kp.gravity * fmax(out[0][k], 0.0))));
     }
     double alpha = amax * kp.inv_r;
     if (DIR == 1) alpha *= cos_e;
@@ -300,12 +283,8 @@ __device__ __forceinline__ void face_flux(const double *sIn, int lin, const doub
     const double hs = 0.5 * (DIR == 0 ? kp.inv_r : cr_e);
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-        const double hi = sIn[(0 * N + k) * kLanes + lin];
-        const double ui = sIn[(1 * N + k) * kLanes + lin];
-        const double vi = sIn[(2 * N + k) * kLanes + lin];
-        const double ho = sOut[(0 * N + k) * kLanes + lout];
-        const double uo = sOut[(1 * N + k) * kLanes + lout];
-        const double vo = sOut[(2 * N + k) * kLanes + lout];
+        const double hi = in[0][k], ui = in[1][k], vi = in[2][k];
+        const double ho = out[0][k], uo = out[1][k], vo = out[2][k];
         const double gi = hi * hi * kp.half_g, go = ho * ho * kp.half_g;
         double fi0, fi1, fi2, fo0, fo1, fo2;
         if (DIR == 0) {
@@ -322,6 +301,42 @@ __device__ __forceinline__ void face_flux(const double *sIn, int lin, const doub
         sF[(1 * N + k) * kLanes + lane] = fma(hs, fi1 + fo1, -ha * (uo - ui));
         sF[(2 * N + k) * kLanes + lane] = fma(hs, fi2 + fo2, -ha * (vo - vi));
     }
+}
+
+template <int P>
+__device__ __forceinline__ void traces_from_smem(double (&tr)[3][P + 1], const double *s, int lane)
+{
+    constexpr int N = P + 1;
+#pragma unroll
+    for (int v = 0; v < 3; ++v)
+#pragma unroll
+        for (int k = 0; k < N; ++k) tr[v][k] = s[(v * N + k) * kLanes + lane];
+}
+
+// Face warp: bottom traces of the row above (from the coefficient ring,
+// all three variables) -> y-face flux with the current row's top traces.
+template <int P>
+__device__ __forceinline__ unsigned yface_from_ring(const double *ring_row, const double *sT,
+                                                    double *sF, int lane, const StageParams &kp,
+                                                    const double *rowtab_above, double alpha_y)
+{
+    constexpr int N = P + 1;
+    constexpr int NP = N * N;
+    using RL = RowLayout<P>;
+    double bt[3][N];
+#pragma unroll
+    for (int v = 0; v < 3; ++v) {
+        double cv[N][N];
+        tile_read<P>(cv, ring_row + v * NP * kLanes, lane);
+        ytrace<P, false>(cv, bt[v]);
+    }
+    unsigned bad = 0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) bad |= !(bt[0][k] > 0.0);
+    double tt[3][N];
+    traces_from_smem<P>(tt, sT, lane);
+    face_flux<P, 1>(tt, bt, sF, lane, kp, rowtab_above[RL::CRB], rowtab_above[RL::COSB], alpha_y);
+    return bad;
 }
 
 // Volume + source projection of variable v at the current row, streamed
@@ -352,8 +367,9 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
                 G[qj] = hv * crc;
                 S[qj] = 0.0;
             } else {
-                const double gh2 = sU[(0 * NP + q) * kLanes + lane];
-                const double r = sU[(3 * NP + q) * kLanes + lane];
+                const double h = sU[(0 * NP + q) * kLanes + lane];
+                const double r = rcp64(fmax(h, kp.h_floor));
+                const double gh2 = h * h * kp.half_g;
                 const double u = hu * r, w = hv * r;
                 const double t = fma(u, row[RL::SRS + qj], row[RL::FCS + qj]);
                 if (v == 1) {
@@ -403,18 +419,25 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
 }
 
 // Boundary lifts, inverse mass, stage combination and store for variable v.
+// The mass block is applied column by column (one row of T from shared
+// memory at a time) so that vol, c and u^n are the only tiles held.
 template <int P, bool HAS_U>
 __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const double (&c)[P + 1][P + 1],
-                                             const double (&un)[P + 1][P + 1], int v,
-                                             const double *sFX, const double *sFtop,
-                                             const double *sFbot, bool has_top, bool has_bot,
-                                             const double *row, int lane, bool owned, double *Yv,
-                                             int nx, int i, const StageParams &kp)
+                                             const double *Uv, int v, const double *sFX,
+                                             const double *sFtop, const double *sFbot, bool has_top,
+                                             bool has_bot, const double *row, int lane, bool owned,
+                                             double *Yv, int nx, int i, const StageParams &kp)
 {
     constexpr int N = P + 1;
     using RL = RowLayout<P>;
+    double un[N][N];
+    if (HAS_U) {                       // u^n: plain loads (U may alias Y)
+#pragma unroll
+        for (int a = 0; a < N; ++a)
+#pragma unroll
+            for (int b = 0; b < N; ++b) un[a][b] = Uv[(size_t)(a * N + b) * nx + i];
+    }
     const int ll = lane > 0 ? lane - 1 : 0;
-    double xe[N], xo[N], ye[N], yo[N];
 #pragma unroll
     for (int b = 0; b < N; ++b) {
         const int o = (v * N) * kLanes;
@@ -431,32 +454,29 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
         }
         t = has_top ? t : 0.0;        // pole faces carry no flux (dg.py:483-495)
         bo = has_bot ? bo : 0.0;
-        // even / odd parity of the broadcast index
-        xe[b] = (l - r) * kp.bdy;
-        xo[b] = (-l - r) * kp.bdy;
-        ye[b] = (bo - t) * kp.bdx;
-        yo[b] = (-bo - t) * kp.bdx;
+        // x lifts broadcast along a (parity of a), y lifts along b (parity of b)
+        const double xe = (l - r) * kp.bdy, xo = (-l - r) * kp.bdy;
+        const double ye = (bo - t) * kp.bdx, yo = (-bo - t) * kp.bdx;
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            vol[a][b] += (a & 1) ? xo : xe;   // x lift: column b
+            vol[b][a] += (a & 1) ? yo : ye;   // y lift of row b: column a parity
+        }
     }
     const double *T = row + RL::T;
-    double Tm[N][N];
-#pragma unroll
-    for (int b = 0; b < N; ++b)
-#pragma unroll
-        for (int bb = 0; bb < N; ++bb) Tm[b][bb] = T[b * N + bb];
     double fin = 0.0;                 // NaN iff some output is not finite
     double mean = 1.0;
 #pragma unroll
-    for (int a = 0; a < N; ++a) {
-        double w[N];
+    for (int b = 0; b < N; ++b) {
+        double tb[N];
 #pragma unroll
-        for (int b = 0; b < N; ++b) w[b] = vol[a][b] + ((a & 1) ? xo[b] : xe[b]) + ((b & 1) ? yo[a] : ye[a]);
-        const double ga = kp.g * (double)(2 * a + 1);
+        for (int bb = 0; bb < N; ++bb) tb[bb] = T[b * N + bb];
 #pragma unroll
-        for (int b = 0; b < N; ++b) {
-            double k = Tm[b][0] * w[0];
+        for (int a = 0; a < N; ++a) {
+            double k = tb[0] * vol[a][0];
 #pragma unroll
-            for (int bb = 1; bb < N; ++bb) k = fma(Tm[b][bb], w[bb], k);
-            double y = fma(kp.b, c[a][b], ga * k);
+            for (int bb = 1; bb < N; ++bb) k = fma(tb[bb], vol[a][bb], k);
+            double y = fma(kp.b, c[a][b], (kp.g * (double)(2 * a + 1)) * k);
             if (HAS_U) y = fma(kp.a, un[a][b], y);
             if (owned) Yv[(size_t)(a * N + b) * nx + i] = y;
             fin += y - y;
@@ -472,7 +492,7 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
 }
 
 template <int P, bool HAS_U>
-__global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(StageParams kp)
+__global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(StageParams kp)
 {
     constexpr int N = P + 1;
     constexpr int NP = N * N;
@@ -493,13 +513,13 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
     const int je = min(jb + kp.rc, kp.j_end);
     if (jb >= je) return;
 
-    // this warp's variable in ring slot s: smem + ring0 + s * TILE
-    double *const ring0 = smem + SM::XR0 + v * NP * kLanes;
+    // coefficient ring: slot s holds row (jb + s) mod 2, layout [var][mode][lane]
+    double *const ringS = smem + SM::XR0;
+    double *const ring0 = ringS + v * NP * kLanes;   // this warp's variable
     double *sU = smem + SM::U;
     double *sXL = smem + SM::XL;
     double *sXR = smem + SM::XRT;
     double *sT = smem + SM::TT;
-    double *sB = smem + SM::BB;
     double *sFX = smem + SM::FX;
     double *sFa = smem + SM::FY0;
     double *sFb = smem + SM::FY1;
@@ -508,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
     const double *Xz = kp.X + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx;
     const double *Uz = kp.U ? kp.U + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx : nullptr;
     double *Yz = kp.Y + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx;
-    const bool chk = (v == 0);
+    const bool chk = (v == 0) && !face_warp;
     unsigned bad = 0;
 
     // rows whose coefficients exist: local r with global row0+r in [0, ny)
@@ -538,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
         alpha_y = kp.alpha_dev[1];
     }
 
-    // bottom face of the chunk's first row
+    // top traces of the row below the chunk (its first row's bottom face)
     const bool below = gfirst > 0;
     double c[N][N];
     if (below && !face_warp) {
@@ -552,26 +572,28 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
 #pragma unroll
         for (int q = 0; q < N; ++q) sT[(v * N + q) * kLanes + lane] = tt[q];
     }
-    if (!face_warp) {
-        cp_wait<1>();
-        tile_read<P>(c, ring0, lane);
-        double bt[N];
-        ytrace<P, false>(c, bt);
-#pragma unroll
-        for (int q = 0; q < N; ++q) {
-            sB[(v * N + q) * kLanes + lane] = bt[q];
-            if (chk) bad |= !(bt[q] > 0.0);
-        }
+    if (!face_warp) cp_wait<1>();                    // row jb landed (own copies)
+    __syncthreads();
+    if (face_warp) {
+        if (below)
+            bad |= yface_from_ring<P>(ringS, sT, sFb, lane, kp, sRow, alpha_y);
+        else
+            bad |= 0u;
     }
     __syncthreads();
-    if (below && face_warp)
-        face_flux<P, 1>(sT, lane, sB, lane, sFb, lane, kp, sRow[RL::CRB], sRow[RL::COSB], alpha_y);
-    __syncthreads();
+    if (face_warp && !below) {
+        // no bottom face, but the first row's bottom traces still need the positivity check
+        double cv[N][N];
+        tile_read<P>(cv, ringS, lane);
+        double bt[N];
+        ytrace<P, false>(cv, bt);
+#pragma unroll
+        for (int k = 0; k < N; ++k) bad |= !(bt[k] > 0.0);
+    }
 
     for (int jl = jb; jl < je; ++jl) {
         const int slot = (jl - jb) & 1;
         double *const cur = ring0 + slot * SM::TILE;
-        double *const nxt = ring0 + (slot ^ 1) * SM::TILE;
         const int jg = kp.row0 + jl;
         const bool has_top = jg + 1 < kp.ny;
         const bool has_bot = jg > 0;
@@ -583,54 +605,36 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 3 : 2)) stage_kernel(Stage
             if (jl + 2 <= min(je, r_last))
                 tile_fetch<P>(cur, Xz + (size_t)(jl + 2) * kp.rstride, nx, i, lane);
             cp_commit();                               // group X(jl+2)
-
             bad |= eval_row<P>(c, sU + v * NP * kLanes, sXL + v * N * kLanes, sXR + v * N * kLanes,
-                               sT + v * N * kLanes, lane, chk, kp.half_g, kp.h_floor);
-            cp_wait<1>();                              // X(jl+1) landed
-            if (has_top) {
-                double cn[N][N];
-                tile_read<P>(cn, nxt, lane);
-                double bt[N];
-                ytrace<P, false>(cn, bt);
-#pragma unroll
-                for (int q = 0; q < N; ++q) {
-                    sB[(v * N + q) * kLanes + lane] = bt[q];
-                    if (chk) bad |= !(bt[q] > 0.0);
-                }
-            }
+                               sT + v * N * kLanes, lane, chk);
+            cp_wait<1>();                              // X(jl+1) landed (own copies)
         }
         __syncthreads();
 
         if (face_warp) {
-            face_flux<P, 0>(sXR, lane, sXL, min(lane + 1, 31), sFX, lane, kp, 0.0, 0.0, alpha_x);
-            if (has_top) {
-                // row above: its bottom edge is the face
-                const double *rn = sRow + ((jl + 1 - jb) % 3) * RL::STRIDE;
-                face_flux<P, 1>(sT, lane, sB, lane, sFa, lane, kp, rn[RL::CRB], rn[RL::COSB],
-                                alpha_y);
+            {
+                double in[3][N], out[3][N];
+                traces_from_smem<P>(in, sXR, lane);
+                traces_from_smem<P>(out, sXL, min(lane + 1, 31));
+                face_flux<P, 0>(in, out, sFX, lane, kp, 0.0, 0.0, alpha_x);
             }
+            if (has_top)
+                bad |= yface_from_ring<P>(ringS + (slot ^ 1) * SM::TILE, sT, sFa, lane, kp,
+                                          sRow + ((jl + 1 - jb) % 3) * RL::STRIDE, alpha_y);
             // stage the table of row jl+2 (its slot held row jl-1, no longer read)
-            if (jl + 2 < je + 1 && jg + 2 < kp.ny) {
+            if (jl + 2 <= je && jg + 2 < kp.ny) {
                 double *dst = sRow + ((jl + 2 - jb) % 3) * RL::STRIDE;
                 const double *src = kp.rowtab + (size_t)(jg + 2) * RL::STRIDE;
                 for (int idx = lane; idx < RL::STRIDE; idx += kLanes) dst[idx] = src[idx];
             }
             __syncthreads();
         } else {
-            // u^n of this row: plain loads (U may alias Y), consumed in finalize
-            double un[N][N];
-            if (HAS_U) {
-                const double *src = Uz + (size_t)jl * kp.rstride;
-#pragma unroll
-                for (int a = 0; a < N; ++a)
-#pragma unroll
-                    for (int b = 0; b < N; ++b) un[a][b] = src[(size_t)(a * N + b) * nx + i];
-            }
             double vol[N][N];
             volume<P>(vol, v, sU, row, lane, kp);
             __syncthreads();
-            bad |= finalize<P, HAS_U>(vol, c, un, v, sFX, sFa, sFb, has_top, has_bot, row, lane, owned,
-                               Yz + (size_t)jl * kp.rstride, nx, i, kp);
+            const size_t roff = (size_t)jl * kp.rstride;
+            bad |= finalize<P, HAS_U>(vol, c, HAS_U ? Uz + roff : nullptr, v, sFX, sFa, sFb, has_top,
+                                      has_bot, row, lane, owned, Yz + roff, nx, i, kp);
         }
         double *tmp = sFa;
         sFa = sFb;
