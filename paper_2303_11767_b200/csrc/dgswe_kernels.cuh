@@ -153,6 +153,20 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// L2 prefetch of one variable's modes for elements [lo, hi) of a row
+// (bulk async prefetch, one mode per lane)
+template <int P>
+__device__ __forceinline__ void row_prefetch_l2(const double *src, int nx, int lo, int hi, int lane)
+{
+    constexpr int NP = (P + 1) * (P + 1);
+    for (int m = lane; m < NP; m += kLanes) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(src + (size_t)m * nx + lo) & ~(uintptr_t)15;
+        const uintptr_t e = (reinterpret_cast<uintptr_t>(src + (size_t)m * nx + hi) + 15) & ~(uintptr_t)15;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a))
+                     : "memory");
+    }
+}
+
 // this lane's element, one variable: NP words, mode-major, lane-minor
 template <int P>
 __device__ __forceinline__ void tile_fetch(double *dst, const double *src, int nx, int i, int lane)
@@ -422,7 +436,7 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
 // The mass block is applied column by column (one row of T from shared
 // memory at a time) so that vol, c and u^n are the only tiles held.
 template <int P, bool HAS_U>
-__device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const double (&c)[P + 1][P + 1],
+__device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const double *cur,
                                              const double *Uv, int v, const double *sFX,
                                              const double *sFtop, const double *sFbot, bool has_top,
                                              bool has_bot, const double *row, int lane, bool owned,
@@ -476,7 +490,7 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
             double k = tb[0] * vol[a][0];
 #pragma unroll
             for (int bb = 1; bb < N; ++bb) k = fma(tb[bb], vol[a][bb], k);
-            double y = fma(kp.b, c[a][b], (kp.g * (double)(2 * a + 1)) * k);
+            double y = fma(kp.b, cur[(a * N + b) * kLanes + lane], (kp.g * (double)(2 * a + 1)) * k);
             if (HAS_U) y = fma(kp.a, un[a][b], y);
             if (owned) Yv[(size_t)(a * N + b) * nx + i] = y;
             fin += y - y;
@@ -529,6 +543,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
     const double *Uz = kp.U ? kp.U + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx : nullptr;
     double *Yz = kp.Y + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx;
     const bool chk = (v == 0) && !face_warp;
+    const int plo = max(i0 - 1, 0), phi = min(i0 + kLanes - 1, nx);   // prefetch range
     unsigned bad = 0;
 
     // rows whose coefficients exist: local r with global row0+r in [0, ny)
@@ -572,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
 #pragma unroll
         for (int q = 0; q < N; ++q) sT[(v * N + q) * kLanes + lane] = tt[q];
     }
-    if (!face_warp) cp_wait<1>();                    // row jb landed (own copies)
+    if (!face_warp) cp_wait<1>();                    // row jb landed (own copies); jb+1 in flight
     __syncthreads();
     if (face_warp) {
         if (below)
@@ -600,14 +615,14 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
         const double *row = sRow + ((jl - jb) % 3) * RL::STRIDE;
 
         if (!face_warp) {
-            tile_read<P>(c, cur, lane);                // X(jl), landed one row ago
-            __syncwarp();
+            // warm L2 for this row's u^n and for row jl+2 (copied in after finalize)
+            if (HAS_U) row_prefetch_l2<P>(Uz + (size_t)jl * kp.rstride, nx, plo, phi, lane);
             if (jl + 2 <= min(je, r_last))
-                tile_fetch<P>(cur, Xz + (size_t)(jl + 2) * kp.rstride, nx, i, lane);
-            cp_commit();                               // group X(jl+2)
+                row_prefetch_l2<P>(Xz + (size_t)(jl + 2) * kp.rstride, nx, plo, phi, lane);
+            tile_read<P>(c, cur, lane);                // X(jl)
             bad |= eval_row<P>(c, sU + v * NP * kLanes, sXL + v * N * kLanes, sXR + v * N * kLanes,
                                sT + v * N * kLanes, lane, chk);
-            cp_wait<1>();                              // X(jl+1) landed (own copies)
+            cp_wait<0>();                              // X(jl+1) landed (own copies)
         }
         __syncthreads();
 
@@ -633,8 +648,13 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
             volume<P>(vol, v, sU, row, lane, kp);
             __syncthreads();
             const size_t roff = (size_t)jl * kp.rstride;
-            bad |= finalize<P, HAS_U>(vol, c, HAS_U ? Uz + roff : nullptr, v, sFX, sFa, sFb, has_top,
-                                      has_bot, row, lane, owned, Yz + roff, nx, i, kp);
+            bad |= finalize<P, HAS_U>(vol, cur, HAS_U ? Uz + roff : nullptr, v, sFX, sFa, sFb,
+                                      has_top, has_bot, row, lane, owned, Yz + roff, nx, i, kp);
+            // X(jl) is consumed: stream row jl+2 into its slot (L2-warm by now)
+            __syncwarp();
+            if (jl + 2 <= min(je, r_last))
+                tile_fetch<P>(cur, Xz + (size_t)(jl + 2) * kp.rstride, nx, i, lane);
+            cp_commit();
         }
         double *tmp = sFa;
         sFa = sFb;
