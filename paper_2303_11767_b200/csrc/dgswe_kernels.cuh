@@ -492,7 +492,7 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
             for (int bb = 1; bb < N; ++bb) k = fma(tb[bb], vol[a][bb], k);
             double y = fma(kp.b, cur[(a * N + b) * kLanes + lane], (kp.g * (double)(2 * a + 1)) * k);
             if (HAS_U) y = fma(kp.a, un[a][b], y);
-            if (owned) Yv[(size_t)(a * N + b) * nx + i] = y;
+            if (owned) Yv[(a * N + b) * nx] = y;
             fin += y - y;
             if (a == 0 && b == 0) mean = y;
         }
@@ -513,9 +513,12 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
     using SM = Smem<P>;
     using RL = RowLayout<P>;
     extern __shared__ double smem[];
-    const int warp = threadIdx.x >> 5;
-    const int v = warp < kVarWarps ? warp : 0;     // face warp borrows var 0's addressing
-    const bool face_warp = warp == kVarWarps;
+    // fixed roles: warp w runs on sub-partition w of its SM, so every
+    // sub-partition executes a single code path (better I-cache locality
+    // than rotating roles across CTAs, measured)
+    const int role = threadIdx.x >> 5;
+    const int v = role < kVarWarps ? role : 0;     // face warp borrows var 0's addressing
+    const bool face_warp = role == kVarWarps;
     const int lane = threadIdx.x & 31;
     const int nx = kp.nx;
     const int i0 = blockIdx.x * kOwned;
@@ -649,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
             __syncthreads();
             const size_t roff = (size_t)jl * kp.rstride;
             bad |= finalize<P, HAS_U>(vol, cur, HAS_U ? Uz + roff : nullptr, v, sFX, sFa, sFb,
-                                      has_top, has_bot, row, lane, owned, Yz + roff, nx, i, kp);
+                                      has_top, has_bot, row, lane, owned, Yz + roff + i, nx, i, kp);
             // X(jl) is consumed: stream row jl+2 into its slot (L2-warm by now)
             __syncwarp();
             if (jl + 2 <= min(je, r_last))
