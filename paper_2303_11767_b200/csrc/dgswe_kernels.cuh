@@ -262,13 +262,17 @@ __device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], do
 }
 
 // Rusanov flux over one face from register traces: "in" = lower/left
-// element, "out" = upper/right element, [var][node].
+// element, "out" = upper/right element, [var][node].  Stored is the face's
+// boundary-integral projection g[var][k'] = scale * sum_k w_k P_k'(x_k) f*[k]
+// (dg.py:206-212, 465-495): both neighbours lift it with their own
+// outward-normal sign and mode parity, so each face is projected once.
 // DIR 0: x-face, physical flux F, alpha = (|u|+c)/R.
 // DIR 1: y-face, physical flux G = cos/R * (...), alpha = cos (|v|+c)/R.
 template <int P, int DIR>
 __device__ __forceinline__ void face_flux(const double (&in)[3][P + 1], const double (&out)[3][P + 1],
                                           double *sF, int lane, const StageParams &kp,
-                                          double cr_e, double cos_e, double alpha_glob)
+                                          double cr_e, double cos_e, double alpha_glob,
+                                          double scale)
 {
     constexpr int N = P + 1;
     constexpr int M = DIR == 0 ? 1 : 2;   // normal momentum
@@ -295,6 +299,7 @@ __device__ __forceinline__ void face_flux(const double (&in)[3][P + 1], const do
     if (kp.alpha_mode != 0) alpha = alpha_glob;
     const double ha = 0.5 * alpha;
     const double hs = 0.5 * (DIR == 0 ? kp.inv_r : cr_e);
+    double fs[3][N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         const double hi = in[0][k], ui = in[1][k], vi = in[2][k];
@@ -311,10 +316,19 @@ __device__ __forceinline__ void face_flux(const double (&in)[3][P + 1], const do
             fi0 = vi; fi1 = ui * vi_; fi2 = fma(vi, vi_, gi);
             fo0 = vo; fo1 = uo * vo_; fo2 = fma(vo, vo_, go);
         }
-        sF[(0 * N + k) * kLanes + lane] = fma(hs, fi0 + fo0, -ha * (ho - hi));
-        sF[(1 * N + k) * kLanes + lane] = fma(hs, fi1 + fo1, -ha * (uo - ui));
-        sF[(2 * N + k) * kLanes + lane] = fma(hs, fi2 + fo2, -ha * (vo - vi));
+        fs[0][k] = fma(hs, fi0 + fo0, -ha * (ho - hi));
+        fs[1][k] = fma(hs, fi1 + fo1, -ha * (uo - ui));
+        fs[2][k] = fma(hs, fi2 + fo2, -ha * (vo - vi));
     }
+#pragma unroll
+    for (int v = 0; v < 3; ++v)
+#pragma unroll
+        for (int b = 0; b < N; ++b) {
+            double g = WP(b, 0) * fs[v][0];
+#pragma unroll
+            for (int k = 1; k < N; ++k) g = fma(WP(b, k), fs[v][k], g);
+            sF[(v * N + b) * kLanes + lane] = g * scale;
+        }
 }
 
 template <int P>
@@ -349,7 +363,8 @@ __device__ __forceinline__ unsigned yface_from_ring(const double *ring_row, cons
     for (int k = 0; k < N; ++k) bad |= !(bt[0][k] > 0.0);
     double tt[3][N];
     traces_from_smem<P>(tt, sT, lane);
-    face_flux<P, 1>(tt, bt, sF, lane, kp, rowtab_above[RL::CRB], rowtab_above[RL::COSB], alpha_y);
+    face_flux<P, 1>(tt, bt, sF, lane, kp, rowtab_above[RL::CRB], rowtab_above[RL::COSB], alpha_y,
+                    kp.bdx);
     return bad;
 }
 
@@ -452,25 +467,17 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
             for (int b = 0; b < N; ++b) un[a][b] = Uv[(size_t)(a * N + b) * nx + i];
     }
     const int ll = lane > 0 ? lane - 1 : 0;
+    const int o = (v * N) * kLanes;
 #pragma unroll
     for (int b = 0; b < N; ++b) {
-        const int o = (v * N) * kLanes;
-        double r = WP(b, 0) * sFX[o + lane];
-        double l = WP(b, 0) * sFX[o + ll];
-        double t = WP(b, 0) * sFtop[o + lane];
-        double bo = WP(b, 0) * sFbot[o + lane];
-#pragma unroll
-        for (int k = 1; k < N; ++k) {
-            r = fma(WP(b, k), sFX[o + k * kLanes + lane], r);
-            l = fma(WP(b, k), sFX[o + k * kLanes + ll], l);
-            t = fma(WP(b, k), sFtop[o + k * kLanes + lane], t);
-            bo = fma(WP(b, k), sFbot[o + k * kLanes + lane], bo);
-        }
-        t = has_top ? t : 0.0;        // pole faces carry no flux (dg.py:483-495)
-        bo = has_bot ? bo : 0.0;
+        // projected face lifts (bdy / bdx folded in by the face warp)
+        const double r = sFX[o + b * kLanes + lane];
+        const double l = sFX[o + b * kLanes + ll];
+        const double t = has_top ? sFtop[o + b * kLanes + lane] : 0.0;   // pole faces carry
+        const double bo = has_bot ? sFbot[o + b * kLanes + lane] : 0.0;  // no flux (dg.py:483-495)
         // x lifts broadcast along a (parity of a), y lifts along b (parity of b)
-        const double xe = (l - r) * kp.bdy, xo = (-l - r) * kp.bdy;
-        const double ye = (bo - t) * kp.bdx, yo = (-bo - t) * kp.bdx;
+        const double xe = l - r, xo = -l - r;
+        const double ye = bo - t, yo = -bo - t;
 #pragma unroll
         for (int a = 0; a < N; ++a) {
             vol[a][b] += (a & 1) ? xo : xe;   // x lift: column b
@@ -634,7 +641,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
                 double in[3][N], out[3][N];
                 traces_from_smem<P>(in, sXR, lane);
                 traces_from_smem<P>(out, sXL, min(lane + 1, 31));
-                face_flux<P, 0>(in, out, sFX, lane, kp, 0.0, 0.0, alpha_x);
+                face_flux<P, 0>(in, out, sFX, lane, kp, 0.0, 0.0, alpha_x, kp.bdy);
             }
             if (has_top)
                 bad |= yface_from_ring<P>(ringS + (slot ^ 1) * SM::TILE, sT, sFa, lane, kp,

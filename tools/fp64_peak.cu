@@ -91,8 +91,10 @@ float timeit(F launch)
     return best;
 }
 
+int main_mixed();
 int main()
 {
+    main_mixed();
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int blocks = sms * 8, threads = 256;
@@ -113,5 +115,54 @@ int main()
     printf("{\"kernel\": \"dmma_m16n8k16\", \"tflops\": %.2f, \"ms\": %.3f}\n", fl / ms / 1e9, ms);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) printf("{\"error\": \"%s\"}\n", cudaGetErrorString(e));
+    return 0;
+}
+
+// --- concurrency probe: DFMA warps and DMMA warps in the same kernel ---
+__global__ void mixed_kernel(double *out, int iters, int mode)
+{
+    // mode 0: all warps DFMA, 1: all DMMA, 2: even warps DFMA / odd warps DMMA
+    const int w = threadIdx.x >> 5;
+    const bool do_mma = mode == 1 || (mode == 2 && (w & 1));
+    double s = 0;
+    if (do_mma) {
+        double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+        double c[4][2] = {};
+        for (int k = 0; k < iters; ++k) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                             : "+d"(c[u][0]), "+d"(c[u][1]) : "d"(a), "d"(b));
+        }
+        for (int u = 0; u < 4; ++u) s += c[u][0] + c[u][1];
+    } else {
+        double x[8];
+        for (int q = 0; q < 8; ++q) x[q] = threadIdx.x + q;
+        // 8 lanes-FMA per thread x 16 x 8 = same FMA count per iteration as 4 DMMA/warp
+        for (int k = 0; k < iters; ++k) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int q = 0; q < 8; ++q) x[q] = fma(x[q], 0.999, 1e-3);
+        }
+        for (int q = 0; q < 8; ++q) s += x[q];
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+int main_mixed()
+{
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int blocks = sms * 8, threads = 256;
+    double *out;
+    cudaMalloc(&out, sizeof(double) * blocks * threads);
+    const int it = 4096;
+    for (int mode = 0; mode < 3; ++mode) {
+        float ms = timeit([&] { mixed_kernel<<<blocks, threads>>>(out, it, mode); });
+        // per warp per iteration: DFMA warp = 32 lanes x 32 FMA = 1024 FMA; DMMA warp = 4 x 256 = 1024 FMA
+        double fl = 2.0 * 1024.0 * (blocks * threads / 32) * (double)it;
+        printf("{\"kernel\": \"mixed_mode%d\", \"tflops\": %.2f, \"ms\": %.3f}\n", mode, fl / ms / 1e9, ms);
+    }
     return 0;
 }
