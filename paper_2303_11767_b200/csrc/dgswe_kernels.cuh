@@ -1,7 +1,8 @@
 // dgswe_kernels.cuh -- fused fp64 DG shallow-water stage kernel for sm_100a.
 //
-// One CTA = 4 warps x 32 lanes: warp v < 3 owns variable v in {h, hu, hv},
-// warp 3 evaluates the Rusanov fluxes of the row's x- and y-faces.
+// One CTA = 4 warps x 32 lanes: warp v < 3 owns variable v in {h, hu, hv};
+// warp 0 (lightest physics) also evaluates the row's x-face fluxes and
+// warp 3 (the face warp) the bottom traces of the row above and the y-face.
 // Lane l holds longitude element i0-1+l (mod nx) of a 30-element strip:
 // lanes 1..30 own their element, lanes 0 and 31 are the periodic/strip halo
 // whose traces feed the strip's two border faces.  The CTA marches north
@@ -637,12 +638,6 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
         __syncthreads();
 
         if (face_warp) {
-            {
-                double in[3][N], out[3][N];
-                traces_from_smem<P>(in, sXR, lane);
-                traces_from_smem<P>(out, sXL, min(lane + 1, 31));
-                face_flux<P, 0>(in, out, sFX, lane, kp, 0.0, 0.0, alpha_x, kp.bdy);
-            }
             if (has_top)
                 bad |= yface_from_ring<P>(ringS + (slot ^ 1) * SM::TILE, sT, sFa, lane, kp,
                                           sRow + ((jl + 1 - jb) % 3) * RL::STRIDE, alpha_y);
@@ -654,6 +649,13 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
             }
             __syncthreads();
         } else {
+            if (v == 0) {
+                // the h warp has the lightest volume work: it takes the x-faces
+                double in[3][N], out[3][N];
+                traces_from_smem<P>(in, sXR, lane);
+                traces_from_smem<P>(out, sXL, min(lane + 1, 31));
+                face_flux<P, 0>(in, out, sFX, lane, kp, 0.0, 0.0, alpha_x, kp.bdy);
+            }
             double vol[N][N];
             volume<P>(vol, v, sU, row, lane, kp);
             __syncthreads();
