@@ -89,6 +89,125 @@ __host__ __device__ inline int row_stride(int p) { return 3 * (p + 1) + 2 + (p +
 #define WP(a, q) c_tab[P][2][a][q]
 #define WD(a, q) c_tab[P][3][a][q]
 
+// Gauss nodes are exactly antisymmetric (numpy's leggauss symmetrises them)
+// and the Legendre recurrences are odd/even in x, so the tables satisfy
+//   T(a, N-1-q) = (-1)^(a + PAR) T(a, q)   exactly,
+// PAR = 0 for P and wP, 1 for P' and wP'.  Every 1-D contraction below
+// uses this even/odd split: N adds + N*ceil(N/2) FMA instead of N*N.
+template <int TAB>
+struct TabPar {
+    static constexpr int v = (TAB == 1 || TAB == 3) ? 1 : 0;
+};
+
+// sum over a = S, S+2, ... < N of T(a, q) in[a]
+template <int P, int TAB, int S>
+__device__ __forceinline__ double dot_step2(const double (&in)[P + 1], int q)
+{
+    double acc = c_tab[P][TAB][S][q] * in[S];
+#pragma unroll
+    for (int a = S + 2; a < P + 1; a += 2) acc = fma(c_tab[P][TAB][a][q], in[a], acc);
+    return acc;
+}
+
+// modes -> nodes: out[q] = sum_a T(a, q) in[a]
+template <int P, int TAB>
+__device__ __forceinline__ void m2n(const double (&in)[P + 1], double (&out)[P + 1])
+{
+    constexpr int N = P + 1, H = N / 2, PAR = TabPar<TAB>::v;
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+        const double e = dot_step2<P, TAB, 0>(in, q);
+        const double o = dot_step2<P, TAB, 1>(in, q);
+        out[q] = e + o;
+        out[N - 1 - q] = PAR == 0 ? e - o : o - e;
+    }
+    if constexpr (N & 1) {   // middle node x = 0: only (a + PAR) even survives
+        if constexpr (PAR == 0)
+            out[H] = dot_step2<P, TAB, 0>(in, H);
+        else if constexpr (N > 1)
+            out[H] = dot_step2<P, TAB, 1>(in, H);
+        else
+            out[H] = 0.0;
+    }
+}
+
+// node-pair folds of a nodal line: ip[q] = x[q] + x[N-1-q], im[q] = x[q] - x[N-1-q]
+template <int P>
+__device__ __forceinline__ void fold(const double (&x)[P + 1], double (&ip)[(P + 1) / 2],
+                                     double (&im)[(P + 1) / 2])
+{
+    constexpr int N = P + 1;
+#pragma unroll
+    for (int q = 0; q < N / 2; ++q) {
+        ip[q] = x[q] + x[N - 1 - q];
+        im[q] = x[q] - x[N - 1 - q];
+    }
+}
+
+// nodes -> modes: out[b] = sum_q T(b, q) x[q], from the folds of x
+template <int P, int TAB>
+__device__ __forceinline__ double n2m_one(const double *ip, const double *im, const double (&x)[P + 1],
+                                          int b)
+{
+    constexpr int N = P + 1, H = N / 2, PAR = TabPar<TAB>::v;
+    const bool sym = ((b + PAR) & 1) == 0;
+    double acc = 0.0;
+    if constexpr (H > 0) {
+        acc = c_tab[P][TAB][b][0] * (sym ? ip[0] : im[0]);
+#pragma unroll
+        for (int q = 1; q < H; ++q) acc = fma(c_tab[P][TAB][b][q], sym ? ip[q] : im[q], acc);
+        if constexpr (N & 1)
+            if (sym) acc = fma(c_tab[P][TAB][b][H], x[H], acc);
+    } else {
+        if (sym) acc = c_tab[P][TAB][b][0] * x[0];
+    }
+    return acc;
+}
+
+template <int P, int TAB>
+__device__ __forceinline__ void n2m(const double (&x)[P + 1], double (&out)[P + 1])
+{
+    constexpr int N = P + 1, H = N / 2;
+    double ip[H > 0 ? H : 1], im[H > 0 ? H : 1];
+    if constexpr (H > 0) fold<P>(x, ip, im);
+#pragma unroll
+    for (int b = 0; b < N; ++b) out[b] = n2m_one<P, TAB>(ip, im, x, b);
+}
+
+// out[b] = sum_q TA(b, q) x[q] + TB(b, q) y[q] in one accumulation chain
+template <int P, int TA, int TB>
+__device__ __forceinline__ void n2m2(const double (&x)[P + 1], const double (&y)[P + 1],
+                                     double (&out)[P + 1])
+{
+    constexpr int N = P + 1, H = N / 2;
+    double xp[H > 0 ? H : 1], xm[H > 0 ? H : 1], yp[H > 0 ? H : 1], ym[H > 0 ? H : 1];
+    if constexpr (H > 0) {
+        fold<P>(x, xp, xm);
+        fold<P>(y, yp, ym);
+    }
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+        const bool sx = ((b + TabPar<TA>::v) & 1) == 0, sy = ((b + TabPar<TB>::v) & 1) == 0;
+        double acc = 0.0;
+        bool first = true;
+#pragma unroll
+        for (int q = 0; q < H; ++q) {
+            acc = first ? c_tab[P][TA][b][q] * (sx ? xp[q] : xm[q])
+                        : fma(c_tab[P][TA][b][q], sx ? xp[q] : xm[q], acc);
+            first = false;
+            acc = fma(c_tab[P][TB][b][q], sy ? yp[q] : ym[q], acc);
+        }
+        if constexpr (N & 1) {
+            if (sx) {
+                acc = first ? c_tab[P][TA][b][H] * x[H] : fma(c_tab[P][TA][b][H], x[H], acc);
+                first = false;
+            }
+            if (sy) acc = first ? c_tab[P][TB][b][H] * y[H] : fma(c_tab[P][TB][b][H], y[H], acc);
+        }
+        out[b] = acc;
+    }
+}
+
 template <int P>
 struct Smem {
     static constexpr int N = P + 1;
@@ -154,18 +273,17 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// L2 prefetch of one variable's modes for elements [lo, hi) of a row
-// (bulk async prefetch, one mode per lane)
+// L2 prefetch of this lane's element of one variable (one mode per
+// instruction; the warp's 32 lanes cover the strip's lines).  Per-lane
+// prefetch.global.L2 rather than cp.async.bulk.prefetch, whose uniform
+// operands made the compiler serialise the lanes (ncu: 11% of issue slots).
 template <int P>
-__device__ __forceinline__ void row_prefetch_l2(const double *src, int nx, int lo, int hi, int lane)
+__device__ __forceinline__ void row_prefetch_l2(const double *src, int nx, int i)
 {
     constexpr int NP = (P + 1) * (P + 1);
-    for (int m = lane; m < NP; m += kLanes) {
-        const uintptr_t a = reinterpret_cast<uintptr_t>(src + (size_t)m * nx + lo) & ~(uintptr_t)15;
-        const uintptr_t e = (reinterpret_cast<uintptr_t>(src + (size_t)m * nx + hi) + 15) & ~(uintptr_t)15;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a))
-                     : "memory");
-    }
+    const double *p = src + i;
+#pragma unroll
+    for (int m = 0; m < NP; ++m, p += nx) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 // this lane's element, one variable: NP words, mode-major, lane-minor
@@ -185,18 +303,19 @@ __device__ __forceinline__ void ytrace(const double (&c)[P + 1][P + 1], double (
     double s[N];
 #pragma unroll
     for (int a = 0; a < N; ++a) {
-        double acc = c[a][0];
+        double e = c[a][0], o = 0.0;
 #pragma unroll
-        for (int b = 1; b < N; ++b) acc = TOP ? acc + c[a][b] : fma(sgn(b), c[a][b], acc);
-        s[a] = acc;
+        for (int b = 2; b < N; b += 2) e += c[a][b];
+        if constexpr (N > 1) {
+            o = c[a][1];
+#pragma unroll
+            for (int b = 3; b < N; b += 2) o += c[a][b];
+            s[a] = TOP ? e + o : e - o;
+        } else {
+            s[a] = e;
+        }
     }
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-        double acc = LEG(0, q) * s[0];
-#pragma unroll
-        for (int a = 1; a < N; ++a) acc = fma(LEG(a, q), s[a], acc);
-        tr[q] = acc;
-    }
+    m2n<P, 0>(s, tr);
 }
 
 template <int P>
@@ -216,24 +335,20 @@ __device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], do
 {
     constexpr int N = P + 1;
     unsigned bad = 0;
-    double t[N][N];
+    double t[N][N];   // t[a][qj] = sum_b c[a][b] P_b(x_qj)
 #pragma unroll
-    for (int a = 0; a < N; ++a)
+    for (int a = 0; a < N; ++a) m2n<P, 0>(c[a], t[a]);
 #pragma unroll
-        for (int q = 0; q < N; ++q) {
-            double acc = c[a][0] * LEG(0, q);
+    for (int q = 0; q < N; ++q) {   // xi = -1 / +1 traces: parity of a
+        double e = t[0][q], o = 0.0;
 #pragma unroll
-            for (int b = 1; b < N; ++b) acc = fma(c[a][b], LEG(b, q), acc);
-            t[a][q] = acc;
+        for (int a = 2; a < N; a += 2) e += t[a][q];
+        if constexpr (N > 1) {
+            o = t[1][q];
+#pragma unroll
+            for (int a = 3; a < N; a += 2) o += t[a][q];
         }
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-        double l = t[0][q], r = t[0][q];
-#pragma unroll
-        for (int a = 1; a < N; ++a) {
-            r += t[a][q];
-            l = fma(sgn(a), t[a][q], l);
-        }
+        const double l = e - o, r = e + o;
         sXL[q * kLanes + lane] = l;
         sXR[q * kLanes + lane] = r;
         if (check) bad |= !(l > 0.0) | !(r > 0.0);
@@ -245,18 +360,16 @@ __device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], do
         sT[q * kLanes + lane] = tt[q];
         if (check) bad |= !(tt[q] > 0.0);
     }
-#pragma unroll 1
-    for (int qi = 0; qi < N; ++qi) {
-        double pa[N];
 #pragma unroll
-        for (int a = 0; a < N; ++a) pa[a] = LEG(a, qi);
+    for (int qj = 0; qj < N; ++qj) {
+        double col[N], u[N];
 #pragma unroll
-        for (int qj = 0; qj < N; ++qj) {
-            double acc = pa[0] * t[0][qj];
+        for (int a = 0; a < N; ++a) col[a] = t[a][qj];
+        m2n<P, 0>(col, u);
 #pragma unroll
-            for (int a = 1; a < N; ++a) acc = fma(pa[a], t[a][qj], acc);
-            sU[(qi * N + qj) * kLanes + lane] = acc;
-            if (check) bad |= !(acc > 0.0);
+        for (int qi = 0; qi < N; ++qi) {
+            sU[(qi * N + qj) * kLanes + lane] = u[qi];
+            if (check) bad |= !(u[qi] > 0.0);
         }
     }
     return bad;
@@ -298,8 +411,9 @@ __device__ __forceinline__ void face_flux(const double (&in)[3][P + 1], const do
     double alpha = amax * kp.inv_r;
     if (DIR == 1) alpha *= cos_e;
     if (kp.alpha_mode != 0) alpha = alpha_glob;
-    const double ha = 0.5 * alpha;
-    const double hs = 0.5 * (DIR == 0 ? kp.inv_r : cr_e);
+    // the face's lift scale (bd_det) is folded into both halves of f*
+    const double ha = (0.5 * scale) * alpha;
+    const double hs = (0.5 * scale) * (DIR == 0 ? kp.inv_r : cr_e);
     double fs[3][N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
@@ -322,14 +436,12 @@ __device__ __forceinline__ void face_flux(const double (&in)[3][P + 1], const do
         fs[2][k] = fma(hs, fi2 + fo2, -ha * (vo - vi));
     }
 #pragma unroll
-    for (int v = 0; v < 3; ++v)
+    for (int v = 0; v < 3; ++v) {
+        double g[N];
+        n2m<P, 2>(fs[v], g);
 #pragma unroll
-        for (int b = 0; b < N; ++b) {
-            double g = WP(b, 0) * fs[v][0];
-#pragma unroll
-            for (int k = 1; k < N; ++k) g = fma(WP(b, k), fs[v][k], g);
-            sF[(v * N + b) * kLanes + lane] = g * scale;
-        }
+        for (int b = 0; b < N; ++b) sF[(v * N + b) * kLanes + lane] = g[b];
+    }
 }
 
 template <int P>
@@ -369,82 +481,105 @@ __device__ __forceinline__ unsigned yface_from_ring(const double *ring_row, cons
     return bad;
 }
 
+// Pointwise flux / source of variable v at the N nodes (qi, qj), qj = 0..N-1
+// (models.py:161-252): F = x-flux * cx/R, G = y-flux * cy cos/R, S = source.
+template <int P>
+__device__ __forceinline__ void node_physics(int v, int qi, const double *sU, const double *row, int lane,
+                                             const StageParams &kp, double (&F)[P + 1],
+                                             double (&G)[P + 1], double (&S)[P + 1])
+{
+    constexpr int N = P + 1;
+    constexpr int NP = N * N;
+    using RL = RowLayout<P>;
+#pragma unroll
+    for (int qj = 0; qj < N; ++qj) {
+        const int q = qi * N + qj;
+        const double hu = sU[(1 * NP + q) * kLanes + lane];
+        const double hv = sU[(2 * NP + q) * kLanes + lane];
+        const double crc = row[RL::CRC + qj];
+        if (v == 0) {
+            F[qj] = hu * kp.inv_r_cx;
+            G[qj] = hv * crc;
+            S[qj] = 0.0;
+        } else {
+            const double h = sU[(0 * NP + q) * kLanes + lane];
+            const double r = rcp64(fmax(h, kp.h_floor));
+            const double gh2 = h * h * kp.half_g;
+            const double u = hu * r, w = hv * r;
+            const double t = fma(u, row[RL::SRS + qj], row[RL::FCS + qj]);
+            if (v == 1) {
+                F[qj] = fma(hu, u, gh2) * kp.inv_r_cx;
+                G[qj] = hu * w * crc;
+                S[qj] = t * hv;
+            } else {
+                F[qj] = hu * w * kp.inv_r_cx;
+                G[qj] = fma(hv, w, gh2) * crc;
+                S[qj] = -fma(gh2, row[RL::SRS + qj], t * hu);
+            }
+        }
+    }
+}
+
+// eta projections of one xi node line: f[b] = sum_qj wP_b F, g[b] = sum_qj (wP'_b G + wP_b S)
+template <int P>
+__device__ __forceinline__ void line_project(int v, const double (&F)[P + 1], const double (&G)[P + 1],
+                                             const double (&S)[P + 1], double (&f)[P + 1],
+                                             double (&g)[P + 1])
+{
+    n2m<P, 2>(F, f);
+    if (v == 0)
+        n2m<P, 3>(G, g);
+    else
+        n2m2<P, 3, 2>(G, S, g);
+}
+
 // Volume + source projection of variable v at the current row, streamed
-// over the xi node index qi:
+// over pairs of xi node lines (qi, N-1-qi) so that the xi contraction also
+// uses the even/odd split:
 // vol[a][b] = sum_q (cx dphi/dxi F + cy dphi/deta G + cs phi S)[q]
 template <int P>
 __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const double *sU,
                                        const double *row, int lane, const StageParams &kp)
 {
     constexpr int N = P + 1;
-    constexpr int NP = N * N;
-    using RL = RowLayout<P>;
+    constexpr int H = N / 2;
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
         for (int b = 0; b < N; ++b) vol[a][b] = 0.0;
 #pragma unroll 1
-    for (int qi = 0; qi < N; ++qi) {
+    for (int ip = 0; ip < H; ++ip) {
         double F[N], G[N], S[N];
-#pragma unroll
-        for (int qj = 0; qj < N; ++qj) {
-            const int q = qi * N + qj;
-            const double hu = sU[(1 * NP + q) * kLanes + lane];
-            const double hv = sU[(2 * NP + q) * kLanes + lane];
-            const double crc = row[RL::CRC + qj];
-            if (v == 0) {
-                F[qj] = hu * kp.inv_r_cx;
-                G[qj] = hv * crc;
-                S[qj] = 0.0;
-            } else {
-                const double h = sU[(0 * NP + q) * kLanes + lane];
-                const double r = rcp64(fmax(h, kp.h_floor));
-                const double gh2 = h * h * kp.half_g;
-                const double u = hu * r, w = hv * r;
-                const double t = fma(u, row[RL::SRS + qj], row[RL::FCS + qj]);
-                if (v == 1) {
-                    F[qj] = fma(hu, u, gh2) * kp.inv_r_cx;
-                    G[qj] = hu * w * crc;
-                    S[qj] = t * hv;
-                } else {
-                    F[qj] = hu * w * kp.inv_r_cx;
-                    G[qj] = fma(hv, w, gh2) * crc;
-                    S[qj] = -fma(gh2, row[RL::SRS + qj], t * hu);
-                }
-            }
-        }
+        double f0[N], g0[N], f1[N], g1[N];
+        node_physics<P>(v, ip, sU, row, lane, kp, F, G, S);
+        line_project<P>(v, F, G, S, f0, g0);
+        node_physics<P>(v, N - 1 - ip, sU, row, lane, kp, F, G, S);
+        line_project<P>(v, F, G, S, f1, g1);
         double pd[N], pp[N];
 #pragma unroll
         for (int a = 0; a < N; ++a) {
-            pd[a] = WD(a, qi);
-            pp[a] = WP(a, qi);
+            pd[a] = WD(a, ip);
+            pp[a] = WP(a, ip);
         }
-        if (v == 0) {
 #pragma unroll
-            for (int b = 0; b < N; ++b) {
-                double f = WP(b, 0) * F[0], g = WD(b, 0) * G[0];
+        for (int b = 0; b < N; ++b) {
+            // wP'_a(N-1-i) = -(-1)^a wP'_a(i), wP_a(N-1-i) = (-1)^a wP_a(i)
+            const double fp = f0[b] + f1[b], fm = f0[b] - f1[b];
+            const double gp = g0[b] + g1[b], gm = g0[b] - g1[b];
 #pragma unroll
-                for (int qj = 1; qj < N; ++qj) {
-                    f = fma(WP(b, qj), F[qj], f);
-                    g = fma(WD(b, qj), G[qj], g);
-                }
-#pragma unroll
-                for (int a = 0; a < N; ++a) vol[a][b] = fma(pd[a], f, fma(pp[a], g, vol[a][b]));
-            }
-        } else {
-#pragma unroll
-            for (int b = 0; b < N; ++b) {
-                double f = WP(b, 0) * F[0], g = fma(WD(b, 0), G[0], WP(b, 0) * S[0]);
-#pragma unroll
-                for (int qj = 1; qj < N; ++qj) {
-                    f = fma(WP(b, qj), F[qj], f);
-                    g = fma(WD(b, qj), G[qj], g);
-                    g = fma(WP(b, qj), S[qj], g);
-                }
-#pragma unroll
-                for (int a = 0; a < N; ++a) vol[a][b] = fma(pd[a], f, fma(pp[a], g, vol[a][b]));
-            }
+            for (int a = 0; a < N; ++a)
+                vol[a][b] = fma(pd[a], (a & 1) ? fp : fm, fma(pp[a], (a & 1) ? gm : gp, vol[a][b]));
         }
+    }
+    if constexpr (N & 1) {   // middle line xi = 0: wP'_a vanishes for even a, wP_a for odd a
+        double F[N], G[N], S[N], f[N], g[N];
+        node_physics<P>(v, H, sU, row, lane, kp, F, G, S);
+        line_project<P>(v, F, G, S, f, g);
+#pragma unroll
+        for (int b = 0; b < N; ++b)
+#pragma unroll
+            for (int a = 0; a < N; ++a)
+                vol[a][b] = (a & 1) ? fma(WD(a, H), f[b], vol[a][b]) : fma(WP(a, H), g[b], vol[a][b]);
     }
 }
 
@@ -486,7 +621,7 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
         }
     }
     const double *T = row + RL::T;
-    double fin = 0.0;                 // NaN iff some output is not finite
+    int fexp = 0;                     // max exponent field of the outputs (integer pipe)
     double mean = 1.0;
 #pragma unroll
     for (int b = 0; b < N; ++b) {
@@ -501,13 +636,13 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
             double y = fma(kp.b, cur[(a * N + b) * kLanes + lane], (kp.g * (double)(2 * a + 1)) * k);
             if (HAS_U) y = fma(kp.a, un[a][b], y);
             if (owned) Yv[(a * N + b) * nx] = y;
-            fin += y - y;
+            fexp = max(fexp, __double2hiint(y) & 0x7ff00000);
             if (a == 0 && b == 0) mean = y;
         }
     }
     unsigned bad = 0;
     if (owned) {
-        bad |= (kp.check_finite && !(fin == fin)) ? 2u : 0u;
+        bad |= (kp.check_finite && fexp == 0x7ff00000) ? 2u : 0u;   // Inf or NaN
         bad |= (v == 0 && kp.check_mean && !(mean > 0.0)) ? 4u : 0u;
     }
     return bad;
@@ -554,7 +689,6 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
     const double *Uz = kp.U ? kp.U + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx : nullptr;
     double *Yz = kp.Y + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx;
     const bool chk = (v == 0) && !face_warp;
-    const int plo = max(i0 - 1, 0), phi = min(i0 + kLanes - 1, nx);   // prefetch range
     unsigned bad = 0;
 
     // rows whose coefficients exist: local r with global row0+r in [0, ny)
@@ -627,9 +761,8 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
 
         if (!face_warp) {
             // warm L2 for this row's u^n and for row jl+2 (copied in after finalize)
-            if (HAS_U) row_prefetch_l2<P>(Uz + (size_t)jl * kp.rstride, nx, plo, phi, lane);
-            if (jl + 2 <= min(je, r_last))
-                row_prefetch_l2<P>(Xz + (size_t)(jl + 2) * kp.rstride, nx, plo, phi, lane);
+            if (HAS_U) row_prefetch_l2<P>(Uz + (size_t)jl * kp.rstride, nx, i);
+            if (jl + 2 <= min(je, r_last)) row_prefetch_l2<P>(Xz + (size_t)(jl + 2) * kp.rstride, nx, i);
             tile_read<P>(c, cur, lane);                // X(jl)
             bad |= eval_row<P>(c, sU + v * NP * kLanes, sXL + v * N * kLanes, sXR + v * N * kLanes,
                                sT + v * N * kLanes, lane, chk);
