@@ -72,11 +72,12 @@ def load():
     """Load (once) the in-tree library; raises if it was not built."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("DGSWE_LIB", LIB_PATH)   # experiment builds (same ABI)
+        if not os.path.exists(path):
             raise DGSWEError(
-                f"{LIB_PATH} not found: build the CUDA library first "
+                f"{path} not found: build the CUDA library first "
                 "(python -c 'import __graft_entry__ as g; g.build()')")
-        lib = ctypes.CDLL(LIB_PATH)
+        lib = ctypes.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

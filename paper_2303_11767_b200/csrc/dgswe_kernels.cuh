@@ -94,6 +94,42 @@ __host__ __device__ inline int row_stride(int p) { return 3 * (p + 1) + 2 + (p +
 //   T(a, N-1-q) = (-1)^(a + PAR) T(a, q)   exactly,
 // PAR = 0 for P and wP, 1 for P' and wP'.  Every 1-D contraction below
 // uses this even/odd split: N adds + N*ceil(N/2) FMA instead of N*N.
+// DG_ABL: timing ablations for experiments only (results are wrong):
+// 1 no y-face, 2 no x-face, 4 no u^n loads, 8 no hu/hv volume, 16 no eval, 32 no finalize math
+#ifndef DG_ABL
+#define DG_ABL 0
+#endif
+#ifndef DG_MINB
+#define DG_MINB 4   // resident CTAs per SM the p <= 3 build is register-capped for
+#endif
+#ifndef DG_VOL_COMPACT
+#define DG_VOL_COMPACT 0
+#endif
+#ifndef DG_FOLD_CX
+#define DG_FOLD_CX 1
+#endif
+#ifndef DG_PF_SPREAD
+#define DG_PF_SPREAD 0
+#endif
+#if DG_FOLD_CX
+#define CXF kp.inv_r_cx
+#define CXN 1.0
+#else
+#define CXF 1.0
+#define CXN kp.inv_r_cx
+#endif
+
+// DG_TIMING builds record per-role phase durations (clock cycles) of every
+// row: [role][A work, barrier-1 wait, B work, barrier-2 wait, C work, rows]
+#ifdef DG_TIMING
+__device__ unsigned long long g_timing[4][6];
+#define TSTAMP(k) unsigned tk##k = clock()
+#define TACC(i, d) tacc[i] += (d)
+#else
+#define TSTAMP(k)
+#define TACC(i, d)
+#endif
+
 template <int TAB>
 struct TabPar {
     static constexpr int v = (TAB == 1 || TAB == 3) ? 1 : 0;
@@ -230,27 +266,37 @@ struct Smem {
 
 __device__ __forceinline__ double sgn(int k) { return (k & 1) ? -1.0 : 1.0; }
 
-// 1/x: MUFU seed + two Newton steps (<= 1 ulp for normal x)
+// max(x, y) for y > 0 on the integer pipe: the signed 64-bit order of the
+// bit patterns equals the floating-point order for non-negative values and
+// puts every negative x below y (fp64 fmax is a DSETP + select sequence,
+// ~25 cycles of dependent latency on sm_100)
+__device__ __forceinline__ double max_pos(double x, double y)
+{
+    const long long xb = __double_as_longlong(x), yb = __double_as_longlong(y);
+    return __longlong_as_double(xb > yb ? xb : yb);
+}
+
+// max of two non-negative values (same integer trick)
+__device__ __forceinline__ double max_nn(double x, double y) { return max_pos(x, y); }
+
+// 1/x: MUFU seed (~2^-22) + one cubic correction r (1 + e + e^2), e = 1 - x r
+// (error ~e^3, i.e. <= 1 ulp for normal x)
 __device__ __forceinline__ double rcp64(double x)
 {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
-    return fma(r, e, r);
+    const double e = fma(-x, r, 1.0);
+    return fma(r, fma(e, e, e), r);
 }
 
-// 1/sqrt(x): MUFU seed + two Newton steps (x > 0, normal)
+// 1/sqrt(x): MUFU seed + one cubic correction y (1 + e/2 + 3e^2/8),
+// e = 1 - x y^2 (x > 0, normal)
 __device__ __forceinline__ double rsqrt64(double x)
 {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    const double hx = 0.5 * x;
-    double e = fma(-hx * y, y, 0.5);
-    y = fma(y, e, y);
-    e = fma(-hx * y, y, 0.5);
-    return fma(y, e, y);
+    const double e = fma(-x * y, y, 1.0);
+    return fma(y, e * fma(e, 0.375, 0.5), y);
 }
 
 // 1/hf and sqrt(g hf) with hf = max(h, floor) from one rsqrt; equals the
@@ -258,7 +304,7 @@ __device__ __forceinline__ double rsqrt64(double x)
 __device__ __forceinline__ void inv_and_celerity(double h, double h_floor, double sqrt_g, double &r,
                                                  double &c)
 {
-    const double hf = fmax(h, h_floor);
+    const double hf = max_pos(h, h_floor);
     const double y = rsqrt64(hf);
     r = y * y;
     c = sqrt_g * (hf * y);
@@ -273,18 +319,36 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// L2 prefetch of this lane's element of one variable (one mode per
-// instruction; the warp's 32 lanes cover the strip's lines).  Per-lane
-// prefetch.global.L2 rather than cp.async.bulk.prefetch, whose uniform
-// operands made the compiler serialise the lanes (ncu: 11% of issue slots).
+// L2 prefetch of one variable's modes over the strip: three probes per mode
+// (first, middle and last element) cover the <= 3 lines a 32-element span
+// touches, spread over the lanes (2 instructions per row at p = 3).
+#if !DG_PF_SPREAD
 template <int P>
-__device__ __forceinline__ void row_prefetch_l2(const double *src, int nx, int i)
+__device__ __forceinline__ void row_prefetch_l2(const double *src, int nx, int ifirst, int lane)
 {
     constexpr int NP = (P + 1) * (P + 1);
+    int i = ifirst + lane;
+    if (i >= nx) i -= nx;
+    if (i < 0) i += nx;
     const double *p = src + i;
 #pragma unroll
     for (int m = 0; m < NP; ++m, p += nx) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+#else
+template <int P>
+__device__ __forceinline__ void row_prefetch_l2(const double *src, int nx, int ifirst, int lane)
+{
+    constexpr int NP = (P + 1) * (P + 1);
+#pragma unroll
+    for (int k = lane; k < 3 * NP; k += kLanes) {
+        const int m = k / 3, part = k - 3 * m;
+        int e = ifirst + (part == 0 ? 0 : part == 1 ? 16 : kLanes - 1);
+        if (e >= nx) e -= nx;
+        if (e < 0) e += nx;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(src + (size_t)m * nx + e));
+    }
+}
+#endif
 
 // this lane's element, one variable: NP words, mode-major, lane-minor
 template <int P>
@@ -391,7 +455,7 @@ __device__ __forceinline__ void face_flux(const double (&in)[3][P + 1], const do
     constexpr int N = P + 1;
     constexpr int M = DIR == 0 ? 1 : 2;   // normal momentum
     double rin[N], rout[N];
-    double amax = 0.0;
+    double am[N];
     bool low = false;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
@@ -399,8 +463,13 @@ __device__ __forceinline__ void face_flux(const double (&in)[3][P + 1], const do
         inv_and_celerity(in[0][k], kp.h_floor, kp.sqrt_g, rin[k], ci);
         inv_and_celerity(out[0][k], kp.h_floor, kp.sqrt_g, rout[k], co);
         low |= (in[0][k] < kp.h_floor) | (out[0][k] < kp.h_floor);
-        amax = fmax(amax, fmax(fabs(in[M][k] * rin[k]) + ci, fabs(out[M][k] * rout[k]) + co));
+        am[k] = max_nn(fabs(in[M][k] * rin[k]) + ci, fabs(out[M][k] * rout[k]) + co);
     }
+#pragma unroll
+    for (int w = 1; w < N; w *= 2)     // pairwise tree: log2(N) dependent maxima
+#pragma unroll
+        for (int k = 0; k + w < N; k += 2 * w) am[k] = max_nn(am[k], am[k + w]);
+    double amax = am[0];
     if (__any_sync(0xffffffffu, low)) {      // h below the velocity floor: exact celerity
         amax = 0.0;
 #pragma unroll
@@ -482,7 +551,8 @@ __device__ __forceinline__ unsigned yface_from_ring(const double *ring_row, cons
 }
 
 // Pointwise flux / source of variable v at the N nodes (qi, qj), qj = 0..N-1
-// (models.py:161-252): F = x-flux * cx/R, G = y-flux * cy cos/R, S = source.
+// (models.py:161-252): F = x-flux (its cx/R goes into the xi weights),
+// G = y-flux * cy cos/R, S = source.
 template <int P>
 __device__ __forceinline__ void node_physics(int v, int qi, const double *sU, const double *row, int lane,
                                              const StageParams &kp, double (&F)[P + 1],
@@ -498,21 +568,21 @@ __device__ __forceinline__ void node_physics(int v, int qi, const double *sU, co
         const double hv = sU[(2 * NP + q) * kLanes + lane];
         const double crc = row[RL::CRC + qj];
         if (v == 0) {
-            F[qj] = hu * kp.inv_r_cx;
+            F[qj] = hu * CXN;
             G[qj] = hv * crc;
             S[qj] = 0.0;
         } else {
             const double h = sU[(0 * NP + q) * kLanes + lane];
-            const double r = rcp64(fmax(h, kp.h_floor));
+            const double r = rcp64(max_pos(h, kp.h_floor));
             const double gh2 = h * h * kp.half_g;
             const double u = hu * r, w = hv * r;
             const double t = fma(u, row[RL::SRS + qj], row[RL::FCS + qj]);
             if (v == 1) {
-                F[qj] = fma(hu, u, gh2) * kp.inv_r_cx;
+                F[qj] = fma(hu, u, gh2) * CXN;
                 G[qj] = hu * w * crc;
                 S[qj] = t * hv;
             } else {
-                F[qj] = hu * w * kp.inv_r_cx;
+                F[qj] = hu * w * CXN;
                 G[qj] = fma(hv, w, gh2) * crc;
                 S[qj] = -fma(gh2, row[RL::SRS + qj], t * hu);
             }
@@ -549,16 +619,35 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
         for (int b = 0; b < N; ++b) vol[a][b] = 0.0;
 #pragma unroll 1
     for (int ip = 0; ip < H; ++ip) {
-        double F[N], G[N], S[N];
         double f0[N], g0[N], f1[N], g1[N];
-        node_physics<P>(v, ip, sU, row, lane, kp, F, G, S);
-        line_project<P>(v, F, G, S, f0, g0);
-        node_physics<P>(v, N - 1 - ip, sU, row, lane, kp, F, G, S);
-        line_project<P>(v, F, G, S, f1, g1);
+#if DG_VOL_COMPACT
+        // one loop body for both lines of the pair (I-cache footprint)
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {
+            double F[N], G[N], S[N];
+            node_physics<P>(v, side ? N - 1 - ip : ip, sU, row, lane, kp, F, G, S);
+            line_project<P>(v, F, G, S, f1, g1);
+            if (side == 0) {
+#pragma unroll
+                for (int b = 0; b < N; ++b) {
+                    f0[b] = f1[b];
+                    g0[b] = g1[b];
+                }
+            }
+        }
+#else
+        {
+            double F[N], G[N], S[N];
+            node_physics<P>(v, ip, sU, row, lane, kp, F, G, S);
+            line_project<P>(v, F, G, S, f0, g0);
+            node_physics<P>(v, N - 1 - ip, sU, row, lane, kp, F, G, S);
+            line_project<P>(v, F, G, S, f1, g1);
+        }
+#endif
         double pd[N], pp[N];
 #pragma unroll
         for (int a = 0; a < N; ++a) {
-            pd[a] = WD(a, ip);
+            pd[a] = WD(a, ip) * CXF;   // F's 1/R * determ/bd_det_x folded in here
             pp[a] = WP(a, ip);
         }
 #pragma unroll
@@ -579,7 +668,8 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
         for (int b = 0; b < N; ++b)
 #pragma unroll
             for (int a = 0; a < N; ++a)
-                vol[a][b] = (a & 1) ? fma(WD(a, H), f[b], vol[a][b]) : fma(WP(a, H), g[b], vol[a][b]);
+                vol[a][b] = (a & 1) ? fma(WD(a, H) * CXF, f[b], vol[a][b])
+                                    : fma(WP(a, H), g[b], vol[a][b]);
     }
 }
 
@@ -596,7 +686,7 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
     constexpr int N = P + 1;
     using RL = RowLayout<P>;
     double un[N][N];
-    if (HAS_U) {                       // u^n: plain loads (U may alias Y)
+    if (HAS_U && !(DG_ABL & 4)) {      // u^n: plain loads (U may alias Y)
 #pragma unroll
         for (int a = 0; a < N; ++a)
 #pragma unroll
@@ -631,10 +721,14 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
 #pragma unroll
         for (int a = 0; a < N; ++a) {
             double k = tb[0] * vol[a][0];
+            if (!(DG_ABL & 32)) {
 #pragma unroll
-            for (int bb = 1; bb < N; ++bb) k = fma(tb[bb], vol[a][bb], k);
+                for (int bb = 1; bb < N; ++bb) k = fma(tb[bb], vol[a][bb], k);
+            } else {
+                k = vol[a][b];
+            }
             double y = fma(kp.b, cur[(a * N + b) * kLanes + lane], (kp.g * (double)(2 * a + 1)) * k);
-            if (HAS_U) y = fma(kp.a, un[a][b], y);
+            if (HAS_U && !(DG_ABL & 4)) y = fma(kp.a, un[a][b], y);
             if (owned) Yv[(a * N + b) * nx] = y;
             fexp = max(fexp, __double2hiint(y) & 0x7ff00000);
             if (a == 0 && b == 0) mean = y;
@@ -649,7 +743,7 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
 }
 
 template <int P, bool HAS_U>
-__global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(StageParams kp)
+__global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel(StageParams kp)
 {
     constexpr int N = P + 1;
     constexpr int NP = N * N;
@@ -751,7 +845,11 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
         for (int k = 0; k < N; ++k) bad |= !(bt[k] > 0.0);
     }
 
+#ifdef DG_TIMING
+    unsigned tacc[5] = {0, 0, 0, 0, 0};
+#endif
     for (int jl = jb; jl < je; ++jl) {
+        TSTAMP(0);
         const int slot = (jl - jb) & 1;
         double *const cur = ring0 + slot * SM::TILE;
         const int jg = kp.row0 + jl;
@@ -761,17 +859,27 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
 
         if (!face_warp) {
             // warm L2 for this row's u^n and for row jl+2 (copied in after finalize)
-            if (HAS_U) row_prefetch_l2<P>(Uz + (size_t)jl * kp.rstride, nx, i);
-            if (jl + 2 <= min(je, r_last)) row_prefetch_l2<P>(Xz + (size_t)(jl + 2) * kp.rstride, nx, i);
+            if (HAS_U) row_prefetch_l2<P>(Uz + (size_t)jl * kp.rstride, nx, i0 - 1, lane);
+            if (jl + 2 <= min(je, r_last))
+                row_prefetch_l2<P>(Xz + (size_t)(jl + 2) * kp.rstride, nx, i0 - 1, lane);
             tile_read<P>(c, cur, lane);                // X(jl)
-            bad |= eval_row<P>(c, sU + v * NP * kLanes, sXL + v * N * kLanes, sXR + v * N * kLanes,
-                               sT + v * N * kLanes, lane, chk);
+            if (DG_ABL & 16) {
+#pragma unroll
+                for (int a = 0; a < N; ++a)
+#pragma unroll
+                    for (int b = 0; b < N; ++b) sU[(v * NP + a * N + b) * kLanes + lane] = c[a][b];
+            } else {
+                bad |= eval_row<P>(c, sU + v * NP * kLanes, sXL + v * N * kLanes, sXR + v * N * kLanes,
+                                   sT + v * N * kLanes, lane, chk);
+            }
             cp_wait<0>();                              // X(jl+1) landed (own copies)
         }
+        TSTAMP(1);
         __syncthreads();
+        TSTAMP(2);
 
         if (face_warp) {
-            if (has_top)
+            if (has_top && !(DG_ABL & 1))
                 bad |= yface_from_ring<P>(ringS + (slot ^ 1) * SM::TILE, sT, sFa, lane, kp,
                                           sRow + ((jl + 1 - jb) % 3) * RL::STRIDE, alpha_y);
             // stage the table of row jl+2 (its slot held row jl-1, no longer read)
@@ -780,9 +888,13 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
                 const double *src = kp.rowtab + (size_t)(jg + 2) * RL::STRIDE;
                 for (int idx = lane; idx < RL::STRIDE; idx += kLanes) dst[idx] = src[idx];
             }
+            TSTAMP(3);
             __syncthreads();
+            TSTAMP(4);
+            TACC(2, tk3 - tk2);
+            TACC(3, tk4 - tk3);
         } else {
-            if (v == 0) {
+            if (v == 0 && !(DG_ABL & 2)) {
                 // the h warp has the lightest volume work: it takes the x-faces
                 double in[3][N], out[3][N];
                 traces_from_smem<P>(in, sXR, lane);
@@ -790,8 +902,17 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
                 face_flux<P, 0>(in, out, sFX, lane, kp, 0.0, 0.0, alpha_x, kp.bdy);
             }
             double vol[N][N];
-            volume<P>(vol, v, sU, row, lane, kp);
+            if ((DG_ABL & 8) && v > 0) {
+#pragma unroll
+                for (int a = 0; a < N; ++a)
+#pragma unroll
+                    for (int b = 0; b < N; ++b) vol[a][b] = sU[(a * N + b) * kLanes + lane];
+            } else {
+                volume<P>(vol, v, sU, row, lane, kp);
+            }
+            TSTAMP(3);
             __syncthreads();
+            TSTAMP(4);
             const size_t roff = (size_t)jl * kp.rstride;
             bad |= finalize<P, HAS_U>(vol, cur, HAS_U ? Uz + roff : nullptr, v, sFX, sFa, sFb,
                                       has_top, has_bot, row, lane, owned, Yz + roff + i, nx, i, kp);
@@ -800,13 +921,25 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? 4 : 2)) stage_kernel(Stage
             if (jl + 2 <= min(je, r_last))
                 tile_fetch<P>(cur, Xz + (size_t)(jl + 2) * kp.rstride, nx, i, lane);
             cp_commit();
+            TSTAMP(5);
+            TACC(2, tk3 - tk2);
+            TACC(3, tk4 - tk3);
+            TACC(4, tk5 - tk4);
         }
+        TACC(0, tk1 - tk0);
+        TACC(1, tk2 - tk1);
         double *tmp = sFa;
         sFa = sFb;
         sFb = tmp;
     }
     if (!face_warp) cp_wait<0>();
 
+#ifdef DG_TIMING
+    if (lane == 0) {
+        for (int k = 0; k < 5; ++k) atomicAdd(&g_timing[role][k], (unsigned long long)tacc[k]);
+        atomicAdd(&g_timing[role][5], (unsigned long long)(je - jb));
+    }
+#endif
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && lane == 0) {
         atomicOr(kp.status, bad);

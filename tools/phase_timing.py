@@ -1,0 +1,43 @@
+"""Per-role phase timing of the stage kernel (DG_TIMING experiment build).
+
+    DGSWE_LIB=build/variants/<timing>.so python tools/phase_timing.py [--config c3]
+Prints average cycles per row for each warp role and phase.
+"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2303_11767_b200 import SpatialOperator, _lib, build_case, default_config  # noqa: E402
+
+
+def main():
+    nx, ny, p, dt = 720, 360, 3, 5e-3
+    cfg = default_config("williamson_tc6").override(nx=nx, ny=ny, p=p)
+    setup = build_case(cfg)
+    op = SpatialOperator(setup.mesh, p, setup.model)
+    st = op.project_state(setup.ic)
+    lib = _lib.load()
+    fn = lib.dgswe_debug_timing
+    fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+    buf = (ctypes.c_ulonglong * 24)()
+    op.ssprk3_steps(st, dt, 3)
+    fn(buf)
+    op.ssprk3_steps(st, dt, 20)
+    torch.cuda.synchronize()
+    fn(buf)
+    a = np.array(list(buf), dtype=np.float64).reshape(4, 6)
+    names = ["h", "hu", "hv", "face"]
+    print("cycles per row:   A-work  wait1   B-work  wait2   C-work   total")
+    for r in range(4):
+        rows = a[r, 5]
+        x = a[r, :5] / max(rows, 1)
+        print(f"{names[r]:5s} {x[0]:8.0f} {x[1]:7.0f} {x[2]:8.0f} {x[3]:7.0f} {x[4]:8.0f} {x.sum():8.0f}")
+
+
+if __name__ == "__main__":
+    main()
