@@ -250,7 +250,7 @@ def run_gpu(args):
     # per-stage launch times (event-timed, same stream, individual launches)
     per_stage = None
     if world == 1:
-        w1, w2 = torch.empty_like(state.data), torch.empty_like(state.data)
+        w1, w2 = torch.zeros_like(state.data), torch.zeros_like(state.data)
         s1 = P.State(w1, nx, ny, 1, op.nphi)
         s2 = P.State(w2, nx, ny, 1, op.nphi)
         reps = 20

@@ -27,9 +27,14 @@
  *                                  DivergenceError (timestep.py:165-166,
  *                                  220-226) as device status bits
  *
- * Layout of every state buffer (fp64):  [nz][nrows][3][nphi][nx]
+ * Layout of every state buffer (fp64), strip-blocked structure of arrays:
+ *   [nz][nrows][3][nstrip][nphi][DGSWE_STRIP]
  *   variable v in {h, hu, hv}; mode m = a*(p+1)+b (a: lambda degree,
- *   b: theta degree, basis.py:5-13); longitude index i fastest.
+ *   b: theta degree, basis.py:5-13); longitude element i = DGSWE_STRIP*s + l
+ *   at strip s, lane l; nstrip = ceil(nx / DGSWE_STRIP).  Lanes i >= nx of
+ *   the last strip are padding: never written, they must hold finite values
+ *   (zero them once).  One variable's row tile of a strip is contiguous
+ *   (nphi * DGSWE_STRIP doubles), the unit of the kernel's TMA copies.
  *   Buffer row r holds global latitude row row0 + r.  The rows computed are
  *   [jlo, jhi) (local); a band's halo rows jlo-1 and jhi must hold the
  *   neighbour band's coefficients whenever they are inside the sphere.
@@ -47,7 +52,8 @@
 extern "C" {
 #endif
 
-#define DGSWE_ABI_VERSION 1
+#define DGSWE_ABI_VERSION 2
+#define DGSWE_STRIP 32          /* longitude elements per strip block */
 
 /* status bits (dgswe_status) */
 #define DGSWE_STATUS_POSITIVITY 0x1u  /* h <= 0 (or NaN) at a quadrature node */
@@ -101,7 +107,7 @@ const char *dgswe_last_error(void);
 int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *tables, dgswe_ctx **out);
 void dgswe_destroy(dgswe_ctx *ctx);
 
-/* elements of one state buffer (nz * nrows * 3 * nphi * nx) */
+/* elements of one state buffer (nz * nrows * 3 * nstrip * nphi * DGSWE_STRIP) */
 int64_t dgswe_state_elems(const dgswe_ctx *ctx);
 
 /* K = M^-1 (volume - boundary + source)(X) on rows [jlo, jhi). */

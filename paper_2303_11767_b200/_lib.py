@@ -14,6 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdgswe_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "dgswe_b200.h")
 
+ABI_VERSION = 2            # DGSWE_ABI_VERSION
+STRIP = 32                 # DGSWE_STRIP: longitude elements per strip block
 STATUS_POSITIVITY = 0x1
 STATUS_NONFINITE = 0x2
 STATUS_MEAN_NONPOS = 0x4
@@ -82,7 +84,7 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.dgswe_abi_version() != 1:
+        if lib.dgswe_abi_version() != ABI_VERSION:
             raise DGSWEError("libdgswe_b200.so ABI version mismatch")
         _lib = lib
     return _lib

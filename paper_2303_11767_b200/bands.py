@@ -11,7 +11,8 @@ point-to-point only (no collective on the hot path).  Both bands evaluate
 the shared face with identical operands and code, so the numerical flux is
 bit-identical on both sides and results do not depend on the band count.
 
-Band buffer (per state): [nz][nrows = owned + 2][3][nphi][nx]; buffer row 0
+Band buffer (per state): [nz][nrows = owned + 2][3][nstrip][nphi][32] (the
+strip-blocked layout of operator.py); buffer row 0
 is the southern halo (global row j0-1), rows 1..owned are owned, the last
 row is the northern halo.  Halo rows at a pole are never read.
 
@@ -98,7 +99,7 @@ class BandLayout:
         return self.rank + 1 if self.j1 < self.ny else None
 
     def scatter(self, full: np.ndarray) -> np.ndarray:
-        """Band buffer (halos filled) from a global (nz, ny, 3, nphi, nx) array."""
+        """Band buffer (halos filled) from a global device-layout array (nz, ny, ...)."""
         nz = full.shape[0]
         out = np.zeros((nz, self.nrows) + full.shape[2:], dtype=full.dtype)
         lo, hi = max(self.j0 - 1, 0), min(self.j1 + 1, self.ny)
@@ -174,7 +175,8 @@ class BandOperator:
         self.group = group
         self.overlap = overlap and transport == "p2p"
         mesh = op_host.mesh
-        self.shape = (op_host.nz, layout.nrows, 3, op_host.nphi, mesh.nx)
+        from .operator import device_shape
+        self.shape = device_shape(op_host.nz, layout.nrows, op_host.nphi, mesh.nx)
         self.ctx = _Context(mesh, op_host.p, op_host.model, op_host.rusanov, op_host.nz,
                             op_host.quad, op_host.vander, op_host.Minv_rows, row0=layout.row0,
                             nrows=layout.nrows, jlo=layout.jlo, jhi=layout.jhi, row_chunk=row_chunk)

@@ -53,7 +53,8 @@ struct DevStatus {
 // global-mode alpha: max over all traces (dg.py:389-411, models.py:271-280)
 template <int P>
 __global__ void alpha_prepass_kernel(const double *__restrict__ X, long long zstride,
-                                     long long rstride, int nx, int ny, int row0, int jlo, int jhi,
+                                     long long rstride, long long vstride, int nx, int ny, int row0,
+                                     int jlo, int jhi,
                                      const double *__restrict__ cos_edge, double inv_r, double gravity,
                                      double h_floor, double *out)
 {
@@ -68,7 +69,8 @@ __global__ void alpha_prepass_kernel(const double *__restrict__ X, long long zst
     for (int v = 0; v < 3; ++v) {
         double c[N][N];
         for (int a = 0; a < N; ++a)
-            for (int b = 0; b < N; ++b) c[a][b] = base[(size_t)(v * NP + a * N + b) * nx + i];
+            for (int b = 0; b < N; ++b)
+                c[a][b] = base[(size_t)v * vstride + (size_t)(i >> 5) * NP * 32 + (a * N + b) * 32 + (i & 31)];
         for (int q = 0; q < N; ++q) {
             double l = 0, r = 0, bo = 0, t = 0;
             for (int a = 0; a < N; ++a) {
@@ -142,7 +144,8 @@ struct GraphKey {
 struct dgswe_ctx {
     dgswe_cfg cfg;
     int n, nphi, rc;
-    long long rstride, zstride;
+    long long vstride, rstride, zstride;
+    int nstrip;
     double *rowtab = nullptr;     // device, ny * row_stride(p)
     double *cos_edge = nullptr;   // device, ny+1
     double *alpha = nullptr;      // device, 2 doubles
@@ -189,7 +192,7 @@ int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, c
     }
     // one wave: split every (strip, level) column of rows into as many
     // contiguous chunks as the resident CTA slots allow
-    const int strips = (c->cfg.nx + dgswe::kOwned - 1) / dgswe::kOwned;
+    const int strips = c->nstrip;
     int rc = kp.rc;
     if (rc <= 0) {
         const long long slots = (long long)c->sms * occ[dev][variant];
@@ -224,6 +227,8 @@ int launch_stage(dgswe_ctx *c, double a, const double *U, double b, const double
     kp.Y = Y;
     kp.zstride = c->zstride;
     kp.rstride = c->rstride;
+    kp.vstride = c->vstride;
+    kp.nstrip = c->nstrip;
     kp.nx = c->cfg.nx;
     kp.ny = c->cfg.ny;
     kp.row0 = c->cfg.row0;
@@ -240,6 +245,7 @@ int launch_stage(dgswe_ctx *c, double a, const double *U, double b, const double
     kp.gravity = c->cfg.gravity;
     kp.half_g = c->half_g;
     kp.h_floor = c->cfg.h_floor;
+    kp.inv_floor = 1.0 / c->cfg.h_floor;
     kp.sqrt_g = sqrt(c->cfg.gravity);
     kp.bdx = c->bdx;
     kp.bdy = c->bdy;
@@ -272,7 +278,8 @@ int launch_alpha_p(dgswe_ctx *c, const double *X, cudaStream_t s)
 {
     const int rows = c->cfg.jhi - c->cfg.jlo;
     dim3 grid((c->cfg.nx + 127) / 128, rows, c->cfg.nz);
-    alpha_prepass_kernel<P><<<grid, 128, 0, s>>>(X, c->zstride, c->rstride, c->cfg.nx, c->cfg.ny,
+    alpha_prepass_kernel<P><<<grid, 128, 0, s>>>(X, c->zstride, c->rstride, c->vstride, c->cfg.nx,
+                                                   c->cfg.ny,
                                                    c->cfg.row0, c->cfg.jlo, c->cfg.jhi, c->cos_edge,
                                                    c->inv_r, c->cfg.gravity, c->cfg.h_floor, c->alpha);
     CUDA_TRY(cudaGetLastError());
@@ -313,7 +320,9 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
     const int n = c.p + 1;
     ctx->n = n;
     ctx->nphi = n * n;
-    ctx->rstride = 3LL * ctx->nphi * c.nx;
+    ctx->nstrip = (c.nx + DGSWE_STRIP - 1) / DGSWE_STRIP;
+    ctx->vstride = (long long)ctx->nstrip * ctx->nphi * DGSWE_STRIP;
+    ctx->rstride = 3LL * ctx->vstride;
     ctx->zstride = ctx->rstride * c.nrows;
     cudaGetDevice(&ctx->device);
 

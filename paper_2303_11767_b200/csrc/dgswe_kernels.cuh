@@ -1,34 +1,34 @@
 // dgswe_kernels.cuh -- fused fp64 DG shallow-water stage kernel for sm_100a.
 //
-// One CTA = 4 warps x 32 lanes: warp v < 3 owns variable v in {h, hu, hv};
-// warp 0 (lightest physics) also evaluates the row's x-face fluxes and
-// warp 3 (the face warp) the bottom traces of the row above and the y-face.
-// Lane l holds longitude element i0-1+l (mod nx) of a 30-element strip:
-// lanes 1..30 own their element, lanes 0 and 31 are the periodic/strip halo
-// whose traces feed the strip's two border faces.  The CTA marches north
-// through a chunk of latitude rows; every y-face is evaluated once per
-// chunk, every x-face once per strip.
+// HBM layout of a state (strip-blocked structure of arrays):
+//   [nz][row][var 3][strip][mode nphi][32 elements]
+// A strip is 32 consecutive longitude elements (the last one zero-padded),
+// so one variable's row tile of a strip is a single contiguous block of
+// nphi * 256 bytes: it moves with ONE TMA bulk copy (cp.async.bulk +
+// mbarrier), its L2 prefetch is one bulk-prefetch instruction, and every
+// per-lane load/store inside it is an immediate offset from one base.
 //
-// Memory pipeline: each lane streams its own element's coefficients with
-// cp.async (LDGSTS) into a two-row shared-memory ring, two rows ahead of
-// use, and the u^n tile of the current row one phase ahead; every lane
-// reads back only the words it copied, so no CTA barrier guards the ring.
+// One CTA = 4 warps x 32 lanes on one strip: warp v < 3 owns variable v in
+// {h, hu, hv}; warp 0 (lightest physics) also evaluates the row's x-faces
+// 1..32 and warp 3 (the face warp) the y-face above the row, the strip's
+// two halo traces and its left border face 0.  Lane l owns element
+// 32*strip + l.  The CTA marches north through a chunk of latitude rows.
 //
 // Per row, per variable and lane (n = p+1, all tensor contractions
-// sum-factorised; constant tables in __constant__):
+// sum-factorised with the even/odd split; constant tables in __constant__):
 //   1. modal -> nodal: t[a][qj] = sum_b c[a][b] P_b(x_qj),
 //      U[qi][qj] = sum_a P_a(x_qi) t[a][qj]; traces L/R from t, T/B from
 //      sum_b c[a][b](+-1)^b                          (dg.py:348-357)
 //   2. nodal values exchanged through shared memory; pointwise flux /
 //      source physics for this warp's variable      (models.py:161-252)
-//   3. face warps: Rusanov flux with local alpha    (dg.py:92-119,385-453)
-//   4. volume + source projection streamed over qi, boundary lifts,
-//      per-row inverse mass (Kronecker block form), fused RK stage update
-//      (dg.py:455-502, timestep.py:132-167)
+//   3. Rusanov fluxes with local alpha               (dg.py:92-119,385-453)
+//   4. volume + source projection streamed over xi node pairs, boundary
+//      lifts, per-row inverse mass (Kronecker block form), fused RK stage
+//      update (dg.py:455-502, timestep.py:132-167)
 //
-// Floating point: FMA contraction and a Newton-refined reciprocal are used;
-// results agree with the reference's exact-order oracle to ~1e-15 relative
-// per step (tests/test_gpu_parity.py).
+// Floating point: FMA contraction, refined MUFU reciprocals and a different
+// summation order than the reference; results agree with the reference's
+// exact-order oracle to ~1e-15 relative per step (tests/test_gpu_parity.py).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -37,8 +37,7 @@
 namespace dgswe {
 
 constexpr int kMaxP = 6;
-constexpr int kLanes = 32;
-constexpr int kOwned = 30;   // owned elements per strip (lanes 1..30)
+constexpr int kLanes = 32;   // elements per strip (== DGSWE_STRIP)
 constexpr int kVarWarps = 3; // one per conserved variable
 constexpr int kWarps = 4;    // + one face warp (Rusanov fluxes)
 constexpr int kThreads = kWarps * kLanes;
@@ -51,14 +50,15 @@ struct StageParams {
     const double *U;      // u^n for the combination (may be null when a == 0)
     double *Y;            // output
     long long zstride;    // doubles per level
-    long long rstride;    // doubles per buffer row (3 * nphi * nx)
-    int nx, ny, row0, nrows;
+    long long rstride;    // doubles per buffer row (3 * vstride)
+    long long vstride;    // doubles per variable row (nstrip * nphi * 32)
+    int nx, nstrip, ny, row0, nrows;
     int j_begin, j_end, rc;   // local rows [j_begin, j_end), rc rows per CTA
     double a, b, g;       // Y = a U + b X + g RHS(X)
     const double *rowtab; // per global row, see RowLayout
     double inv_r;         // 1/R
     double inv_r_cx;      // (1/R) * determ/bd_det_x
-    double gravity, half_g, h_floor, sqrt_g;
+    double gravity, half_g, h_floor, inv_floor, sqrt_g;
     double bdx, bdy;      // bd_det_x, bd_det_y
     int alpha_mode;       // 0 local, 1 pinned, 2 global (from alpha_dev)
     double alpha;
@@ -94,29 +94,8 @@ __host__ __device__ inline int row_stride(int p) { return 3 * (p + 1) + 2 + (p +
 //   T(a, N-1-q) = (-1)^(a + PAR) T(a, q)   exactly,
 // PAR = 0 for P and wP, 1 for P' and wP'.  Every 1-D contraction below
 // uses this even/odd split: N adds + N*ceil(N/2) FMA instead of N*N.
-// DG_ABL: timing ablations for experiments only (results are wrong):
-// 1 no y-face, 2 no x-face, 4 no u^n loads, 8 no hu/hv volume, 16 no eval, 32 no finalize math
-#ifndef DG_ABL
-#define DG_ABL 0
-#endif
 #ifndef DG_MINB
 #define DG_MINB 4   // resident CTAs per SM the p <= 3 build is register-capped for
-#endif
-#ifndef DG_VOL_COMPACT
-#define DG_VOL_COMPACT 0
-#endif
-#ifndef DG_FOLD_CX
-#define DG_FOLD_CX 1
-#endif
-#ifndef DG_PF_SPREAD
-#define DG_PF_SPREAD 0
-#endif
-#if DG_FOLD_CX
-#define CXF kp.inv_r_cx
-#define CXN 1.0
-#else
-#define CXF 1.0
-#define CXN kp.inv_r_cx
 #endif
 
 // DG_TIMING builds record per-role phase durations (clock cycles) of every
@@ -251,17 +230,23 @@ struct Smem {
     static constexpr int TILE = 3 * NP * kLanes;         // one row of coefficients, all vars
     static constexpr int TR = 3 * N * kLanes;            // one trace / face-flux set
     // offsets in doubles
-    static constexpr int XR0 = 0;                        // coefficient ring slot 0
+    static constexpr int XR0 = 0;                        // coefficient ring slot 0 [var][mode][lane]
     static constexpr int XR1 = XR0 + TILE;               // slot 1
     static constexpr int U = XR1 + TILE;                 // nodal values [3][NP][32]
     static constexpr int XL = U + TILE;                  // [3][N][32]
     static constexpr int XRT = XL + TR;
     static constexpr int TT = XRT + TR;                  // top traces of current row
-    static constexpr int FX = TT + TR;                   // x-face flux, right face of lane
-    static constexpr int FY0 = FX + TR;                  // y-face flux buffers
+    static constexpr int FX = TT + TR;                   // x-face fluxes [3][N][33], face f left of lane f
+                                                         // (face 0 lives in F0, double-buffered)
+    static constexpr int FY0 = FX + 3 * N * (kLanes + 1);   // y-face flux buffers [3][N][32]
     static constexpr int FY1 = FY0 + TR;
-    static constexpr int ROW = FY1 + TR;                 // row-table ring, 3 rows
-    static constexpr int TOTAL = ROW + 3 * RowLayout<P>::STRIDE;
+    static constexpr int HL = FY1 + TR;                  // left-halo R trace [3][N]
+    static constexpr int HR = HL + 3 * N;                // right-halo L trace [3][N]
+    static constexpr int E0 = HR + 3 * N;                // element 0's L trace [3][N] (face warp)
+    static constexpr int F0 = E0 + 3 * N;                // face 0 flux [row parity][3][N]
+    static constexpr int ROW = F0 + 6 * N;               // row-table ring, 3 rows
+    static constexpr int MBAR = ROW + 3 * RowLayout<P>::STRIDE;   // 6 mbarriers [slot][var]
+    static constexpr int TOTAL = MBAR + 6;
 };
 
 __device__ __forceinline__ double sgn(int k) { return (k & 1) ? -1.0 : 1.0; }
@@ -299,64 +284,61 @@ __device__ __forceinline__ double rsqrt64(double x)
     return fma(y, e * fma(e, 0.375, 0.5), y);
 }
 
-// 1/hf and sqrt(g hf) with hf = max(h, floor) from one rsqrt; equals the
-// reference's sqrt(g max(h, 0)) whenever h >= floor (callers fix the rest)
-__device__ __forceinline__ void inv_and_celerity(double h, double h_floor, double sqrt_g, double &r,
-                                                 double &c)
+// 1/hf with hf = max(h, floor) (models.py:161-166) and the celerity
+// sqrt(g max(h, 0)) (models.py:254-258) from ONE rsqrt of h: below the floor
+// 1/hf is the constant 1/floor, and h <= 0 (flagged by the positivity
+// check) gives c = 0 like the reference.
+__device__ __forceinline__ void inv_and_celerity(double h, double h_floor, double inv_floor, double sqrt_g,
+                                                 double &r, double &c)
 {
-    const double hf = max_pos(h, h_floor);
-    const double y = rsqrt64(hf);
-    r = y * y;
-    c = sqrt_g * (hf * y);
+    const double y = rsqrt64(max_pos(h, 2.2250738585072014e-308));
+    r = h >= h_floor ? y * y : inv_floor;
+    c = h > 0.0 ? sqrt_g * (h * y) : 0.0;
 }
 
-__device__ __forceinline__ void cp_async8(double *dst, const double *src)
+// --- TMA bulk copies and mbarriers (one elected lane per variable warp) ---
+__device__ __forceinline__ unsigned smem_u32(const void *p)
 {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(src) : "memory");
+    return (unsigned)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// L2 prefetch of one variable's modes over the strip: three probes per mode
-// (first, middle and last element) cover the <= 3 lines a 32-element span
-// touches, spread over the lanes (2 instructions per row at p = 3).
-#if !DG_PF_SPREAD
-template <int P>
-__device__ __forceinline__ void row_prefetch_l2(const double *src, int nx, int ifirst, int lane)
+__device__ __forceinline__ void mbar_init(unsigned long long *mb, unsigned count)
 {
-    constexpr int NP = (P + 1) * (P + 1);
-    int i = ifirst + lane;
-    if (i >= nx) i -= nx;
-    if (i < 0) i += nx;
-    const double *p = src + i;
-#pragma unroll
-    for (int m = 0; m < NP; ++m, p += nx) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
 }
-#else
-template <int P>
-__device__ __forceinline__ void row_prefetch_l2(const double *src, int nx, int ifirst, int lane)
-{
-    constexpr int NP = (P + 1) * (P + 1);
-#pragma unroll
-    for (int k = lane; k < 3 * NP; k += kLanes) {
-        const int m = k / 3, part = k - 3 * m;
-        int e = ifirst + (part == 0 ? 0 : part == 1 ? 16 : kLanes - 1);
-        if (e >= nx) e -= nx;
-        if (e < 0) e += nx;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(src + (size_t)m * nx + e));
-    }
-}
-#endif
 
-// this lane's element, one variable: NP words, mode-major, lane-minor
-template <int P>
-__device__ __forceinline__ void tile_fetch(double *dst, const double *src, int nx, int i, int lane)
+// one variable's row tile of the strip (bytes contiguous) -> shared memory
+__device__ __forceinline__ void tma_row(double *dst, const double *src, unsigned bytes,
+                                        unsigned long long *mb)
 {
-    constexpr int NP = (P + 1) * (P + 1);
-#pragma unroll
-    for (int m = 0; m < NP; ++m) cp_async8(dst + m * kLanes + lane, src + (size_t)m * nx + i);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(mb))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long *mb, unsigned parity)
+{
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(mb)),
+        "r"(parity)
+        : "memory");
+}
+
+// shared-memory reads of the generic proxy before a TMA overwrite
+__device__ __forceinline__ void fence_proxy_async()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2_bulk(const double *src, unsigned bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
 // bottom (sign -1) or top (sign +1) trace at the n edge nodes from modes
@@ -448,7 +430,7 @@ __device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], do
 // DIR 1: y-face, physical flux G = cos/R * (...), alpha = cos (|v|+c)/R.
 template <int P, int DIR>
 __device__ __forceinline__ void face_flux(const double (&in)[3][P + 1], const double (&out)[3][P + 1],
-                                          double *sF, int lane, const StageParams &kp,
+                                          double *sF, int ld, int col, const StageParams &kp,
                                           double cr_e, double cos_e, double alpha_glob,
                                           double scale)
 {
@@ -456,27 +438,18 @@ __device__ __forceinline__ void face_flux(const double (&in)[3][P + 1], const do
     constexpr int M = DIR == 0 ? 1 : 2;   // normal momentum
     double rin[N], rout[N];
     double am[N];
-    bool low = false;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         double ci, co;
-        inv_and_celerity(in[0][k], kp.h_floor, kp.sqrt_g, rin[k], ci);
-        inv_and_celerity(out[0][k], kp.h_floor, kp.sqrt_g, rout[k], co);
-        low |= (in[0][k] < kp.h_floor) | (out[0][k] < kp.h_floor);
+        inv_and_celerity(in[0][k], kp.h_floor, kp.inv_floor, kp.sqrt_g, rin[k], ci);
+        inv_and_celerity(out[0][k], kp.h_floor, kp.inv_floor, kp.sqrt_g, rout[k], co);
         am[k] = max_nn(fabs(in[M][k] * rin[k]) + ci, fabs(out[M][k] * rout[k]) + co);
     }
 #pragma unroll
     for (int w = 1; w < N; w *= 2)     // pairwise tree: log2(N) dependent maxima
 #pragma unroll
         for (int k = 0; k + w < N; k += 2 * w) am[k] = max_nn(am[k], am[k + w]);
-    double amax = am[0];
-    if (__any_sync(0xffffffffu, low)) {      // h below the velocity floor: exact celerity
-        amax = 0.0;
-#pragma unroll
-        for (int k = 0; k < N; ++k)
-            amax = fmax(amax, fmax(fabs(in[M][k] * rin[k]) + sqrt(kp.gravity * fmax(in[0][k], 0.0)),
-                                   fabs(out[M][k] * rout[k]) + sqrt(kp.gravity * fmax(out[0][k], 0.0))));
-    }
+    const double amax = am[0];
     double alpha = amax * kp.inv_r;
     if (DIR == 1) alpha *= cos_e;
     if (kp.alpha_mode != 0) alpha = alpha_glob;
@@ -509,45 +482,71 @@ __device__ __forceinline__ void face_flux(const double (&in)[3][P + 1], const do
         double g[N];
         n2m<P, 2>(fs[v], g);
 #pragma unroll
-        for (int b = 0; b < N; ++b) sF[(v * N + b) * kLanes + lane] = g[b];
+        for (int b = 0; b < N; ++b) sF[(v * N + b) * ld + col] = g[b];
     }
 }
 
+// The same flux with the direction a runtime value: the face warp serves
+// its y-faces and the strip's border x-face from ONE inlined copy (the
+// stage kernel is instruction-cache sensitive, measured).
 template <int P>
-__device__ __forceinline__ void traces_from_smem(double (&tr)[3][P + 1], const double *s, int lane)
+__device__ __forceinline__ void face_flux_rt(const double (&in)[3][P + 1], const double (&out)[3][P + 1],
+                                             double *sF, int ld, int col, const StageParams &kp, int dir,
+                                             double cr_e, double cos_e, double alpha_glob, double scale)
+{
+    constexpr int N = P + 1;
+    double rin[N], rout[N], mi[N], mo[N];
+    double am[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        double ci, co;
+        inv_and_celerity(in[0][k], kp.h_floor, kp.inv_floor, kp.sqrt_g, rin[k], ci);
+        inv_and_celerity(out[0][k], kp.h_floor, kp.inv_floor, kp.sqrt_g, rout[k], co);
+        mi[k] = dir == 0 ? in[1][k] : in[2][k];     // normal momentum
+        mo[k] = dir == 0 ? out[1][k] : out[2][k];
+        am[k] = max_nn(fabs(mi[k] * rin[k]) + ci, fabs(mo[k] * rout[k]) + co);
+    }
+#pragma unroll
+    for (int w = 1; w < N; w *= 2)
+#pragma unroll
+        for (int k = 0; k + w < N; k += 2 * w) am[k] = max_nn(am[k], am[k + w]);
+    double alpha = am[0] * kp.inv_r;
+    if (dir == 1) alpha *= cos_e;
+    if (kp.alpha_mode != 0) alpha = alpha_glob;
+    const double ha = (0.5 * scale) * alpha;
+    const double hs = (0.5 * scale) * (dir == 0 ? kp.inv_r : cr_e);
+    const double sx = dir == 0 ? 1.0 : 0.0, sy = 1.0 - sx;   // where g h^2 / 2 enters
+    double fs[3][N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const double hi = in[0][k], ui = in[1][k], vi = in[2][k];
+        const double ho = out[0][k], uo = out[1][k], vo = out[2][k];
+        const double gi = hi * hi * kp.half_g, go = ho * ho * kp.half_g;
+        const double wi = mi[k] * rin[k], wo = mo[k] * rout[k];   // normal velocities
+        const double fi1 = fma(ui, wi, sx * gi), fo1 = fma(uo, wo, sx * go);
+        const double fi2 = fma(vi, wi, sy * gi), fo2 = fma(vo, wo, sy * go);
+        fs[0][k] = fma(hs, mi[k] + mo[k], -ha * (ho - hi));
+        fs[1][k] = fma(hs, fi1 + fo1, -ha * (uo - ui));
+        fs[2][k] = fma(hs, fi2 + fo2, -ha * (vo - vi));
+    }
+#pragma unroll
+    for (int v = 0; v < 3; ++v) {
+        double g[N];
+        n2m<P, 2>(fs[v], g);
+#pragma unroll
+        for (int b = 0; b < N; ++b) sF[(v * N + b) * ld + col] = g[b];
+    }
+}
+
+// traces [3][N] from shared memory: element column `col` of a [3][N][ld] array
+template <int P>
+__device__ __forceinline__ void traces_from_smem(double (&tr)[3][P + 1], const double *s, int ld, int col)
 {
     constexpr int N = P + 1;
 #pragma unroll
     for (int v = 0; v < 3; ++v)
 #pragma unroll
-        for (int k = 0; k < N; ++k) tr[v][k] = s[(v * N + k) * kLanes + lane];
-}
-
-// Face warp: bottom traces of the row above (from the coefficient ring,
-// all three variables) -> y-face flux with the current row's top traces.
-template <int P>
-__device__ __forceinline__ unsigned yface_from_ring(const double *ring_row, const double *sT,
-                                                    double *sF, int lane, const StageParams &kp,
-                                                    const double *rowtab_above, double alpha_y)
-{
-    constexpr int N = P + 1;
-    constexpr int NP = N * N;
-    using RL = RowLayout<P>;
-    double bt[3][N];
-#pragma unroll
-    for (int v = 0; v < 3; ++v) {
-        double cv[N][N];
-        tile_read<P>(cv, ring_row + v * NP * kLanes, lane);
-        ytrace<P, false>(cv, bt[v]);
-    }
-    unsigned bad = 0;
-#pragma unroll
-    for (int k = 0; k < N; ++k) bad |= !(bt[0][k] > 0.0);
-    double tt[3][N];
-    traces_from_smem<P>(tt, sT, lane);
-    face_flux<P, 1>(tt, bt, sF, lane, kp, rowtab_above[RL::CRB], rowtab_above[RL::COSB], alpha_y,
-                    kp.bdx);
-    return bad;
+        for (int k = 0; k < N; ++k) tr[v][k] = s[(v * N + k) * ld + col];
 }
 
 // Pointwise flux / source of variable v at the N nodes (qi, qj), qj = 0..N-1
@@ -568,7 +567,7 @@ __device__ __forceinline__ void node_physics(int v, int qi, const double *sU, co
         const double hv = sU[(2 * NP + q) * kLanes + lane];
         const double crc = row[RL::CRC + qj];
         if (v == 0) {
-            F[qj] = hu * CXN;
+            F[qj] = hu;
             G[qj] = hv * crc;
             S[qj] = 0.0;
         } else {
@@ -578,11 +577,11 @@ __device__ __forceinline__ void node_physics(int v, int qi, const double *sU, co
             const double u = hu * r, w = hv * r;
             const double t = fma(u, row[RL::SRS + qj], row[RL::FCS + qj]);
             if (v == 1) {
-                F[qj] = fma(hu, u, gh2) * CXN;
+                F[qj] = fma(hu, u, gh2);
                 G[qj] = hu * w * crc;
                 S[qj] = t * hv;
             } else {
-                F[qj] = hu * w * CXN;
+                F[qj] = hu * w;
                 G[qj] = fma(hv, w, gh2) * crc;
                 S[qj] = -fma(gh2, row[RL::SRS + qj], t * hu);
             }
@@ -620,22 +619,6 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
 #pragma unroll 1
     for (int ip = 0; ip < H; ++ip) {
         double f0[N], g0[N], f1[N], g1[N];
-#if DG_VOL_COMPACT
-        // one loop body for both lines of the pair (I-cache footprint)
-#pragma unroll 1
-        for (int side = 0; side < 2; ++side) {
-            double F[N], G[N], S[N];
-            node_physics<P>(v, side ? N - 1 - ip : ip, sU, row, lane, kp, F, G, S);
-            line_project<P>(v, F, G, S, f1, g1);
-            if (side == 0) {
-#pragma unroll
-                for (int b = 0; b < N; ++b) {
-                    f0[b] = f1[b];
-                    g0[b] = g1[b];
-                }
-            }
-        }
-#else
         {
             double F[N], G[N], S[N];
             node_physics<P>(v, ip, sU, row, lane, kp, F, G, S);
@@ -643,11 +626,10 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
             node_physics<P>(v, N - 1 - ip, sU, row, lane, kp, F, G, S);
             line_project<P>(v, F, G, S, f1, g1);
         }
-#endif
         double pd[N], pp[N];
 #pragma unroll
         for (int a = 0; a < N; ++a) {
-            pd[a] = WD(a, ip) * CXF;   // F's 1/R * determ/bd_det_x folded in here
+            pd[a] = WD(a, ip) * kp.inv_r_cx;   // F's 1/R * determ/bd_det_x folded in here
             pp[a] = WP(a, ip);
         }
 #pragma unroll
@@ -668,7 +650,7 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
         for (int b = 0; b < N; ++b)
 #pragma unroll
             for (int a = 0; a < N; ++a)
-                vol[a][b] = (a & 1) ? fma(WD(a, H) * CXF, f[b], vol[a][b])
+                vol[a][b] = (a & 1) ? fma(WD(a, H) * kp.inv_r_cx, f[b], vol[a][b])
                                     : fma(WP(a, H), g[b], vol[a][b]);
     }
 }
@@ -676,29 +658,31 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
 // Boundary lifts, inverse mass, stage combination and store for variable v.
 // The mass block is applied column by column (one row of T from shared
 // memory at a time) so that vol, c and u^n are the only tiles held.
+// Uv / Yv point at this lane's element of the variable's strip block
+// (mode stride 32 doubles: immediate offsets).
 template <int P, bool HAS_U>
 __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const double *cur,
-                                             const double *Uv, int v, const double *sFX,
+                                             const double *Uv, int v, const double *sFX, const double *sF0,
                                              const double *sFtop, const double *sFbot, bool has_top,
                                              bool has_bot, const double *row, int lane, bool owned,
-                                             double *Yv, int nx, int i, const StageParams &kp)
+                                             double *Yv, const StageParams &kp)
 {
     constexpr int N = P + 1;
     using RL = RowLayout<P>;
     double un[N][N];
-    if (HAS_U && !(DG_ABL & 4)) {      // u^n: plain loads (U may alias Y)
+    if (HAS_U) {                       // u^n: plain loads (U may alias Y)
 #pragma unroll
         for (int a = 0; a < N; ++a)
 #pragma unroll
-            for (int b = 0; b < N; ++b) un[a][b] = Uv[(size_t)(a * N + b) * nx + i];
+            for (int b = 0; b < N; ++b) un[a][b] = Uv[(a * N + b) * kLanes];
     }
-    const int ll = lane > 0 ? lane - 1 : 0;
-    const int o = (v * N) * kLanes;
+    constexpr int LDX = kLanes + 1;    // x-face columns: face f is the left face of lane f
+    const int o = (v * N) * kLanes, ox = (v * N) * LDX;
 #pragma unroll
     for (int b = 0; b < N; ++b) {
-        // projected face lifts (bdy / bdx folded in by the face warp)
-        const double r = sFX[o + b * kLanes + lane];
-        const double l = sFX[o + b * kLanes + ll];
+        // projected face lifts (bdy / bdx folded in by the face warps)
+        const double l = lane == 0 ? sF0[v * N + b] : sFX[ox + b * LDX + lane];
+        const double r = sFX[ox + b * LDX + lane + 1];
         const double t = has_top ? sFtop[o + b * kLanes + lane] : 0.0;   // pole faces carry
         const double bo = has_bot ? sFbot[o + b * kLanes + lane] : 0.0;  // no flux (dg.py:483-495)
         // x lifts broadcast along a (parity of a), y lifts along b (parity of b)
@@ -721,15 +705,11 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
 #pragma unroll
         for (int a = 0; a < N; ++a) {
             double k = tb[0] * vol[a][0];
-            if (!(DG_ABL & 32)) {
 #pragma unroll
-                for (int bb = 1; bb < N; ++bb) k = fma(tb[bb], vol[a][bb], k);
-            } else {
-                k = vol[a][b];
-            }
+            for (int bb = 1; bb < N; ++bb) k = fma(tb[bb], vol[a][bb], k);
             double y = fma(kp.b, cur[(a * N + b) * kLanes + lane], (kp.g * (double)(2 * a + 1)) * k);
-            if (HAS_U && !(DG_ABL & 4)) y = fma(kp.a, un[a][b], y);
-            if (owned) Yv[(a * N + b) * nx] = y;
+            if (HAS_U) y = fma(kp.a, un[a][b], y);
+            if (owned) Yv[(a * N + b) * kLanes] = y;
             fexp = max(fexp, __double2hiint(y) & 0x7ff00000);
             if (a == 0 && b == 0) mean = y;
         }
@@ -742,33 +722,96 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
     return bad;
 }
 
+// Face warp: the traces of the strip's left border face for one row.
+// Lanes 0..5 each build one trace: (side 0) R trace of the left neighbour
+// element eL = (32 s - 1) mod nx, from global memory (L2-warmed a row
+// ahead); (side 1) L trace of the strip's element 0, from the coefficient
+// ring.  Also the L trace of the right neighbour eR = (32 s + nvalid) mod nx
+// (lanes 6..8), which the h warp needs for the last lane's right face.
+template <int P>
+__device__ __forceinline__ void border_traces(const double *Xrow, const double *ring_slot, int eL, int eR,
+                                              double *sHL, double *sE0, double *sHR, int lane,
+                                              const StageParams &kp)
+{
+    constexpr int N = P + 1;
+    constexpr int NP = N * N;
+    if (lane < 9) {
+        const int side = lane / 3, v = lane - 3 * side;
+        double c[N][N];
+        if (side == 1) {
+            const double *src = ring_slot + v * NP * kLanes;   // lane 0 of the ring tile
+#pragma unroll
+            for (int a = 0; a < N; ++a)
+#pragma unroll
+                for (int b = 0; b < N; ++b) c[a][b] = src[(a * N + b) * kLanes];
+        } else {
+            const int e = side == 0 ? eL : eR;
+            const double *src = Xrow + (size_t)v * kp.vstride + (size_t)(e >> 5) * NP * kLanes + (e & 31);
+#pragma unroll
+            for (int a = 0; a < N; ++a)
+#pragma unroll
+                for (int b = 0; b < N; ++b) c[a][b] = __ldg(src + (a * N + b) * kLanes);
+        }
+        double t[N][N];
+#pragma unroll
+        for (int a = 0; a < N; ++a) m2n<P, 0>(c[a], t[a]);
+        const double sg = side == 0 ? 1.0 : -1.0;    // R trace: sum_a t, L trace: sum_a (-1)^a t
+        double *dst = side == 0 ? sHL : side == 1 ? sE0 : sHR;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            double e = t[0][q], o = 0.0;
+#pragma unroll
+            for (int a = 2; a < N; a += 2) e += t[a][q];
+            if constexpr (N > 1) {
+                o = t[1][q];
+#pragma unroll
+                for (int a = 3; a < N; a += 2) o += t[a][q];
+            }
+            dst[v * N + q] = fma(sg, o, e);
+        }
+    }
+    __syncwarp();
+}
+
+// bottom traces (eta = -1) of one row, all three variables, from its ring tile
+template <int P>
+__device__ __forceinline__ void bottom_traces(const double *ring_row, int lane, double (&bt)[3][P + 1])
+{
+    constexpr int N = P + 1;
+    constexpr int NP = N * N;
+#pragma unroll
+    for (int v = 0; v < 3; ++v) {
+        double cv[N][N];
+        tile_read<P>(cv, ring_row + v * NP * kLanes, lane);
+        ytrace<P, false>(cv, bt[v]);
+    }
+}
+
 template <int P, bool HAS_U>
 __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel(StageParams kp)
 {
     constexpr int N = P + 1;
     constexpr int NP = N * N;
+    constexpr unsigned kTileBytes = NP * kLanes * sizeof(double);   // one variable's row tile
     using SM = Smem<P>;
     using RL = RowLayout<P>;
     extern __shared__ double smem[];
     // fixed roles: warp w runs on sub-partition w of its SM, so every
     // sub-partition executes a single code path (better I-cache locality
-    // than rotating roles across CTAs, measured)
+    // than rotating roles, measured)
     const int role = threadIdx.x >> 5;
     const int v = role < kVarWarps ? role : 0;     // face warp borrows var 0's addressing
     const bool face_warp = role == kVarWarps;
     const int lane = threadIdx.x & 31;
     const int nx = kp.nx;
-    const int i0 = blockIdx.x * kOwned;
-    int i = (i0 - 1 + lane) % nx;
-    if (i < 0) i += nx;
-    const int nown = min(kOwned, nx - i0);
-    const bool owned = lane >= 1 && lane <= nown;
+    const int strip = blockIdx.x;
+    const int nvalid = min(kLanes, nx - strip * kLanes);
+    const bool owned = lane < nvalid;
     const int jb = kp.j_begin + blockIdx.y * kp.rc;
     const int je = min(jb + kp.rc, kp.j_end);
     if (jb >= je) return;
 
-    // coefficient ring: slot s holds row (jb + s) mod 2, layout [var][mode][lane]
-    double *const ringS = smem + SM::XR0;
+    double *const ringS = smem + SM::XR0;          // [slot][var][mode][lane]
     double *const ring0 = ringS + v * NP * kLanes;   // this warp's variable
     double *sU = smem + SM::U;
     double *sXL = smem + SM::XL;
@@ -778,23 +821,34 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
     double *sFa = smem + SM::FY0;
     double *sFb = smem + SM::FY1;
     double *sRow = smem + SM::ROW;
+    unsigned long long *mbar = reinterpret_cast<unsigned long long *>(smem + SM::MBAR);   // [slot][var]
 
-    const double *Xz = kp.X + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx;
-    const double *Uz = kp.U ? kp.U + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx : nullptr;
-    double *Yz = kp.Y + (size_t)blockIdx.z * kp.zstride + (size_t)v * NP * nx;
+    // this strip's block of variable v (row 0); per-lane element pointers
+    const double *Xb = kp.X + (size_t)blockIdx.z * kp.zstride + (size_t)strip * NP * kLanes;
+    const double *Xz = Xb + (size_t)v * kp.vstride;
+    const double *Uz = kp.U ? kp.U + (size_t)blockIdx.z * kp.zstride + (size_t)strip * NP * kLanes +
+                                  (size_t)v * kp.vstride + lane
+                            : nullptr;
+    double *Yz = kp.Y + (size_t)blockIdx.z * kp.zstride + (size_t)strip * NP * kLanes +
+                 (size_t)v * kp.vstride + lane;
     const bool chk = (v == 0) && !face_warp;
     unsigned bad = 0;
 
     // rows whose coefficients exist: local r with global row0+r in [0, ny)
     const int r_last = min(kp.nrows - 1, kp.ny - 1 - kp.row0);
+    const int last_fetch = min(je, r_last);        // rows jb..last_fetch stream through the ring
 
-    // prologue: start streaming rows jb and jb+1
-    if (!face_warp) {
-        tile_fetch<P>(ring0, Xz + (size_t)jb * kp.rstride, nx, i, lane);
-        cp_commit();
-        if (jb + 1 <= min(je, r_last))
-            tile_fetch<P>(ring0 + SM::TILE, Xz + (size_t)(jb + 1) * kp.rstride, nx, i, lane);
-        cp_commit();
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 6; ++k) mbar_init(mbar + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // prologue: the var warps' elected lanes start streaming rows jb, jb+1
+    if (!face_warp && lane == 0) {
+        tma_row(ring0, Xz + (size_t)jb * kp.rstride, kTileBytes, mbar + v);
+        if (jb + 1 <= last_fetch)
+            tma_row(ring0 + SM::TILE, Xz + (size_t)(jb + 1) * kp.rstride, kTileBytes, mbar + 3 + v);
     }
 
     // row-table ring: slot (r - jb) % 3 holds local row r (rows jb, jb+1 now,
@@ -814,132 +868,138 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
 
     // top traces of the row below the chunk (its first row's bottom face)
     const bool below = gfirst > 0;
-    double c[N][N];
     if (below && !face_warp) {
-        const double *src = Xz + (size_t)(jb - 1) * kp.rstride;
+        const double *src = Xz + (size_t)(jb - 1) * kp.rstride + lane;
+        double c[N][N];
 #pragma unroll
         for (int a = 0; a < N; ++a)
 #pragma unroll
-            for (int b = 0; b < N; ++b) c[a][b] = __ldg(src + (size_t)(a * N + b) * nx + i);
+            for (int b = 0; b < N; ++b) c[a][b] = __ldg(src + (a * N + b) * kLanes);
         double tt[N];
         ytrace<P, true>(c, tt);
 #pragma unroll
         for (int q = 0; q < N; ++q) sT[(v * N + q) * kLanes + lane] = tt[q];
     }
-    if (!face_warp) cp_wait<1>();                    // row jb landed (own copies); jb+1 in flight
-    __syncthreads();
+    if (!face_warp) mbar_wait(mbar + v, 0);        // row jb landed (this variable)
+    // periodic neighbours of the strip's border elements
+    const int eL = (strip * kLanes - 1 + nx) % nx;
+    const int eR = (strip * kLanes + nvalid) % nx;
+    __syncthreads();                               // prologue barrier A
+
     if (face_warp) {
-        if (below)
-            bad |= yface_from_ring<P>(ringS, sT, sFb, lane, kp, sRow, alpha_y);
-        else
-            bad |= 0u;
-    }
-    __syncthreads();
-    if (face_warp && !below) {
-        // no bottom face, but the first row's bottom traces still need the positivity check
-        double cv[N][N];
-        tile_read<P>(cv, ringS, lane);
-        double bt[N];
-        ytrace<P, false>(cv, bt);
+        // Face warp.  Iteration `it` (from the pre-iteration jb-1): job 0 =
+        // the y-face above row it (the bottom face of row jb in the
+        // pre-iteration), job 1 = the strip's left border x-face of row it+1,
+        // computed in the window between the rows' barriers 2 and 1.
+        double *fa = sFa, *fb = sFb;
+        for (int it = jb - 1; it < je; ++it) {
+            const int k = it - jb;
+            const bool pre = it < jb;
+            if (!pre) __syncthreads();                 // barrier 1 of row it
+            const double *next_tile = ringS + ((k + 1) & 1) * SM::TILE;   // X(it+1)
+            if (it + 1 <= last_fetch) {
+                double bt[3][N];
+                bottom_traces<P>(next_tile, lane, bt);
 #pragma unroll
-        for (int k = 0; k < N; ++k) bad |= !(bt[k] > 0.0);
-    }
-
-#ifdef DG_TIMING
-    unsigned tacc[5] = {0, 0, 0, 0, 0};
-#endif
-    for (int jl = jb; jl < je; ++jl) {
-        TSTAMP(0);
-        const int slot = (jl - jb) & 1;
-        double *const cur = ring0 + slot * SM::TILE;
-        const int jg = kp.row0 + jl;
-        const bool has_top = jg + 1 < kp.ny;
-        const bool has_bot = jg > 0;
-        const double *row = sRow + ((jl - jb) % 3) * RL::STRIDE;
-
-        if (!face_warp) {
-            // warm L2 for this row's u^n and for row jl+2 (copied in after finalize)
-            if (HAS_U) row_prefetch_l2<P>(Uz + (size_t)jl * kp.rstride, nx, i0 - 1, lane);
-            if (jl + 2 <= min(je, r_last))
-                row_prefetch_l2<P>(Xz + (size_t)(jl + 2) * kp.rstride, nx, i0 - 1, lane);
-            tile_read<P>(c, cur, lane);                // X(jl)
-            if (DG_ABL & 16) {
-#pragma unroll
-                for (int a = 0; a < N; ++a)
-#pragma unroll
-                    for (int b = 0; b < N; ++b) sU[(v * NP + a * N + b) * kLanes + lane] = c[a][b];
-            } else {
-                bad |= eval_row<P>(c, sU + v * NP * kLanes, sXL + v * N * kLanes, sXR + v * N * kLanes,
-                                   sT + v * N * kLanes, lane, chk);
+                for (int q = 0; q < N; ++q) bad |= owned && !(bt[0][q] > 0.0);
+                const bool face = pre ? below : (kp.row0 + it + 1 < kp.ny);
+                if (face) {
+                    double tt[3][N];
+                    traces_from_smem<P>(tt, sT, kLanes, lane);
+                    const double *above = sRow + ((k + 1) % 3) * RL::STRIDE;
+                    face_flux_rt<P>(tt, bt, pre ? fb : fa, kLanes, lane, kp, 1, above[RL::CRB],
+                                    above[RL::COSB], alpha_y, kp.bdx);
+                }
             }
-            cp_wait<0>();                              // X(jl+1) landed (own copies)
-        }
-        TSTAMP(1);
-        __syncthreads();
-        TSTAMP(2);
-
-        if (face_warp) {
-            if (has_top && !(DG_ABL & 1))
-                bad |= yface_from_ring<P>(ringS + (slot ^ 1) * SM::TILE, sT, sFa, lane, kp,
-                                          sRow + ((jl + 1 - jb) % 3) * RL::STRIDE, alpha_y);
-            // stage the table of row jl+2 (its slot held row jl-1, no longer read)
-            if (jl + 2 <= je && jg + 2 < kp.ny) {
-                double *dst = sRow + ((jl + 2 - jb) % 3) * RL::STRIDE;
-                const double *src = kp.rowtab + (size_t)(jg + 2) * RL::STRIDE;
+            if (!pre && it + 2 <= je && kp.row0 + it + 2 < kp.ny) {
+                // stage the table of row it+2 (its slot held row it-1, no longer read)
+                double *dst = sRow + ((k + 2) % 3) * RL::STRIDE;
+                const double *src = kp.rowtab + (size_t)(kp.row0 + it + 2) * RL::STRIDE;
                 for (int idx = lane; idx < RL::STRIDE; idx += kLanes) dst[idx] = src[idx];
             }
-            TSTAMP(3);
-            __syncthreads();
-            TSTAMP(4);
-            TACC(2, tk3 - tk2);
-            TACC(3, tk4 - tk3);
-        } else {
-            if (v == 0 && !(DG_ABL & 2)) {
-                // the h warp has the lightest volume work: it takes the x-faces
+            __syncthreads();                           // barrier 2 of row it (prologue barrier B)
+            if (!pre) {
+                double *t = fa;
+                fa = fb;
+                fb = t;
+            }
+            if (it + 1 < je) {
+                const double *Xrow = kp.X + (size_t)blockIdx.z * kp.zstride + (size_t)(it + 1) * kp.rstride;
+                if (it + 2 < je) {
+                    // warm L2 for the next row's two neighbour elements
+                    for (int t = lane; t < 6 * NP; t += kLanes) {
+                        const int side = t / (3 * NP), r = t - side * 3 * NP, vv = r / NP, m = r - vv * NP;
+                        const int e = side ? eR : eL;
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(
+                            Xrow + kp.rstride + (size_t)vv * kp.vstride + (size_t)(e >> 5) * NP * kLanes +
+                            m * kLanes + (e & 31)));
+                    }
+                }
+                border_traces<P>(Xrow, next_tile, eL, eR, smem + SM::HL, smem + SM::E0, smem + SM::HR,
+                                 lane, kp);
                 double in[3][N], out[3][N];
-                traces_from_smem<P>(in, sXR, lane);
-                traces_from_smem<P>(out, sXL, min(lane + 1, 31));
-                face_flux<P, 0>(in, out, sFX, lane, kp, 0.0, 0.0, alpha_x, kp.bdy);
+                traces_from_smem<P>(in, smem + SM::HL, 1, 0);
+                traces_from_smem<P>(out, smem + SM::E0, 1, 0);
+                // every lane computes the same face (uniform control flow, identical stores)
+                face_flux_rt<P>(in, out, smem + SM::F0 + ((k + 1) & 1) * 3 * N, 1, 0, kp, 0, 0.0, 0.0,
+                                alpha_x, kp.bdy);
+            }
+        }
+    } else {
+        __syncthreads();                           // prologue barrier B
+        for (int jl = jb; jl < je; ++jl) {
+            const int k = jl - jb;
+            const int slot = k & 1;
+            double *const cur = ring0 + slot * SM::TILE;
+            const int jg = kp.row0 + jl;
+            const bool has_top = jg + 1 < kp.ny;
+            const bool has_bot = jg > 0;
+            const double *row = sRow + (k % 3) * RL::STRIDE;
+
+            // warm L2 for this row's u^n and for row jl+2 (copied in after finalize)
+            if (lane == 0) {
+                if (HAS_U) prefetch_l2_bulk(Uz - lane + (size_t)jl * kp.rstride, kTileBytes);
+                if (jl + 2 <= last_fetch) prefetch_l2_bulk(Xz + (size_t)(jl + 2) * kp.rstride, kTileBytes);
+            }
+            {
+                double c[N][N];
+                tile_read<P>(c, cur, lane);            // X(jl)
+                bad |= owned & eval_row<P>(c, sU + v * NP * kLanes, sXL + v * N * kLanes,
+                                           sXR + v * N * kLanes, sT + v * N * kLanes, lane, chk);
+            }
+            if (jl + 1 <= last_fetch) mbar_wait(mbar + (slot ^ 1) * 3 + v, ((k + 1) >> 1) & 1);   // X(jl+1)
+            __syncthreads();                           // barrier 1
+
+            if (v == 0) {
+                // the h warp has the lightest volume work: it takes the x-faces 1..32
+                // (right face of every lane; the last valid lane's neighbour is the halo)
+                double in[3][N], out[3][N];
+                traces_from_smem<P>(in, sXR, kLanes, lane);
+                if (lane == nvalid - 1)
+                    traces_from_smem<P>(out, smem + SM::HR, 1, 0);
+                else
+                    traces_from_smem<P>(out, sXL, kLanes, min(lane + 1, kLanes - 1));
+                face_flux<P, 0>(in, out, sFX, kLanes + 1, lane + 1, kp, 0.0, 0.0, alpha_x, kp.bdy);
             }
             double vol[N][N];
-            if ((DG_ABL & 8) && v > 0) {
-#pragma unroll
-                for (int a = 0; a < N; ++a)
-#pragma unroll
-                    for (int b = 0; b < N; ++b) vol[a][b] = sU[(a * N + b) * kLanes + lane];
-            } else {
-                volume<P>(vol, v, sU, row, lane, kp);
-            }
-            TSTAMP(3);
-            __syncthreads();
-            TSTAMP(4);
+            volume<P>(vol, v, sU, row, lane, kp);
+            __syncthreads();                           // barrier 2
             const size_t roff = (size_t)jl * kp.rstride;
-            bad |= finalize<P, HAS_U>(vol, cur, HAS_U ? Uz + roff : nullptr, v, sFX, sFa, sFb,
-                                      has_top, has_bot, row, lane, owned, Yz + roff + i, nx, i, kp);
+            bad |= finalize<P, HAS_U>(vol, cur, HAS_U ? Uz + roff : nullptr, v, sFX,
+                                      smem + SM::F0 + slot * 3 * N, sFa, sFb, has_top, has_bot, row, lane,
+                                      owned, Yz + roff, kp);
             // X(jl) is consumed: stream row jl+2 into its slot (L2-warm by now)
             __syncwarp();
-            if (jl + 2 <= min(je, r_last))
-                tile_fetch<P>(cur, Xz + (size_t)(jl + 2) * kp.rstride, nx, i, lane);
-            cp_commit();
-            TSTAMP(5);
-            TACC(2, tk3 - tk2);
-            TACC(3, tk4 - tk3);
-            TACC(4, tk5 - tk4);
+            if (lane == 0 && jl + 2 <= last_fetch) {
+                fence_proxy_async();
+                tma_row(cur, Xz + (size_t)(jl + 2) * kp.rstride, kTileBytes, mbar + slot * 3 + v);
+            }
+            double *tmp = sFa;
+            sFa = sFb;
+            sFb = tmp;
         }
-        TACC(0, tk1 - tk0);
-        TACC(1, tk2 - tk1);
-        double *tmp = sFa;
-        sFa = sFb;
-        sFb = tmp;
     }
-    if (!face_warp) cp_wait<0>();
 
-#ifdef DG_TIMING
-    if (lane == 0) {
-        for (int k = 0; k < 5; ++k) atomicAdd(&g_timing[role][k], (unsigned long long)tacc[k]);
-        atomicAdd(&g_timing[role][5], (unsigned long long)(je - jb));
-    }
-#endif
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && lane == 0) {
         atomicOr(kp.status, bad);

@@ -6,11 +6,14 @@ dg.py:47-89 and 166-543 (constructor, attributes, ``zero_state``,
 ``max_physical_speed``); the right-hand side itself is one fused CUDA launch
 through the C ABI (include/dgswe_b200.h, ``dgswe_rhs``).
 
-Device layout of a state: one fp64 tensor ``data[z, j, v, m, i]``
-(level, latitude row, variable, mode, longitude) -- structure of arrays
-with longitude fastest so a warp's 32 lanes read 32 consecutive elements.
-There is no halo ring: the periodic longitude wrap is an index wrap inside
-the kernel (replaces ``_halo_exchange``, dg.py:330-346).
+Device layout of a state: one fp64 tensor ``data[z, j, v, s, m, l]``
+(level, latitude row, variable, strip, mode, lane) with longitude element
+i = 32 s + l -- a strip-blocked structure of arrays: a warp's 32 lanes read
+32 consecutive elements of one mode, and one variable's row tile of a strip
+is a single contiguous block (the unit of the kernel's TMA copies).  The
+last strip is zero-padded past nx.  There is no halo ring: the periodic
+longitude wrap is an index wrap inside the kernel (replaces
+``_halo_exchange``, dg.py:330-346).
 """
 
 from __future__ import annotations
@@ -42,14 +45,37 @@ class RusanovParams:
             raise ValueError(f"mode must be 'local' or 'global', got {self.mode!r}")
 
 
+STRIP = _lib.STRIP
+
+
+def nstrips(nx: int) -> int:
+    return (nx + STRIP - 1) // STRIP
+
+
+def device_shape(nz: int, nrows: int, nphi: int, nx: int) -> tuple:
+    """Shape of a device state buffer: (nz, nrows, 3, nstrip, nphi, STRIP)."""
+    return (nz, nrows, 3, nstrips(nx), nphi, STRIP)
+
+
 def _to_device_layout(stack: np.ndarray) -> np.ndarray:
-    """(3, nx, ny, nz, nphi) reference interior layout -> (nz, ny, 3, nphi, nx)."""
-    return np.ascontiguousarray(np.transpose(stack, (3, 2, 0, 4, 1)))
+    """(3, nx, ny, nz, nphi) reference interior layout -> (nz, ny, 3, nstrip, nphi, STRIP)."""
+    _, nx, ny, nz, nphi = stack.shape
+    ns = nstrips(nx)
+    pad = np.zeros((3, ns * STRIP, ny, nz, nphi), dtype=np.float64)
+    pad[:, :nx] = stack
+    pad = pad.reshape(3, ns, STRIP, ny, nz, nphi)
+    return np.ascontiguousarray(np.transpose(pad, (4, 3, 0, 1, 5, 2)))
 
 
-def _to_reference_layout(data: torch.Tensor) -> np.ndarray:
-    """(nz, ny, 3, nphi, nx) device tensor -> (3, nx, ny, nz, nphi) host."""
-    return np.ascontiguousarray(data.detach().cpu().numpy().transpose(2, 4, 1, 0, 3))
+def lon_major(data: torch.Tensor, nx: int) -> torch.Tensor:
+    """View-transform of a device state to (nz, nrows, 3, nphi, nx) (a copy)."""
+    nz, nr, nv, ns, nphi, L = data.shape
+    return data.permute(0, 1, 2, 4, 3, 5).reshape(nz, nr, nv, nphi, ns * L)[..., :nx]
+
+
+def _to_reference_layout(data: torch.Tensor, nx: int) -> np.ndarray:
+    """(nz, ny, 3, nstrip, nphi, STRIP) device tensor -> (3, nx, ny, nz, nphi) host."""
+    return np.ascontiguousarray(lon_major(data, nx).detach().cpu().numpy().transpose(2, 4, 1, 0, 3))
 
 
 class _VarView:
@@ -81,9 +107,9 @@ class State:
     def __init__(self, data: torch.Tensor, nx: int, ny: int, nz: int, nphi: int):
         if data.dtype != torch.float64 or not data.is_cuda:
             raise TypeError("State data must be a CUDA float64 tensor")
-        if tuple(data.shape) != (nz, ny, 3, nphi, nx) or not data.is_contiguous():
-            raise ValueError(f"State data must be contiguous (nz, ny, 3, nphi, nx), got "
-                             f"{tuple(data.shape)}")
+        if tuple(data.shape) != device_shape(nz, ny, nphi, nx) or not data.is_contiguous():
+            raise ValueError(f"State data must be contiguous {device_shape(nz, ny, nphi, nx)} "
+                             f"(nz, ny, 3, nstrip, nphi, {STRIP}), got {tuple(data.shape)}")
         self.data = data
         self.names = VAR_NAMES
         self.nx, self.ny, self.nz, self.nphi = nx, ny, nz, nphi
@@ -99,16 +125,19 @@ class State:
     def interior_coeffs(self, name: str) -> np.ndarray:
         v = self.names.index(name)
         return np.ascontiguousarray(
-            self.data[:, :, v].detach().cpu().numpy().transpose(3, 1, 0, 2))
+            lon_major(self.data, self.nx)[:, :, v].detach().cpu().numpy().transpose(3, 1, 0, 2))
 
     def set_interior_coeffs(self, name: str, arr) -> None:
         v = self.names.index(name)
         a = np.broadcast_to(np.asarray(arr, dtype=np.float64), (self.nx, self.ny, self.nz, self.nphi))
-        self.data[:, :, v].copy_(torch.from_numpy(np.ascontiguousarray(a.transpose(2, 1, 3, 0))))
+        stack = np.zeros((3, self.nx, self.ny, self.nz, self.nphi))
+        stack[0] = a
+        dev = torch.from_numpy(_to_device_layout(stack)).to(self.data.device)
+        self.data[:, :, v].copy_(dev[:, :, 0])
 
     def to_numpy(self) -> np.ndarray:
         """(3, nx, ny, nz, nphi) host copy in the reference's interior layout."""
-        return _to_reference_layout(self.data)
+        return _to_reference_layout(self.data, self.nx)
 
     def copy(self) -> "State":
         return State(self.data.clone(), self.nx, self.ny, self.nz, self.nphi)
@@ -229,7 +258,7 @@ class SpatialOperator:
 
     @property
     def state_shape(self):
-        return (self.nz, self.mesh.ny, 3, self.nphi, self.mesh.nx)
+        return device_shape(self.nz, self.mesh.ny, self.nphi, self.mesh.nx)
 
     def zero_state(self) -> State:
         d = torch.zeros(self.state_shape, dtype=torch.float64, device=self.device)
@@ -259,7 +288,8 @@ class SpatialOperator:
     # -- device entry points ------------------------------------------------
 
     def _check(self, state: State):
-        if tuple(state.data.shape) != self.state_shape:
+        if tuple(state.data.shape) != self.state_shape or (state.nx, state.ny, state.nz, state.nphi) != \
+                (self.mesh.nx, self.mesh.ny, self.nz, self.nphi):
             raise ValueError(f"state shape {tuple(state.data.shape)} != operator {self.state_shape}")
 
     def raise_on_status(self, flags: int):
@@ -301,7 +331,8 @@ class SpatialOperator:
         key = state.data.data_ptr()
         ws = self._scratch.get(key)
         if ws is None:
-            ws = (torch.empty_like(state.data), torch.empty_like(state.data))
+            # zeroed once: the strip padding past nx is read but never written
+            ws = (torch.zeros_like(state.data), torch.zeros_like(state.data))
             self._scratch = {key: ws}
         c = self._ctx
         _lib.check(c.lib.dgswe_ssprk3(c.h, _ptr(state.data), _ptr(ws[0]), _ptr(ws[1]), float(dt),
@@ -319,7 +350,7 @@ class SpatialOperator:
         """(nx, ny, nz, nq) nodal values per variable."""
         if self._phi_dev is None:
             self._phi_dev = torch.from_numpy(self.vander.phi).to(self.device)
-        U = torch.einsum("qm,zjvmi->vijzq", self._phi_dev, state.data)
+        U = torch.einsum("qm,zjvmi->vijzq", self._phi_dev, lon_major(state.data, self.mesh.nx))
         return {n: U[v].cpu().numpy() for v, n in enumerate(VAR_NAMES)}
 
     def interior_theta(self):
@@ -329,7 +360,7 @@ class SpatialOperator:
         """max over interior nodes of max(|u|,|v|) + sqrt(g h) (models.py:282-285)."""
         if self._phi_dev is None:
             self._phi_dev = torch.from_numpy(self.vander.phi).to(self.device)
-        U = torch.einsum("qm,zjvmi->vzjqi", self._phi_dev, state.data)
+        U = torch.einsum("qm,zjvmi->vzjqi", self._phi_dev, lon_major(state.data, self.mesh.nx))
         h = U[0]
         hf = torch.clamp_min(h, self.model.h_floor)
         c = torch.sqrt(self.model.gravity * torch.clamp_min(h, 0.0))

@@ -240,7 +240,7 @@ def test_positivity_raises(P):
     setup = P.build_case(P.default_config("williamson_tc6").override(nx=12, ny=6, p=2))
     op = P.SpatialOperator(setup.mesh, 2, setup.model)
     st = op.project_state(setup.ic)
-    st.data[0, 3, 0, 0, 5] = -100.0
+    st.data[0, 3, 0, 0, 0, 5] = -100.0   # (z, row, var, strip, mode, lane)
     with pytest.raises(P.PositivityError):
         op.assemble_rhs(st)
     with pytest.raises(P.PositivityError):
@@ -270,7 +270,7 @@ def test_nonfinite_detected(P):
     setup = P.build_case(P.default_config("williamson_tc6").override(nx=12, ny=6, p=2))
     op = P.SpatialOperator(setup.mesh, 2, setup.model)
     st = op.project_state(setup.ic)
-    st.data[0, 2, 1, 3, 4] = float("inf")
+    st.data[0, 2, 1, 0, 3, 4] = float("inf")
     with pytest.raises((P.DivergenceError, P.PositivityError)):
         P.rk_step(st, op.assemble_rhs, 1.0, P.tableau(3))
 
