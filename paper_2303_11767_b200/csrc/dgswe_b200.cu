@@ -559,11 +559,11 @@ int64_t dgswe_launch_count(const dgswe_ctx *ctx) { return ctx ? ctx->launches : 
 
 #ifdef DG_TIMING
 // experiment builds only: per-role phase cycle sums since the last call
-int dgswe_debug_timing(unsigned long long *out24)
+int dgswe_debug_timing(unsigned long long *out28)
 {
     CUDA_TRY(cudaDeviceSynchronize());
-    CUDA_TRY(cudaMemcpyFromSymbol(out24, dgswe::g_timing, sizeof(unsigned long long) * 24));
-    static unsigned long long zero[24] = {};
+    CUDA_TRY(cudaMemcpyFromSymbol(out28, dgswe::g_timing, sizeof(unsigned long long) * 28));
+    static unsigned long long zero[28] = {};
     CUDA_TRY(cudaMemcpyToSymbol(dgswe::g_timing, zero, sizeof zero));
     return DGSWE_OK;
 }

@@ -101,8 +101,10 @@ __host__ __device__ inline int row_stride(int p) { return 3 * (p + 1) + 2 + (p +
 // DG_TIMING builds record per-role phase durations (clock cycles) of every
 // row: [role][A work, barrier-1 wait, B work, barrier-2 wait, C work, rows]
 #ifdef DG_TIMING
-__device__ unsigned long long g_timing[4][6];
-#define TSTAMP(k) unsigned tk##k = clock()
+__device__ unsigned long long g_timing[4][7];
+#define TSTAMP(k)                                                                  \
+    unsigned tk##k;                                                                \
+    asm volatile("mov.u32 %0, %%clock;" : "=r"(tk##k)::"memory")
 #define TACC(i, d) tacc[i] += (d)
 #else
 #define TSTAMP(k)
@@ -885,6 +887,9 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
     const int eL = (strip * kLanes - 1 + nx) % nx;
     const int eR = (strip * kLanes + nvalid) % nx;
     __syncthreads();                               // prologue barrier A
+#ifdef DG_TIMING
+    unsigned tacc[6] = {0, 0, 0, 0, 0, 0};
+#endif
 
     if (face_warp) {
         // Face warp.  Iteration `it` (from the pre-iteration jb-1): job 0 =
@@ -895,7 +900,9 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
         for (int it = jb - 1; it < je; ++it) {
             const int k = it - jb;
             const bool pre = it < jb;
+            TSTAMP(a);
             if (!pre) __syncthreads();                 // barrier 1 of row it
+            TSTAMP(b);
             const double *next_tile = ringS + ((k + 1) & 1) * SM::TILE;   // X(it+1)
             if (it + 1 <= last_fetch) {
                 double bt[3][N];
@@ -917,7 +924,9 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
                 const double *src = kp.rowtab + (size_t)(kp.row0 + it + 2) * RL::STRIDE;
                 for (int idx = lane; idx < RL::STRIDE; idx += kLanes) dst[idx] = src[idx];
             }
+            TSTAMP(c);
             __syncthreads();                           // barrier 2 of row it (prologue barrier B)
+            TSTAMP(d);
             if (!pre) {
                 double *t = fa;
                 fa = fb;
@@ -944,6 +953,13 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
                 face_flux_rt<P>(in, out, smem + SM::F0 + ((k + 1) & 1) * 3 * N, 1, 0, kp, 0, 0.0, 0.0,
                                 alpha_x, kp.bdy);
             }
+            TSTAMP(e);
+            if (!pre) {
+                TACC(2, tkb - tka);   // barrier 1 wait
+                TACC(3, tkc - tkb);   // y-face
+                TACC(4, tkd - tkc);   // barrier 2 wait
+                TACC(5, tke - tkd);   // border face (next row)
+            }
         }
     } else {
         __syncthreads();                           // prologue barrier B
@@ -955,6 +971,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
             const bool has_top = jg + 1 < kp.ny;
             const bool has_bot = jg > 0;
             const double *row = sRow + (k % 3) * RL::STRIDE;
+            TSTAMP(s);
 
             // warm L2 for this row's u^n and for row jl+2 (copied in after finalize)
             if (lane == 0) {
@@ -967,8 +984,11 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
                 bad |= owned & eval_row<P>(c, sU + v * NP * kLanes, sXL + v * N * kLanes,
                                            sXR + v * N * kLanes, sT + v * N * kLanes, lane, chk);
             }
+            TSTAMP(0);
             if (jl + 1 <= last_fetch) mbar_wait(mbar + (slot ^ 1) * 3 + v, ((k + 1) >> 1) & 1);   // X(jl+1)
+            TSTAMP(1);
             __syncthreads();                           // barrier 1
+            TSTAMP(2);
 
             if (v == 0) {
                 // the h warp has the lightest volume work: it takes the x-faces 1..32
@@ -983,7 +1003,9 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
             }
             double vol[N][N];
             volume<P>(vol, v, sU, row, lane, kp);
+            TSTAMP(3);
             __syncthreads();                           // barrier 2
+            TSTAMP(4);
             const size_t roff = (size_t)jl * kp.rstride;
             bad |= finalize<P, HAS_U>(vol, cur, HAS_U ? Uz + roff : nullptr, v, sFX,
                                       smem + SM::F0 + slot * 3 * N, sFa, sFb, has_top, has_bot, row, lane,
@@ -994,12 +1016,25 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
                 fence_proxy_async();
                 tma_row(cur, Xz + (size_t)(jl + 2) * kp.rstride, kTileBytes, mbar + slot * 3 + v);
             }
+            TSTAMP(5);
+            TACC(0, tk0 - tks);   // phase A work (eval)
+            TACC(1, tk1 - tk0);   // wait for X(jl+1)
+            TACC(2, tk2 - tk1);   // barrier 1
+            TACC(3, tk3 - tk2);   // phase B work
+            TACC(4, tk4 - tk3);   // barrier 2
+            TACC(5, tk5 - tk4);   // phase C work (finalize)
             double *tmp = sFa;
             sFa = sFb;
             sFb = tmp;
         }
     }
 
+#ifdef DG_TIMING
+    if (lane == 0) {
+        for (int q = 0; q < 6; ++q) atomicAdd(&g_timing[role][q], (unsigned long long)tacc[q]);
+        atomicAdd(&g_timing[role][6], (unsigned long long)(je - jb));
+    }
+#endif
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && lane == 0) {
         atomicOr(kp.status, bad);

@@ -24,19 +24,19 @@ def main():
     lib = _lib.load()
     fn = lib.dgswe_debug_timing
     fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
-    buf = (ctypes.c_ulonglong * 24)()
+    buf = (ctypes.c_ulonglong * 28)()
     op.ssprk3_steps(st, dt, 3)
     fn(buf)
     op.ssprk3_steps(st, dt, 20)
     torch.cuda.synchronize()
     fn(buf)
-    a = np.array(list(buf), dtype=np.float64).reshape(4, 6)
+    a = np.array(list(buf), dtype=np.float64).reshape(4, 7)
     names = ["h", "hu", "hv", "face"]
-    print("cycles per row:   A-work  wait1   B-work  wait2   C-work   total")
+    print("cycles/row  eval  ringwait  bar1  B-work  bar2  C-work  total   (face: -, -, bar1, yface, bar2, border)")
     for r in range(4):
-        rows = a[r, 5]
-        x = a[r, :5] / max(rows, 1)
-        print(f"{names[r]:5s} {x[0]:8.0f} {x[1]:7.0f} {x[2]:8.0f} {x[3]:7.0f} {x[4]:8.0f} {x.sum():8.0f}")
+        rows = a[r, 6]
+        x = a[r, :6] / max(rows, 1)
+        print(f"{names[r]:5s} " + " ".join(f"{y:7.0f}" for y in x) + f" {x.sum():8.0f}")
 
 
 if __name__ == "__main__":
