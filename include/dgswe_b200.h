@@ -19,9 +19,11 @@
  *                                  rk_step (timestep.py:149-167), fused
  *   dgswe_axpy                     timestep._axpy (timestep.py:132-141) and the
  *                                  finite check of rk_step (165-166)
- *   dgswe_ssprk3                   integrate's step loop (timestep.py:210-229)
- *                                  for tableau(3) (timestep.py:65-70), as
- *                                  Shu-Osher stages, CUDA-graph batched
+ *   dgswe_stage2                   an RK4 stage with the accumulator as a
+ *                                  second output (timestep.py:71-81, 163-164)
+ *   dgswe_rk_steps / dgswe_ssprk3  integrate's step loop (timestep.py:210-229)
+ *                                  for tableau(1..4) (timestep.py:57-82), as
+ *                                  fused stages, CUDA-graph batched
  *   dgswe_alpha_prepass            global Rusanov alpha (dg.py:389-411)
  *   dgswe_status                   PositivityError (models.py:143-146) and
  *                                  DivergenceError (timestep.py:165-166,
@@ -123,10 +125,27 @@ int dgswe_stage(dgswe_ctx *ctx, double a, const double *U, double b, const doubl
 int dgswe_stage_rows(dgswe_ctx *ctx, double a, const double *U, double b, const double *X,
                      double g, double *Y, int tag, int r0, int r1, void *stream);
 
+/* Y = a*U + b*X + g*RHS(X) and Y2 = A + g2*RHS(X) in one launch, on local
+ * rows [r0, r1): the stage of classical RK4 whose second output is the
+ * running accumulator u + sum_i dt b_i k_i (timestep.py:71-81, 163-164).
+ * Y2 may alias A; neither output may alias X. */
+int dgswe_stage2(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g,
+                 double *Y, const double *A, double g2, double *Y2, int tag, int r0, int r1,
+                 void *stream);
+
 /* y = y + x*coef on rows [jlo, jhi), two roundings (timestep.py:137-141);
  * check_finite != 0 raises DGSWE_STATUS_NONFINITE for non-finite results. */
 int dgswe_axpy(dgswe_ctx *ctx, double coef, const double *x, double *y, int check_finite,
                int tag, void *stream);
+
+/* nsteps of the explicit RK method of `order` 1..4 (tableau(order) of
+ * timestep.py:57-82, fused stage form: Euler, Heun/SSPRK2 and SSPRK3 in
+ * Shu-Osher form, classical RK4 with its accumulator as a second kernel
+ * output) on u in place, scratch w1 (all orders), w2 (order >= 3), w3
+ * (order 4); one CUDA graph per (order, buffers, dt, nsteps).  Status tags
+ * are the 0-based step index within the call.  Single-band contexts only. */
+int dgswe_rk_steps(dgswe_ctx *ctx, int order, double *u, double *w1, double *w2, double *w3, double dt,
+                   int nsteps, int check_mean, void *stream);
 
 /* nsteps of Shu-Osher SSPRK3 on u (in place) with scratch w1, w2, batched
  * into one CUDA graph per (buffers, dt, nsteps).  check_mean != 0 enables

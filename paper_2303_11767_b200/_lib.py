@@ -55,6 +55,8 @@ SIGNATURES = {
     "dgswe_stage_rows": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _I, _I, _VP]),
     "dgswe_axpy": (_I, [_VP, _D, _VP, _VP, _I, _I, _VP]),
     "dgswe_ssprk3": (_I, [_VP, _VP, _VP, _VP, _D, _I, _I, _VP]),
+    "dgswe_rk_steps": (_I, [_VP, _I, _VP, _VP, _VP, _VP, _D, _I, _I, _VP]),
+    "dgswe_stage2": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _VP, _D, _VP, _I, _I, _I, _VP]),
     "dgswe_alpha_prepass": (_I, [_VP, _VP, _VP]),
     "dgswe_alpha_buffer": (_VP, [_VP]),
     "dgswe_set_external_alpha": (_I, [_VP, _I]),

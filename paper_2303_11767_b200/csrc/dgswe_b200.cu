@@ -131,13 +131,14 @@ __global__ void axpy_kernel(const double *__restrict__ x, double *__restrict__ y
 }  // namespace
 
 struct GraphKey {
-    double *u, *w1, *w2;
+    int order;
+    double *u, *w1, *w2, *w3;
     double dt;
     int nsteps, check_mean;
     bool operator<(const GraphKey &o) const
     {
-        return std::tie(u, w1, w2, dt, nsteps, check_mean) <
-               std::tie(o.u, o.w1, o.w2, o.dt, o.nsteps, o.check_mean);
+        return std::tie(order, u, w1, w2, w3, dt, nsteps, check_mean) <
+               std::tie(o.order, o.u, o.w1, o.w2, o.w3, o.dt, o.nsteps, o.check_mean);
     }
 };
 
@@ -162,6 +163,21 @@ struct dgswe_ctx {
 
 namespace {
 
+template <int P, bool HU, bool HY>
+int setup_variant(int dev, size_t smem, int (&occ)[64][4])
+{
+    const int var = (HU ? 1 : 0) + (HY ? 2 : 0);
+    if (!occ[dev][var]) {
+        CUDA_TRY(cudaFuncSetAttribute(dgswe::stage_kernel<P, HU, HY>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int o = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, dgswe::stage_kernel<P, HU, HY>,
+                                                               dgswe::kThreads, smem));
+        occ[dev][var] = o > 0 ? o : 1;
+    }
+    return occ[dev][var];
+}
+
 template <int P>
 int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, cudaStream_t s)
 {
@@ -169,33 +185,26 @@ int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, c
     const int rows = r1 - r0;
     if (rows <= 0) return DGSWE_OK;
     const size_t smem = (size_t)SM::TOTAL * sizeof(double) + (size_t)c->smem_pad;
-    static int occ[64][2] = {};     // resident CTAs per SM, per device and variant
+    static int occ[64][4] = {};     // resident CTAs per SM, per device and variant
     static size_t occ_smem[64] = {};
-    if (occ_smem[c->device & 63] != smem) {
-        occ[c->device & 63][0] = occ[c->device & 63][1] = 0;
-        occ_smem[c->device & 63] = smem;
-    }
     const int dev = c->device & 63;
-    const int variant = kp.U ? 1 : 0;
-    if (!occ[dev][variant]) {
-        CUDA_TRY(cudaFuncSetAttribute(dgswe::stage_kernel<P, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CUDA_TRY(cudaFuncSetAttribute(dgswe::stage_kernel<P, false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int o1 = 0, o0 = 0;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, dgswe::stage_kernel<P, true>,
-                                                               dgswe::kThreads, smem));
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o0, dgswe::stage_kernel<P, false>,
-                                                               dgswe::kThreads, smem));
-        occ[dev][1] = o1 > 0 ? o1 : 1;
-        occ[dev][0] = o0 > 0 ? o0 : 1;
+    if (occ_smem[dev] != smem) {
+        for (int k = 0; k < 4; ++k) occ[dev][k] = 0;
+        occ_smem[dev] = smem;
     }
+    const bool hu = kp.U != nullptr, hy = kp.Y2 != nullptr;
+    int o;
+    if (hy)
+        o = hu ? setup_variant<P, true, true>(dev, smem, occ) : setup_variant<P, false, true>(dev, smem, occ);
+    else
+        o = hu ? setup_variant<P, true, false>(dev, smem, occ) : setup_variant<P, false, false>(dev, smem, occ);
+    if (o < 0) return o;
     // one wave: split every (strip, level) column of rows into as many
     // contiguous chunks as the resident CTA slots allow
     const int strips = c->nstrip;
     int rc = kp.rc;
     if (rc <= 0) {
-        const long long slots = (long long)c->sms * occ[dev][variant];
+        const long long slots = (long long)c->sms * o;
         long long chunks = slots / ((long long)strips * c->cfg.nz);
         if (chunks < 1) chunks = 1;
         rc = (int)((rows + chunks - 1) / chunks);
@@ -203,21 +212,30 @@ int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, c
     dgswe::StageParams kq = kp;
     kq.rc = rc;
     dim3 grid(strips, (rows + rc - 1) / rc, c->cfg.nz);
-    if (kq.U)
-        dgswe::stage_kernel<P, true><<<grid, dgswe::kThreads, smem, s>>>(kq);
-    else
-        dgswe::stage_kernel<P, false><<<grid, dgswe::kThreads, smem, s>>>(kq);
+    if (hy) {
+        if (hu)
+            dgswe::stage_kernel<P, true, true><<<grid, dgswe::kThreads, smem, s>>>(kq);
+        else
+            dgswe::stage_kernel<P, false, true><<<grid, dgswe::kThreads, smem, s>>>(kq);
+    } else {
+        if (hu)
+            dgswe::stage_kernel<P, true, false><<<grid, dgswe::kThreads, smem, s>>>(kq);
+        else
+            dgswe::stage_kernel<P, false, false><<<grid, dgswe::kThreads, smem, s>>>(kq);
+    }
     CUDA_TRY(cudaGetLastError());
     c->launches += 1;
     return DGSWE_OK;
 }
 
+// Y = a U + b X + g RHS(X) [, Y2 = A + g2 RHS(X)] on local rows [r0, r1)
 int launch_stage(dgswe_ctx *c, double a, const double *U, double b, const double *X, double g,
-                 double *Y, int tag, int r0, int r1, int check_finite, int check_mean,
-                 cudaStream_t s)
+                 double *Y, const double *A, double g2, double *Y2, int tag, int r0, int r1,
+                 int check_finite, int check_mean, cudaStream_t s)
 {
     if (!X || !Y) return fail(DGSWE_EINVAL, "null state pointer");
-    if (X == Y) return fail(DGSWE_EINVAL, "output must not alias the stage input");
+    if (X == Y || X == Y2) return fail(DGSWE_EINVAL, "outputs must not alias the stage input");
+    if (Y2 && (Y2 == Y || !A)) return fail(DGSWE_EINVAL, "second output needs its own buffer and an addend");
     if (a != 0.0 && !U) return fail(DGSWE_EINVAL, "U is required when a != 0");
     if (r0 < c->cfg.jlo || r1 > c->cfg.jhi || r0 > r1)
         return fail(DGSWE_EINVAL, "row range [%d,%d) outside [%d,%d)", r0, r1, c->cfg.jlo, c->cfg.jhi);
@@ -225,6 +243,9 @@ int launch_stage(dgswe_ctx *c, double a, const double *U, double b, const double
     kp.X = X;
     kp.U = (a != 0.0) ? U : nullptr;
     kp.Y = Y;
+    kp.A = Y2 ? A : nullptr;
+    kp.Y2 = Y2;
+    kp.g2 = g2;
     kp.zstride = c->zstride;
     kp.rstride = c->rstride;
     kp.vstride = c->vstride;
@@ -415,7 +436,8 @@ int64_t dgswe_state_elems(const dgswe_ctx *ctx)
 int dgswe_rhs(dgswe_ctx *ctx, const double *X, double *K, void *stream)
 {
     if (!ctx) return fail(DGSWE_EINVAL, "null context");
-    return launch_stage(ctx, 0.0, nullptr, 0.0, X, 1.0, K, 0, ctx->cfg.jlo, ctx->cfg.jhi, 0, 0,
+    return launch_stage(ctx, 0.0, nullptr, 0.0, X, 1.0, K, nullptr, 0.0, nullptr, 0, ctx->cfg.jlo,
+                        ctx->cfg.jhi, 0, 0,
                         (cudaStream_t)stream);
 }
 
@@ -423,7 +445,7 @@ int dgswe_stage(dgswe_ctx *ctx, double a, const double *U, double b, const doubl
                 double *Y, int tag, void *stream)
 {
     if (!ctx) return fail(DGSWE_EINVAL, "null context");
-    return launch_stage(ctx, a, U, b, X, g, Y, tag, ctx->cfg.jlo, ctx->cfg.jhi, 0, 0,
+    return launch_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, ctx->cfg.jlo, ctx->cfg.jhi, 0, 0,
                         (cudaStream_t)stream);
 }
 
@@ -431,7 +453,15 @@ int dgswe_stage_rows(dgswe_ctx *ctx, double a, const double *U, double b, const 
                      double *Y, int tag, int r0, int r1, void *stream)
 {
     if (!ctx) return fail(DGSWE_EINVAL, "null context");
-    return launch_stage(ctx, a, U, b, X, g, Y, tag, r0, r1, 0, 0, (cudaStream_t)stream);
+    return launch_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, r0, r1, 0, 0,
+                        (cudaStream_t)stream);
+}
+
+int dgswe_stage2(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g,
+                 double *Y, const double *A, double g2, double *Y2, int tag, int r0, int r1, void *stream)
+{
+    if (!ctx) return fail(DGSWE_EINVAL, "null context");
+    return launch_stage(ctx, a, U, b, X, g, Y, A, g2, Y2, tag, r0, r1, 0, 0, (cudaStream_t)stream);
 }
 
 int dgswe_axpy(dgswe_ctx *ctx, double coef, const double *x, double *y, int check_finite, int tag,
@@ -476,32 +506,77 @@ int dgswe_set_external_alpha(dgswe_ctx *ctx, int external)
     return DGSWE_OK;
 }
 
-static int enqueue_ssprk3(dgswe_ctx *ctx, double *u, double *w1, double *w2, double dt, int nsteps,
-                          int check_mean, cudaStream_t s)
+// K steps of the fused explicit RK method of `order` (the tableaux of
+// timestep.py:57-82, evaluated in stage form; every stage is one kernel):
+//   1: forward Euler, ping-pong u <-> w1 (a final copy when K is odd)
+//   2: Heun == SSPRK2 Shu-Osher: w1 = u + dt L(u); u = u/2 + (w1 + dt L(w1))/2
+//   3: SSPRK3 Shu-Osher (== tableau(3), timestep.py:65-70)
+//   4: classical RK4 (timestep.py:71-81) with the accumulator as the stage
+//      kernel's second output: acc = u + dt/6 k1 (+ dt/3 k2 + dt/3 k3),
+//      stage inputs u + dt/2 k1, u + dt/2 k2, u + dt k3, u = acc + dt/6 k4
+static int enqueue_rk(dgswe_ctx *ctx, int order, double *u, double *w1, double *w2, double *w3, double dt,
+                      int nsteps, int check_mean, cudaStream_t s)
 {
     const int lo = ctx->cfg.jlo, hi = ctx->cfg.jhi;
     for (int k = 0; k < nsteps; ++k) {
-        // Shu-Osher SSPRK3 == tableau(3) of timestep.py:65-70
-        int rc = launch_stage(ctx, 0.0, nullptr, 1.0, u, dt, w1, k, lo, hi, 0, 0, s);
-        if (!rc) rc = launch_stage(ctx, 0.75, u, 0.25, w1, 0.25 * dt, w2, k, lo, hi, 0, 0, s);
-        if (!rc) rc = launch_stage(ctx, 1.0 / 3.0, u, 2.0 / 3.0, w2, (2.0 / 3.0) * dt, u, k, lo, hi, 1,
-                                   check_mean, s);
+        int rc = DGSWE_OK;
+        switch (order) {
+        case 1: {
+            double *x = (k & 1) ? w1 : u, *y = (k & 1) ? u : w1;
+            rc = launch_stage(ctx, 0.0, nullptr, 1.0, x, dt, y, nullptr, 0.0, nullptr, k, lo, hi, 1, check_mean, s);
+            break;
+        }
+        case 2:
+            rc = launch_stage(ctx, 0.0, nullptr, 1.0, u, dt, w1, nullptr, 0.0, nullptr, k, lo, hi, 0, 0, s);
+            if (!rc)
+                rc = launch_stage(ctx, 0.5, u, 0.5, w1, 0.5 * dt, u, nullptr, 0.0, nullptr, k, lo, hi, 1,
+                                  check_mean, s);
+            break;
+        case 3:
+            rc = launch_stage(ctx, 0.0, nullptr, 1.0, u, dt, w1, nullptr, 0.0, nullptr, k, lo, hi, 0, 0, s);
+            if (!rc)
+                rc = launch_stage(ctx, 0.75, u, 0.25, w1, 0.25 * dt, w2, nullptr, 0.0, nullptr, k, lo, hi, 0, 0,
+                                  s);
+            if (!rc)
+                rc = launch_stage(ctx, 1.0 / 3.0, u, 2.0 / 3.0, w2, (2.0 / 3.0) * dt, u, nullptr, 0.0, nullptr,
+                                  k, lo, hi, 1, check_mean, s);
+            break;
+        case 4:
+            rc = launch_stage(ctx, 0.0, nullptr, 1.0, u, 0.5 * dt, w1, u, dt / 6.0, w3, k, lo, hi, 0, 0, s);
+            if (!rc)
+                rc = launch_stage(ctx, 1.0, u, 0.0, w1, 0.5 * dt, w2, w3, dt / 3.0, w3, k, lo, hi, 0, 0, s);
+            if (!rc)
+                rc = launch_stage(ctx, 1.0, u, 0.0, w2, dt, w1, w3, dt / 3.0, w3, k, lo, hi, 0, 0, s);
+            if (!rc)
+                rc = launch_stage(ctx, 1.0, w3, 0.0, w1, dt / 6.0, u, nullptr, 0.0, nullptr, k, lo, hi, 1,
+                                  check_mean, s);
+            break;
+        default:
+            return fail(DGSWE_EUNSUPPORTED, "RK order %d not supported (1..4)", order);
+        }
         if (rc) return rc;
     }
+    if (order == 1 && (nsteps & 1))
+        CUDA_TRY(cudaMemcpyAsync(u, w1, sizeof(double) * (size_t)ctx->zstride * ctx->cfg.nz,
+                                 cudaMemcpyDeviceToDevice, s));
     return DGSWE_OK;
 }
 
-int dgswe_ssprk3(dgswe_ctx *ctx, double *u, double *w1, double *w2, double dt, int nsteps,
-                 int check_mean, void *stream)
+static int stages_of(int order) { return order; }
+
+int dgswe_rk_steps(dgswe_ctx *ctx, int order, double *u, double *w1, double *w2, double *w3, double dt,
+                   int nsteps, int check_mean, void *stream)
 {
-    if (!ctx || !u || !w1 || !w2) return fail(DGSWE_EINVAL, "null argument");
+    if (!ctx || !u || !w1) return fail(DGSWE_EINVAL, "null argument");
+    if (order < 1 || order > 4) return fail(DGSWE_EUNSUPPORTED, "RK order %d not supported (1..4)", order);
+    if ((order >= 3 && !w2) || (order == 4 && !w3)) return fail(DGSWE_EINVAL, "missing scratch buffer");
     if (nsteps < 0) return fail(DGSWE_EINVAL, "nsteps must be >= 0");
     if (nsteps == 0) return DGSWE_OK;
     if (ctx->cfg.jlo != 0 || ctx->cfg.jhi != ctx->cfg.ny || ctx->cfg.row0 != 0)
-        return fail(DGSWE_EINVAL, "dgswe_ssprk3 needs a single-band context; use dgswe_stage per band");
+        return fail(DGSWE_EINVAL, "fused RK steps need a single-band context; use dgswe_stage per band");
     cudaStream_t s = (cudaStream_t)stream;
-    if (getenv("DGSWE_NO_GRAPH")) return enqueue_ssprk3(ctx, u, w1, w2, dt, nsteps, check_mean, s);
-    GraphKey key{u, w1, w2, dt, nsteps, check_mean};
+    if (getenv("DGSWE_NO_GRAPH")) return enqueue_rk(ctx, order, u, w1, w2, w3, dt, nsteps, check_mean, s);
+    GraphKey key{order, u, w1, w2, w3, dt, nsteps, check_mean};
     auto it = ctx->graphs.find(key);
     if (it == ctx->graphs.end()) {
         if (ctx->graphs.size() >= 8) {
@@ -516,7 +591,7 @@ int dgswe_ssprk3(dgswe_ctx *ctx, double *u, double *w1, double *w2, double dt, i
         }
         CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
         const long long before = ctx->launches;
-        int rc = enqueue_ssprk3(ctx, u, w1, w2, dt, nsteps, check_mean, cap);
+        int rc = enqueue_rk(ctx, order, u, w1, w2, w3, dt, nsteps, check_mean, cap);
         cudaGraph_t graph = nullptr;
         cudaError_t e = cudaStreamEndCapture(cap, &graph);
         ctx->launches = before;   // counted at replay
@@ -534,8 +609,14 @@ int dgswe_ssprk3(dgswe_ctx *ctx, double *u, double *w1, double *w2, double dt, i
     }
     CUDA_TRY(cudaGraphLaunch(it->second, s));
     const int per_stage = 1 + (ctx->cfg.alpha_mode == DGSWE_ALPHA_GLOBAL ? 1 : 0);
-    ctx->launches += 3LL * nsteps * per_stage;
+    ctx->launches += (long long)stages_of(order) * nsteps * per_stage;
     return DGSWE_OK;
+}
+
+int dgswe_ssprk3(dgswe_ctx *ctx, double *u, double *w1, double *w2, double dt, int nsteps,
+                 int check_mean, void *stream)
+{
+    return dgswe_rk_steps(ctx, 3, u, w1, w2, nullptr, dt, nsteps, check_mean, stream);
 }
 
 int dgswe_status(dgswe_ctx *ctx, uint32_t *flags, int32_t *first_tag, int reset, void *stream)

@@ -49,6 +49,9 @@ struct StageParams {
     const double *X;      // stage input (level 0, buffer row 0)
     const double *U;      // u^n for the combination (may be null when a == 0)
     double *Y;            // output
+    const double *A;      // second output's addend (HAS_Y2 kernels; may alias Y2)
+    double *Y2;           // second output Y2 = A + g2 RHS(X) (classical RK4's accumulator)
+    double g2;
     long long zstride;    // doubles per level
     long long rstride;    // doubles per buffer row (3 * vstride)
     long long vstride;    // doubles per variable row (nstrip * nphi * 32)
@@ -662,9 +665,10 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
 // memory at a time) so that vol, c and u^n are the only tiles held.
 // Uv / Yv point at this lane's element of the variable's strip block
 // (mode stride 32 doubles: immediate offsets).
-template <int P, bool HAS_U>
+template <int P, bool HAS_U, bool HAS_Y2>
 __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const double *cur,
-                                             const double *Uv, int v, const double *sFX, const double *sF0,
+                                             const double *Uv, const double *Av, double *Y2v, int v,
+                                             const double *sFX, const double *sF0,
                                              const double *sFtop, const double *sFbot, bool has_top,
                                              bool has_bot, const double *row, int lane, bool owned,
                                              double *Yv, const StageParams &kp)
@@ -677,6 +681,13 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
         for (int a = 0; a < N; ++a)
 #pragma unroll
             for (int b = 0; b < N; ++b) un[a][b] = Uv[(a * N + b) * kLanes];
+    }
+    double an[HAS_Y2 ? N : 1][HAS_Y2 ? N : 1];
+    if constexpr (HAS_Y2) {            // second output's addend (may alias Y2)
+#pragma unroll
+        for (int a = 0; a < N; ++a)
+#pragma unroll
+            for (int b = 0; b < N; ++b) an[a][b] = Av[(a * N + b) * kLanes];
     }
     constexpr int LDX = kLanes + 1;    // x-face columns: face f is the left face of lane f
     const int o = (v * N) * kLanes, ox = (v * N) * LDX;
@@ -713,6 +724,10 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
             if (HAS_U) y = fma(kp.a, un[a][b], y);
             if (owned) Yv[(a * N + b) * kLanes] = y;
             fexp = max(fexp, __double2hiint(y) & 0x7ff00000);
+            if constexpr (HAS_Y2) {
+                const double y2 = fma(kp.g2 * (double)(2 * a + 1), k, an[a][b]);
+                if (owned) Y2v[(a * N + b) * kLanes] = y2;
+            }
             if (a == 0 && b == 0) mean = y;
         }
     }
@@ -789,7 +804,7 @@ __device__ __forceinline__ void bottom_traces(const double *ring_row, int lane, 
     }
 }
 
-template <int P, bool HAS_U>
+template <int P, bool HAS_U, bool HAS_Y2>
 __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel(StageParams kp)
 {
     constexpr int N = P + 1;
@@ -831,8 +846,11 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
     const double *Uz = kp.U ? kp.U + (size_t)blockIdx.z * kp.zstride + (size_t)strip * NP * kLanes +
                                   (size_t)v * kp.vstride + lane
                             : nullptr;
-    double *Yz = kp.Y + (size_t)blockIdx.z * kp.zstride + (size_t)strip * NP * kLanes +
-                 (size_t)v * kp.vstride + lane;
+    const size_t lane_off = (size_t)blockIdx.z * kp.zstride + (size_t)strip * NP * kLanes +
+                            (size_t)v * kp.vstride + lane;
+    double *Yz = kp.Y + lane_off;
+    const double *Az = HAS_Y2 ? kp.A + lane_off : nullptr;
+    double *Y2z = HAS_Y2 ? kp.Y2 + lane_off : nullptr;
     const bool chk = (v == 0) && !face_warp;
     unsigned bad = 0;
 
@@ -1007,7 +1025,8 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
             __syncthreads();                           // barrier 2
             TSTAMP(4);
             const size_t roff = (size_t)jl * kp.rstride;
-            bad |= finalize<P, HAS_U>(vol, cur, HAS_U ? Uz + roff : nullptr, v, sFX,
+            bad |= finalize<P, HAS_U, HAS_Y2>(vol, cur, HAS_U ? Uz + roff : nullptr,
+                                              HAS_Y2 ? Az + roff : nullptr, HAS_Y2 ? Y2z + roff : nullptr, v, sFX,
                                       smem + SM::F0 + slot * 3 * N, sFa, sFb, has_top, has_bot, row, lane,
                                       owned, Yz + roff, kp);
             // X(jl) is consumed: stream row jl+2 into its slot (L2-warm by now)

@@ -325,18 +325,34 @@ class SpatialOperator:
         _lib.check(c.lib.dgswe_axpy(c.h, float(coef), _ptr(x.data), _ptr(y.data),
                                     int(check_finite), int(tag), c.stream()), "dgswe_axpy")
 
-    def ssprk3_steps(self, state: State, dt: float, nsteps: int, check_mean: bool = False):
-        """nsteps fused Shu-Osher SSPRK3 steps in place (one CUDA graph)."""
+    def rk_steps(self, state: State, dt: float, nsteps: int, order: int = 3, check_mean: bool = False):
+        """nsteps fused steps of tableau(order) (1..4) in place, one CUDA graph:
+        Euler, Heun / SSPRK3 in Shu-Osher form, classical RK4 with the
+        accumulator as the stage kernel's second output."""
         self._check(state)
         key = state.data.data_ptr()
         ws = self._scratch.get(key)
         if ws is None:
             # zeroed once: the strip padding past nx is read but never written
-            ws = (torch.zeros_like(state.data), torch.zeros_like(state.data))
+            ws = tuple(torch.zeros_like(state.data) for _ in range(3))
             self._scratch = {key: ws}
         c = self._ctx
-        _lib.check(c.lib.dgswe_ssprk3(c.h, _ptr(state.data), _ptr(ws[0]), _ptr(ws[1]), float(dt),
-                                      int(nsteps), int(check_mean), c.stream()), "dgswe_ssprk3")
+        _lib.check(c.lib.dgswe_rk_steps(c.h, int(order), _ptr(state.data), _ptr(ws[0]), _ptr(ws[1]),
+                                        _ptr(ws[2]), float(dt), int(nsteps), int(check_mean), c.stream()),
+                   "dgswe_rk_steps")
+
+    def ssprk3_steps(self, state: State, dt: float, nsteps: int, check_mean: bool = False):
+        """nsteps fused Shu-Osher SSPRK3 steps in place (one CUDA graph)."""
+        self.rk_steps(state, dt, nsteps, 3, check_mean)
+
+    def stage2(self, a: float, U: State | None, b: float, X: State, g: float, Y: State, A: State,
+               g2: float, Y2: State, tag: int = 0):
+        """Y = a U + b X + g RHS(X) and Y2 = A + g2 RHS(X) in one launch (no sync)."""
+        c = self._ctx
+        _lib.check(c.lib.dgswe_stage2(c.h, float(a), _ptr(U.data if U is not None else None), float(b),
+                                      _ptr(X.data), float(g), _ptr(Y.data), _ptr(A.data), float(g2),
+                                      _ptr(Y2.data), int(tag), 0, self.mesh.ny, c.stream()),
+                   "dgswe_stage2")
 
     def status(self, reset: bool = True):
         return self._ctx.status(reset)

@@ -7,13 +7,15 @@ Same API as /root/reference/pkg/src/dgswe/timestep.py (``ButcherTableau``,
 * ``rk_step`` -- Butcher form for any tableau: per stage a device copy,
   fused axpy launches (two roundings, like ``_axpy`` timestep.py:132-141)
   and one fused RHS launch; one status read per step.
-* ``integrate`` with ``tableau(3)`` -- the SSPRK3 tableau of
-  timestep.py:65-70 evaluated in Shu-Osher form: three fused stage launches
-  per step (RHS + stage combination in one kernel, 21.3 B/DOF of HBM
-  traffic), batched into CUDA graphs; status (positivity / non-finite /
-  cell-mean) is read once per batch and mapped back to the failing step.
-  Shu-Osher and Butcher SSPRK3 are the same method; they differ only in
-  rounding (~1e-15 relative after 100 steps).
+* ``integrate`` with ``tableau(1..4)`` -- the tableaux of timestep.py:57-82
+  evaluated as fused stages (RHS + stage combination in one kernel):
+  Euler; Heun and SSPRK3 in Shu-Osher form (SSPRK3: three launches per step,
+  21.3 B/DOF of HBM traffic); classical RK4 with its accumulator as the
+  stage kernel's second output.  Steps are batched into CUDA graphs; status
+  (positivity / non-finite / cell-mean) is read once per batch and mapped
+  back to the failing step.  Stage and Butcher forms are the same methods;
+  they differ only in rounding (~1e-15 relative after 100 steps, SURVEY.md
+  section 8a10).
 """
 
 from __future__ import annotations
@@ -130,8 +132,12 @@ def _device_operator(rhs_fn):
     return None
 
 
-def _is_rk3(tab: ButcherTableau) -> bool:
-    return tab == _TABLES[3]
+def _fused_order(tab: ButcherTableau):
+    """The order k if ``tab`` is tableau(k) (fused stage form exists), else None."""
+    for k, t in _TABLES.items():
+        if tab == t:
+            return k
+    return None
 
 
 def rk_step(state, rhs_fn, dt: float, tab: ButcherTableau, workspace: _RKWorkspace | None = None):
@@ -199,8 +205,8 @@ def integrate(state, operator, controls: TimeControls, tab: ButcherTableau, call
               check_positivity=None, batch: int = 64, fused: bool = True):
     """Advance ``state`` to t_final (timestep.py:180-233).
 
-    With our SpatialOperator and ``tableau(3)`` the steps run as fused
-    SSPRK3 CUDA-graph batches of up to ``batch`` steps between callback
+    With our SpatialOperator and ``tableau(1..4)`` the steps run as fused
+    CUDA-graph batches of up to ``batch`` steps between callback
     cadences; errors are detected per batch and reported with the exact
     failing step and time, as the reference does per step.
     """
@@ -219,7 +225,8 @@ def integrate(state, operator, controls: TimeControls, tab: ButcherTableau, call
     steps = _step_sizes(t_final, dt)
     n_steps = len(steps)
     from .operator import SpatialOperator
-    use_fused = (fused and isinstance(operator, SpatialOperator) and _is_rk3(tab)
+    order = _fused_order(tab)
+    use_fused = (fused and isinstance(operator, SpatialOperator) and order is not None
                  and check_positivity in (None, "h"))
     started = time.perf_counter()
     if not use_fused:
@@ -253,7 +260,7 @@ def integrate(state, operator, controls: TimeControls, tab: ButcherTableau, call
             if any((step + k) % c == 0 for c in cadences):
                 break
             k += 1
-        operator.ssprk3_steps(state, h, k, check_mean=check_positivity == "h")
+        operator.rk_steps(state, h, k, order, check_mean=check_positivity == "h")
         flags, tag = operator.status(reset=True)
         if flags:
             bad = step + tag + 1

@@ -122,6 +122,52 @@ def test_fused_ssprk3_parity(P, golden, oracle_mod, name):
         assert abs((mg - m0) - (m1 - m0)) <= 1e-13 * abs(m0)
 
 
+# Euler and Heun are unstable for DG advection at the RK3 cases' dt (their
+# stability regions miss the imaginary axis), so they run on their own
+# golden cases only; classical RK4 also on the RK3 cases.
+FUSED_RK = [("tc6_rk1", None), ("tc6_rk2", None), ("tc6_rk4", None)] + \
+    [(c, 4) for c in ("tc6_40x20_p3", "tc2_c1", "tc6_nx2", "tc6_nz2", "tc6_p4", "tc2_p3_odd",
+                      "tc6_global", "tc6_wide")]
+
+
+@pytest.mark.parametrize("name,order", FUSED_RK)
+def test_fused_rk_parity(P, golden, oracle_mod, name, order):
+    """Fused stage forms of tableau(1), (2), (4) (Euler; Heun in Shu-Osher
+    form; classical RK4 with the accumulator as a second kernel output)
+    against the oracle's Butcher-form steps (timestep.py:149-167)."""
+    meta, g = golden
+    e = meta["cases"][name]
+    order = order or e["rk"]
+    t, orc, X = oracle_case(oracle_mod, e)
+    U, status, _ = orc.rk_steps(X, e["dt"], order, e["nsteps"])
+    assert status == 0
+    op = make_op(P, e)
+    st = op.state_from_array(X)
+    op.rk_steps(st, e["dt"], e["nsteps"], order)
+    flags, _ = op.status()
+    assert flags == 0
+    assert_state_close(st.to_numpy(), U, e["case"])
+    if order == e["rk"] and f"{name}/final" in g:      # the reference's own output
+        assert_state_close(st.to_numpy(), g[f"{name}/final"], e["case"])
+
+
+def test_fused_rk4_integrate_odd_batches(P, oracle_mod):
+    """integrate() with tableau(4) through the fused path, batches split by
+    callbacks, equals the oracle's Butcher RK4; Euler with an odd step count
+    (ping-pong buffers + final copy) too."""
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=24, ny=12, p=3))
+    op = P.SpatialOperator(setup.mesh, 3, setup.model)
+    t, orc, X = oracle_mod.build_case("williamson_tc6", 24, 12, 3)
+    for order, n, dt in ((4, 11, 8.0), (1, 7, 1.0), (2, 5, 2.0)):
+        st = op.state_from_array(X)
+        seen = []
+        P.integrate(st, op, P.TimeControls(n * dt, dt=dt), P.tableau(order),
+                    callbacks=[(4, lambda s, tt, x: seen.append(s))])
+        U, _, _ = orc.rk_steps(X, dt, order, n)
+        assert_state_close(st.to_numpy(), U, "williamson_tc6")
+        assert seen[-1] == n
+
+
 def test_integrate_c1_against_reference(P, golden):
     """Config C1 end to end through the public API (project -> integrate)
     against the reference's own 100-step output."""
