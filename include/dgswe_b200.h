@@ -166,6 +166,29 @@ int dgswe_set_external_alpha(dgswe_ctx *ctx, int external);
  * first_tag receives the smallest tag that raised a flag (INT32_MAX if none). */
 int dgswe_status(dgswe_ctx *ctx, uint32_t *flags, int32_t *first_tag, int reset, void *stream);
 
+/* ---- device diagnostics (single-band contexts; synchronise `stream`) ----
+ * dgswe_mass: *out = sum over elements of sum_m m0_rows[j][m] c_m of variable
+ *   `var`, level `level` (diagnostics.mass_integral, diagnostics.py:92-107);
+ *   m0_rows is the host (ny, nphi) array of row 0 of each row's mass matrix.
+ * dgswe_l2_sums: out2[0] = sum over elements and the nq2 nodes of a finer
+ *   rule of wrow[j][q] (u_q - ref_q)^2, out2[1] = sum of wrow[j][q] ref_q^2,
+ *   with u_q = sum_m phi2[q][m] c_m (diagnostics.l2_error, diagnostics.py:
+ *   42-80, before the determ factor and sqrt); phi2 (nq2, nphi) and wrow
+ *   (ny, nq2) are host arrays, ref is a DEVICE array [ny][nx][nq2].
+ * Both reduce in a fixed order in double-double: deterministic run to run. */
+int dgswe_mass(dgswe_ctx *ctx, const double *X, int var, int level, const double *m0_rows, double *out,
+               void *stream);
+int dgswe_l2_sums(dgswe_ctx *ctx, const double *X, int var, int level, const double *phi2, int nq2,
+                  const double *wrow, const double *ref, double *out2, void *stream);
+
+/* Initial-condition projection (basis.project_initial, basis.py:206-233):
+ * fvals is a DEVICE array [3][ny][nx][(p+1)^2] of nodal values at the Gauss
+ * nodes (q = qi*(p+1) + qj, qi along lambda), cos_nodes the host (ny, p+1)
+ * cos(theta) of the node latitudes, determ = dx*dy/4; writes every level of
+ * the state Y (cos-weighted moments, then the row's inverse mass). */
+int dgswe_project(dgswe_ctx *ctx, const double *fvals, const double *cos_nodes, double determ, double *Y,
+                  void *stream);
+
 /* Kernel launches issued by this context since creation (instrumentation). */
 int64_t dgswe_launch_count(const dgswe_ctx *ctx);
 

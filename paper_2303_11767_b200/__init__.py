@@ -18,7 +18,8 @@ from .geometry import (BOTTOM, EARTH, LEFT, RIGHT, TOP, Mesh, MassMatrix, Neighb
                        mass_matrix_sphere, min_effective_diameter, project_initial,
                        sphere_row_mass_matrices)
 from .physics import PositivityError, SphereSWEModel, X_DIR, Y_DIR, swe_sphere_model  # noqa: F401
-from .monitors import convergence_rate, l2_error, mass_integral  # noqa: F401
+from .monitors import (convergence_rate, l2_error, l2_error_host, mass_integral,  # noqa: F401
+                       mass_integral_host)
 from .stepping import (ButcherTableau, DivergenceError, StepLog, TimeControls,  # noqa: F401
                        integrate, rk_step, tableau)
 from .williamson import (CASE_IDS, CaseConfig, RunSetup, build_case, default_config,  # noqa: F401

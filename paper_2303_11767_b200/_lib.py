@@ -56,6 +56,9 @@ SIGNATURES = {
     "dgswe_axpy": (_I, [_VP, _D, _VP, _VP, _I, _I, _VP]),
     "dgswe_ssprk3": (_I, [_VP, _VP, _VP, _VP, _D, _I, _I, _VP]),
     "dgswe_rk_steps": (_I, [_VP, _I, _VP, _VP, _VP, _VP, _D, _I, _I, _VP]),
+    "dgswe_mass": (_I, [_VP, _VP, _I, _I, _PD, _PD, _VP]),
+    "dgswe_l2_sums": (_I, [_VP, _VP, _I, _I, _PD, _I, _PD, _VP, _PD, _VP]),
+    "dgswe_project": (_I, [_VP, _VP, _PD, _D, _VP, _VP]),
     "dgswe_stage2": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _VP, _D, _VP, _I, _I, _I, _VP]),
     "dgswe_alpha_prepass": (_I, [_VP, _VP, _VP]),
     "dgswe_alpha_buffer": (_VP, [_VP]),

@@ -21,6 +21,7 @@
 
 #include "../../include/dgswe_b200.h"
 #include "dgswe_kernels.cuh"
+#include "dgswe_diag.cuh"
 
 namespace {
 
@@ -157,6 +158,8 @@ struct dgswe_ctx {
     int sms = 148;
     int smem_pad = 0;             // experiment knob: extra dynamic smem per CTA
     std::map<GraphKey, cudaGraphExec_t> graphs;
+    double *diag = nullptr;       // device scratch for diagnostics (row partials + tables)
+    size_t diag_bytes = 0;
     // derived scalars
     double inv_r, inv_r_cx, half_g, bdx, bdy;
 };
@@ -425,6 +428,7 @@ void dgswe_destroy(dgswe_ctx *ctx)
     cudaFree(ctx->cos_edge);
     cudaFree(ctx->alpha);
     cudaFree(ctx->status);
+    cudaFree(ctx->diag);
     delete ctx;
 }
 
@@ -637,6 +641,122 @@ int dgswe_status(dgswe_ctx *ctx, uint32_t *flags, int32_t *first_tag, int reset,
 }
 
 int64_t dgswe_launch_count(const dgswe_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+// ---- device diagnostics and IC projection (dgswe_diag.cuh) ----
+
+static int diag_scratch(dgswe_ctx *c, size_t doubles)
+{
+    if (c->diag_bytes < doubles * sizeof(double)) {
+        cudaFree(c->diag);
+        c->diag = nullptr;
+        c->diag_bytes = 0;
+        CUDA_TRY(cudaMalloc(&c->diag, doubles * sizeof(double)));
+        c->diag_bytes = doubles * sizeof(double);
+    }
+    return DGSWE_OK;
+}
+
+static dgswe::DiagLayout diag_layout(const dgswe_ctx *c)
+{
+    return {c->zstride, c->rstride, c->vstride, c->cfg.nx, c->cfg.ny, c->nphi};
+}
+
+static int check_diag(const dgswe_ctx *c, const double *X, int var, int level)
+{
+    if (!c || !X) return fail(DGSWE_EINVAL, "null argument");
+    if (var < 0 || var > 2 || level < 0 || level >= c->cfg.nz) return fail(DGSWE_EINVAL, "bad var/level");
+    if (c->cfg.row0 != 0 || c->cfg.nrows != c->cfg.ny)
+        return fail(DGSWE_EINVAL, "diagnostics need a single-band context");
+    return DGSWE_OK;
+}
+
+int dgswe_mass(dgswe_ctx *ctx, const double *X, int var, int level, const double *m0_rows, double *out,
+               void *stream)
+{
+    int rc = check_diag(ctx, X, var, level);
+    if (rc) return rc;
+    if (!m0_rows || !out) return fail(DGSWE_EINVAL, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int ny = ctx->cfg.ny, nphi = ctx->nphi;
+    rc = diag_scratch(ctx, (size_t)ny * nphi + 2 * (size_t)ny + 2);
+    if (rc) return rc;
+    double *tab = ctx->diag, *part = tab + (size_t)ny * nphi, *res = part + 2 * (size_t)ny;
+    CUDA_TRY(cudaMemcpyAsync(tab, m0_rows, sizeof(double) * ny * nphi, cudaMemcpyHostToDevice, s));
+    const dgswe::DiagLayout L = diag_layout(ctx);
+    dgswe::mass_rows_kernel<<<dim3(ny, 1), 256, 0, s>>>(X + (size_t)level * ctx->zstride, L, var, tab, part);
+    dgswe::rows_total_kernel<1><<<1, 256, 0, s>>>(part, ny, 0, res);
+    CUDA_TRY(cudaGetLastError());
+    ctx->launches += 2;
+    CUDA_TRY(cudaMemcpyAsync(out, res, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return DGSWE_OK;
+}
+
+int dgswe_l2_sums(dgswe_ctx *ctx, const double *X, int var, int level, const double *phi2, int nq2,
+                  const double *wrow, const double *ref, double *out2, void *stream)
+{
+    int rc = check_diag(ctx, X, var, level);
+    if (rc) return rc;
+    if (!phi2 || !wrow || !ref || !out2 || nq2 < 1) return fail(DGSWE_EINVAL, "bad argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int ny = ctx->cfg.ny, nphi = ctx->nphi;
+    const size_t nt = (size_t)nq2 * nphi + (size_t)ny * nq2;
+    rc = diag_scratch(ctx, nt + 4 * (size_t)ny + 2);
+    if (rc) return rc;
+    double *dphi = ctx->diag, *dw = dphi + (size_t)nq2 * nphi, *part = ctx->diag + nt, *res = part + 4 * (size_t)ny;
+    CUDA_TRY(cudaMemcpyAsync(dphi, phi2, sizeof(double) * nq2 * nphi, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(dw, wrow, sizeof(double) * ny * nq2, cudaMemcpyHostToDevice, s));
+    const dgswe::DiagLayout L = diag_layout(ctx);
+    dgswe::l2_rows_kernel<<<dim3(ny, 1), 256, 0, s>>>(X + (size_t)level * ctx->zstride, L, var, dphi, nq2, dw,
+                                                       ref, part);
+    dgswe::rows_total_kernel<2><<<1, 256, 0, s>>>(part, ny, 0, res);
+    CUDA_TRY(cudaGetLastError());
+    ctx->launches += 2;
+    CUDA_TRY(cudaMemcpyAsync(out2, res, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return DGSWE_OK;
+}
+
+}  // extern "C"
+
+template <int P>
+static void launch_project(dgswe_ctx *c, const double *f, const double *cosn, double determ, double *Y,
+                           cudaStream_t s)
+{
+    dim3 grid((c->cfg.nx + 127) / 128, c->cfg.ny, 3);
+    const int rs = dgswe::row_stride(P);
+    dgswe::project_kernel<P><<<grid, 128, 0, s>>>(f, cosn, c->rowtab, rs, dgswe::RowLayout<P>::T,
+                                                  diag_layout(c), c->cfg.nz, determ, Y);
+}
+
+extern "C" {
+
+int dgswe_project(dgswe_ctx *ctx, const double *fvals, const double *cos_nodes, double determ, double *Y,
+                  void *stream)
+{
+    if (!ctx || !fvals || !cos_nodes || !Y) return fail(DGSWE_EINVAL, "null argument");
+    if (ctx->cfg.row0 != 0 || ctx->cfg.nrows != ctx->cfg.ny)
+        return fail(DGSWE_EINVAL, "projection needs a single-band context");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int ny = ctx->cfg.ny, n = ctx->n;
+    int rc = diag_scratch(ctx, (size_t)ny * n);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(ctx->diag, cos_nodes, sizeof(double) * ny * n, cudaMemcpyHostToDevice, s));
+    switch (ctx->cfg.p) {
+    case 0: launch_project<0>(ctx, fvals, ctx->diag, determ, Y, s); break;
+    case 1: launch_project<1>(ctx, fvals, ctx->diag, determ, Y, s); break;
+    case 2: launch_project<2>(ctx, fvals, ctx->diag, determ, Y, s); break;
+    case 3: launch_project<3>(ctx, fvals, ctx->diag, determ, Y, s); break;
+    case 4: launch_project<4>(ctx, fvals, ctx->diag, determ, Y, s); break;
+    case 5: launch_project<5>(ctx, fvals, ctx->diag, determ, Y, s); break;
+    case 6: launch_project<6>(ctx, fvals, ctx->diag, determ, Y, s); break;
+    default: return fail(DGSWE_EUNSUPPORTED, "degree not supported");
+    }
+    CUDA_TRY(cudaGetLastError());
+    ctx->launches += 1;
+    CUDA_TRY(cudaStreamSynchronize(s));   // the host staging buffers may be reused by the caller
+    return DGSWE_OK;
+}
 
 #ifdef DG_TIMING
 // experiment builds only: per-role phase cycle sums since the last call

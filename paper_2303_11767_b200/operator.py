@@ -281,9 +281,30 @@ class SpatialOperator:
         """Adopt a reference ``dgswe.dg.State`` (interior coefficients)."""
         return self.state_from_array(np.stack([ref_state.interior_coeffs(n) for n in VAR_NAMES]))
 
-    def project_state(self, ic_funcs: dict) -> State:
-        return self.state_from_coeffs({name: project_initial(f, self.mesh, self.vander)
-                                       for name, f in ic_funcs.items()})
+    def project_state(self, ic_funcs: dict, device: bool = False) -> State:
+        """cos-weighted L2 projection of the initial condition (basis.py:206-233).
+
+        ``device=False`` (default): numpy on the host in the reference's
+        operation order (bitwise equal to the reference).  ``device=True``:
+        the functions are evaluated on the GPU (torch-capable callables, else
+        numpy and upload) and projected by ``dgswe_project`` -- for grids
+        where host setup is slow; equal to the host result to rounding."""
+        if not device:
+            return self.state_from_coeffs({name: project_initial(f, self.mesh, self.vander)
+                                           for name, f in ic_funcs.items()})
+        from .geometry import element_node_coords
+        from .monitors import reference_nodal
+        lam, th = element_node_coords(self.mesh, self.quad.nodes)
+        zero = lambda lam_, th_: 0.0 * lam_ + 0.0 * th_     # noqa: E731
+        f = torch.stack([reference_nodal(ic_funcs.get(name, zero), lam, th, self.device)
+                         for name in VAR_NAMES])               # (3, ny, nx, n*n)
+        out = self.zero_state()
+        cosn = np.ascontiguousarray(np.cos(th), dtype=np.float64)
+        c = self._ctx
+        _lib.check(c.lib.dgswe_project(c.h, _ptr(f), cosn.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                       float(self.mesh.determ), _ptr(out.data), c.stream()),
+                   "dgswe_project")
+        return out
 
     # -- device entry points ------------------------------------------------
 

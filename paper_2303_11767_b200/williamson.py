@@ -26,6 +26,23 @@ TC6_K = 7.848e-6
 TC6_H0 = 8.0e3
 TC6_R = 4
 
+def _xp(*arrays):
+    """numpy, or torch when the coordinates are torch tensors (the device
+    initial-condition projection evaluates these functions on the GPU)."""
+    for a in arrays:
+        if type(a).__module__.startswith("torch"):
+            import torch
+            return torch
+    return np
+
+
+def _zeros(lam, th):
+    xp = _xp(lam, th)
+    if xp is np:
+        return np.zeros(np.broadcast(lam, th).shape)
+    return xp.zeros(xp.broadcast_shapes(lam.shape, th.shape), dtype=xp.float64, device=lam.device)
+
+
 CASE_IDS = ("advection_sine", "geostrophic_adjustment", "williamson_tc2", "williamson_tc6")
 SPHERE_CASES = ("williamson_tc2", "williamson_tc6")
 
@@ -70,11 +87,11 @@ def ic_williamson_tc2(constants: PhysicalConstants = EARTH):
     k = constants.radius * constants.omega * u0 + 0.5 * u0 * u0
 
     def height(lam, th):
-        return (TC2_GH0 - k * np.sin(th) ** 2) / g + 0.0 * lam
+        return (TC2_GH0 - k * _xp(th).sin(th) ** 2) / g + 0.0 * lam
 
     return ({"h": height,
-             "hu": lambda lam, th: height(lam, th) * u0 * np.cos(th),
-             "hv": lambda lam, th: np.zeros(np.broadcast(lam, th).shape)},
+             "hu": lambda lam, th: height(lam, th) * u0 * _xp(th).cos(th),
+             "hv": _zeros},
             height)
 
 
@@ -84,19 +101,21 @@ def tc6_fields(constants: PhysicalConstants = EARTH):
     w, K, R = TC6_OMEGA, TC6_K, TC6_R
 
     def winds(lam, th):
-        c = np.cos(th)
-        u = a * w * c + a * K * c ** (R - 1) * (R * np.sin(th) ** 2 - c**2) * np.cos(R * lam)
-        v = -a * K * R * c ** (R - 1) * np.sin(th) * np.sin(R * lam)
+        xp = _xp(lam, th)
+        c = xp.cos(th)
+        u = a * w * c + a * K * c ** (R - 1) * (R * xp.sin(th) ** 2 - c**2) * xp.cos(R * lam)
+        v = -a * K * R * c ** (R - 1) * xp.sin(th) * xp.sin(R * lam)
         return u, v
 
     def height(lam, th):
-        c = np.cos(th)
+        xp = _xp(lam, th)
+        c = xp.cos(th)
         A = 0.5 * w * (2.0 * Om + w) * c**2 + 0.25 * K**2 * c ** (2 * R) * (
             (R + 1) * c**2 + (2 * R**2 - R - 2) - 2.0 * R**2 * c ** (-2))
         B = (2.0 * (Om + w) * K) / ((R + 1) * (R + 2)) * c**R * (
             (R**2 + 2 * R + 2) - (R + 1) ** 2 * c**2)
         C = 0.25 * K**2 * c ** (2 * R) * ((R + 1) * c**2 - (R + 2))
-        return TC6_H0 + (a * a / g) * (A + B * np.cos(R * lam) + C * np.cos(2 * R * lam))
+        return TC6_H0 + (a * a / g) * (A + B * xp.cos(R * lam) + C * xp.cos(2 * R * lam))
 
     return height, winds
 

@@ -90,6 +90,7 @@ def test_butcher_steps_parity(P, golden, oracle_mod, name):
     assert status == 0
     op = make_op(P, e)
     st = op.state_from_array(X)
+    mg0 = [P.mass_integral(st, op, "h", level=k) for k in range(e["nz"])]
     tab = P.tableau(e["rk"])
     for _ in range(e["nsteps"]):
         P.rk_step(st, op.assemble_rhs, e["dt"], tab)
@@ -98,9 +99,11 @@ def test_butcher_steps_parity(P, golden, oracle_mod, name):
     if f"{name}/final" in g:            # the reference's own output
         assert_state_close(got, g[f"{name}/final"], e["case"])
     for k in range(e["nz"]):
+        # drift (device reduction at both ends) vs the reference's drift
         m0, m1 = e["mass_ic"][k], e["mass_final"][k]
         mg = P.mass_integral(st, op, "h", level=k)
-        assert abs((mg - m0) - (m1 - m0)) <= 1e-13 * abs(m0)
+        assert abs((mg - mg0[k]) - (m1 - m0)) <= 1e-13 * abs(m0)
+        assert abs(P.mass_integral_host(st, op, "h", level=k) - m1) <= 1e-13 * abs(m0)
 
 
 @pytest.mark.parametrize("name", RK3_CASES)
@@ -111,6 +114,7 @@ def test_fused_ssprk3_parity(P, golden, oracle_mod, name):
     U, _, _ = orc.rk_steps(X, e["dt"], 3, e["nsteps"])
     op = make_op(P, e)
     st = op.state_from_array(X)
+    mg0 = [P.mass_integral(st, op, "h", level=k) for k in range(e["nz"])]
     op.ssprk3_steps(st, e["dt"], e["nsteps"])
     flags, _ = op.status()
     assert flags == 0
@@ -119,7 +123,7 @@ def test_fused_ssprk3_parity(P, golden, oracle_mod, name):
     for k in range(e["nz"]):
         m0, m1 = e["mass_ic"][k], e["mass_final"][k]
         mg = P.mass_integral(st, op, "h", level=k)
-        assert abs((mg - m0) - (m1 - m0)) <= 1e-13 * abs(m0)
+        assert abs((mg - mg0[k]) - (m1 - m0)) <= 1e-13 * abs(m0)
 
 
 # Euler and Heun are unstable for DG advection at the RK3 cases' dt (their
@@ -182,7 +186,7 @@ def test_integrate_c1_against_reference(P, golden):
     st, log = P.integrate(st, op, P.TimeControls(cfg.t_final, dt=cfg.dt), P.tableau(3))
     assert log.steps == 100 and log.t == 1000.0 and log.dt == 10.0
     assert_state_close(st.to_numpy(), g["tc2_c1/final"], "williamson_tc2")
-    m = P.mass_integral(st, op)
+    m = P.mass_integral_host(st, op)
     assert abs((m - e["mass_ic"][0]) - (e["mass_final"][0] - e["mass_ic"][0])) <= 1e-13 * abs(m)
     l2 = P.l2_error(st, setup.exact(1000.0), op, "h", relative=True)
     assert abs(l2 - e["l2_h_rel_final"]) <= 1e-9 * e["l2_h_rel_final"]
@@ -402,3 +406,32 @@ def test_launch_counter_counts_kernels(P):
     op.ssprk3_steps(st, 10.0, 5)
     torch.cuda.synchronize()
     assert op.launch_count() - n0 == 15
+
+
+@pytest.mark.parametrize("case,nx,ny,p,nz", [("williamson_tc2", 40, 20, 2, 1), ("williamson_tc6", 70, 21, 3, 2),
+                                             ("williamson_tc6", 33, 9, 4, 1), ("williamson_tc2", 7, 5, 1, 1)])
+def test_device_diagnostics_and_projection(P, case, nx, ny, p, nz):
+    """Device mass_integral / l2_error (fixed-order double-double reductions)
+    against the reference-order host versions (diagnostics.py:42-107), and
+    the device initial-condition projection against the host one
+    (basis.py:206-233)."""
+    setup = P.build_case(P.default_config(case).override(nx=nx, ny=ny, p=p, nz=nz))
+    op = P.SpatialOperator(setup.mesh, p, setup.model, nz=nz)
+    st = op.project_state(setup.ic)
+    sd = op.project_state(setup.ic, device=True)
+    a, b = st.to_numpy(), sd.to_numpy()
+    for v in range(3):
+        scale = max(np.linalg.norm(a[v]), 1e-300)
+        assert np.linalg.norm(a[v] - b[v]) <= 1e-13 * max(scale, np.linalg.norm(a[0])), v
+    for k in range(nz):
+        for var in ("h", "hu"):
+            md, mh = P.mass_integral(st, op, var, k), P.mass_integral_host(st, op, var, k)
+            assert md == P.mass_integral(st, op, var, k)            # deterministic
+            assert abs(md - mh) <= 1e-14 * max(abs(mh), 1.0) * (1 + nx * ny * 1e-2)
+    ref = (lambda lam, th: setup.exact(0.0)(lam, th)) if case == "williamson_tc2" else setup.ic["h"]
+    # perturb so the error is not identically the projection error of the IC
+    op.ssprk3_steps(st, 1.0, 2)
+    ed, eh = P.l2_error(st, ref, op, "h", relative=True), P.l2_error_host(st, ref, op, "h", relative=True)
+    assert ed > 0 and abs(ed - eh) <= 1e-9 * eh
+    ed, eh = P.l2_error(st, ref, op, "h"), P.l2_error_host(st, ref, op, "h")
+    assert abs(ed - eh) <= 1e-9 * eh
