@@ -435,3 +435,31 @@ def test_device_diagnostics_and_projection(P, case, nx, ny, p, nz):
     assert ed > 0 and abs(ed - eh) <= 1e-9 * eh
     ed, eh = P.l2_error(st, ref, op, "h"), P.l2_error_host(st, ref, op, "h")
     assert abs(ed - eh) <= 1e-9 * eh
+
+
+@pytest.mark.parametrize("nx", [31, 32, 33, 64, 65, 97])
+@pytest.mark.parametrize("p", [1, 3, 4])
+def test_strip_boundaries(P, oracle_mod, nx, p):
+    """Strip-blocked layout edge cases: grids just below / at / above a
+    multiple of the 32-element strip (padding lanes, the last strip's right
+    neighbour wrapping to element 0, border faces between strips) against
+    the oracle, and the padding left untouched (zero)."""
+    ny = 5
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=nx, ny=ny, p=p))
+    op = P.SpatialOperator(setup.mesh, p, setup.model)
+    t, orc, X = oracle_mod.build_case("williamson_tc6", nx, ny, p)
+    st = op.state_from_array(X)
+    K = op.assemble_rhs(st).to_numpy()
+    Kr = orc.rhs(X)
+    sens = ulp_sensitivity(orc, X, Kr)
+    for v in range(3):
+        assert rel(K, Kr, v) <= max(20 * sens[v], 1e-13), (v, rel(K, Kr, v), sens[v])
+    dt = 160.0 / nx / (p + 1) ** 2        # well inside the stability limit (SURVEY 8d)
+    op.rk_steps(st, dt, 3, 3)
+    op.rk_steps(st, dt, 2, 4)
+    assert op.status()[0] == 0
+    U, _, _ = orc.rk_steps(X, dt, 3, 3)
+    U, _, _ = orc.rk_steps(U, dt, 4, 2)
+    assert_state_close(st.to_numpy(), U, "williamson_tc6")
+    pad = st.data.permute(0, 1, 2, 4, 3, 5).reshape(1, ny, 3, op.nphi, -1)[..., nx:]
+    assert pad.numel() == 0 or float(pad.abs().max()) == 0.0
