@@ -202,15 +202,34 @@ int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, c
     else
         o = hu ? setup_variant<P, true, false>(dev, smem, occ) : setup_variant<P, false, false>(dev, smem, occ);
     if (o < 0) return o;
-    // one wave: split every (strip, level) column of rows into as many
-    // contiguous chunks as the resident CTA slots allow
+    // Row chunking: every (strip, level) column of rows is split into
+    // contiguous chunks, one CTA each.  The chunk count minimises the
+    // modelled makespan  waves * (rows per chunk + kChunkOverhead), where
+    // waves = ceil(CTAs / resident slots) and the overhead (prologue and
+    // first-row work, measured ~1.4 rows) favours long chunks.  Narrow grids
+    // get one full wave (C3: 23 strips x 24 chunks of 15 rows); wide grids,
+    // whose strips alone outnumber the slots, get several waves of short
+    // chunks instead of one under-filled wave of very long ones.
     const int strips = c->nstrip;
     int rc = kp.rc;
     if (rc <= 0) {
+        constexpr double kChunkOverhead = 1.5;
         const long long slots = (long long)c->sms * o;
-        long long chunks = slots / ((long long)strips * c->cfg.nz);
-        if (chunks < 1) chunks = 1;
-        rc = (int)((rows + chunks - 1) / chunks);
+        const long long cols = (long long)strips * c->cfg.nz;
+        double best = 1e300;
+        long long best_chunks = 1;
+        const long long max_chunks = rows < 4 * slots ? rows : 4 * slots;
+        for (long long ch = 1; ch <= max_chunks; ++ch) {
+            const long long per = (rows + ch - 1) / ch;
+            if (ch > 1 && (rows + ch - 2) / (ch - 1) == per) continue;   // same chunk length
+            const long long waves = (cols * ch + slots - 1) / slots;
+            const double t = (double)waves * ((double)per + kChunkOverhead);
+            if (t < best - 1e-9) {
+                best = t;
+                best_chunks = ch;
+            }
+        }
+        rc = (int)((rows + best_chunks - 1) / best_chunks);
     }
     dgswe::StageParams kq = kp;
     kq.rc = rc;
