@@ -125,6 +125,11 @@ int dgswe_stage(dgswe_ctx *ctx, double a, const double *U, double b, const doubl
 int dgswe_stage_rows(dgswe_ctx *ctx, double a, const double *U, double b, const double *X,
                      double g, double *Y, int tag, int r0, int r1, void *stream);
 
+/* Same over two row ranges [r0, r1) and [r2, r3) (r1 <= r2) in ONE launch:
+ * a band's two boundary rows after its halo exchange. */
+int dgswe_stage_rows2(dgswe_ctx *ctx, double a, const double *U, double b, const double *X,
+                      double g, double *Y, int tag, int r0, int r1, int r2, int r3, void *stream);
+
 /* Y = a*U + b*X + g*RHS(X) and Y2 = A + g2*RHS(X) in one launch, on local
  * rows [r0, r1): the stage of classical RK4 whose second output is the
  * running accumulator u + sum_i dt b_i k_i (timestep.py:71-81, 163-164).

@@ -53,6 +53,7 @@ SIGNATURES = {
     "dgswe_rhs": (_I, [_VP, _VP, _VP, _VP]),
     "dgswe_stage": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _VP]),
     "dgswe_stage_rows": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _I, _I, _VP]),
+    "dgswe_stage_rows2": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _I, _I, _I, _I, _VP]),
     "dgswe_axpy": (_I, [_VP, _D, _VP, _VP, _I, _I, _VP]),
     "dgswe_ssprk3": (_I, [_VP, _VP, _VP, _VP, _D, _I, _I, _VP]),
     "dgswe_rk_steps": (_I, [_VP, _I, _VP, _VP, _VP, _VP, _D, _I, _I, _VP]),

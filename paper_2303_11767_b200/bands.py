@@ -204,6 +204,13 @@ class BandOperator:
             ctypes.c_void_p(X.data_ptr()), float(g), ctypes.c_void_p(Y.data_ptr()), int(tag),
             int(r0), int(r1), c.stream()), "dgswe_stage_rows")
 
+    def _launch2(self, a, U, b, X, g, Y, tag, r0, r1, r2, r3):
+        c = self.ctx
+        _lib.check(c.lib.dgswe_stage_rows2(
+            c.h, float(a), ctypes.c_void_p(U.data_ptr() if U is not None else 0), float(b),
+            ctypes.c_void_p(X.data_ptr()), float(g), ctypes.c_void_p(Y.data_ptr()), int(tag),
+            int(r0), int(r1), int(r2), int(r3), c.stream()), "dgswe_stage_rows2")
+
     def stage(self, a, U, b, X, g, Y, tag=0):
         """Halo exchange of X, then Y = a U + b X + g RHS(X) on owned rows."""
         L = self.layout
@@ -219,8 +226,8 @@ class BandOperator:
         if self.overlap and L.owned > 2:
             self._launch(a, U, b, X, g, Y, tag, L.jlo + 1, L.jhi - 1)   # no halo needed
             self.halo.finish()
-            self._launch(a, U, b, X, g, Y, tag, L.jlo, L.jlo + 1)
-            self._launch(a, U, b, X, g, Y, tag, L.jhi - 1, L.jhi)
+            # both boundary rows in one launch
+            self._launch2(a, U, b, X, g, Y, tag, L.jlo, L.jlo + 1, L.jhi - 1, L.jhi)
         else:
             self.halo.finish()
             self._launch(a, U, b, X, g, Y, tag, L.jlo, L.jhi)

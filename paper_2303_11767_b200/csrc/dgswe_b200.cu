@@ -185,7 +185,7 @@ template <int P>
 int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, cudaStream_t s)
 {
     using SM = dgswe::Smem<P>;
-    const int rows = r1 - r0;
+    const int rows = (r1 - r0) > (kp.j_end2 - kp.j_begin2) ? (r1 - r0) : (kp.j_end2 - kp.j_begin2);
     if (rows <= 0) return DGSWE_OK;
     const size_t smem = (size_t)SM::TOTAL * sizeof(double) + (size_t)c->smem_pad;
     static int occ[64][4] = {};     // resident CTAs per SM, per device and variant
@@ -233,7 +233,12 @@ int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, c
     }
     dgswe::StageParams kq = kp;
     kq.rc = rc;
-    dim3 grid(strips, (rows + rc - 1) / rc, c->cfg.nz);
+    int nchunks = (rows + rc - 1) / rc;
+    if (kp.j_end2 > kp.j_begin2) {   // a second row range in the same launch
+        kq.nchunk1 = nchunks;
+        nchunks += (kp.j_end2 - kp.j_begin2 + rc - 1) / rc;
+    }
+    dim3 grid(strips, nchunks, c->cfg.nz);
     if (hy) {
         if (hu)
             dgswe::stage_kernel<P, true, true><<<grid, dgswe::kThreads, smem, s>>>(kq);
@@ -253,7 +258,7 @@ int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, c
 // Y = a U + b X + g RHS(X) [, Y2 = A + g2 RHS(X)] on local rows [r0, r1)
 int launch_stage(dgswe_ctx *c, double a, const double *U, double b, const double *X, double g,
                  double *Y, const double *A, double g2, double *Y2, int tag, int r0, int r1,
-                 int check_finite, int check_mean, cudaStream_t s)
+                 int check_finite, int check_mean, cudaStream_t s, int r2 = 0, int r3 = 0)
 {
     if (!X || !Y) return fail(DGSWE_EINVAL, "null state pointer");
     if (X == Y || X == Y2) return fail(DGSWE_EINVAL, "outputs must not alias the stage input");
@@ -278,6 +283,11 @@ int launch_stage(dgswe_ctx *c, double a, const double *U, double b, const double
     kp.nrows = c->cfg.nrows;
     kp.j_begin = r0;
     kp.j_end = r1;
+    kp.nchunk1 = INT_MAX;
+    kp.j_begin2 = r2;
+    kp.j_end2 = r3;
+    if (r3 > r2 && (r2 < c->cfg.jlo || r3 > c->cfg.jhi || r2 < r1))
+        return fail(DGSWE_EINVAL, "second row range [%d,%d) invalid", r2, r3);
     kp.rc = c->rc;
     kp.a = a;
     kp.b = b;
@@ -478,6 +488,14 @@ int dgswe_stage_rows(dgswe_ctx *ctx, double a, const double *U, double b, const 
     if (!ctx) return fail(DGSWE_EINVAL, "null context");
     return launch_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, r0, r1, 0, 0,
                         (cudaStream_t)stream);
+}
+
+int dgswe_stage_rows2(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g,
+                      double *Y, int tag, int r0, int r1, int r2, int r3, void *stream)
+{
+    if (!ctx) return fail(DGSWE_EINVAL, "null context");
+    return launch_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, r0, r1, 0, 0,
+                        (cudaStream_t)stream, r2, r3);
 }
 
 int dgswe_stage2(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g,

@@ -57,6 +57,8 @@ struct StageParams {
     long long vstride;    // doubles per variable row (nstrip * nphi * 32)
     int nx, nstrip, ny, row0, nrows;
     int j_begin, j_end, rc;   // local rows [j_begin, j_end), rc rows per CTA
+    int nchunk1;              // chunks of the first range; later chunks cover [j_begin2, j_end2)
+    int j_begin2, j_end2;
     double a, b, g;       // Y = a U + b X + g RHS(X)
     const double *rowtab; // per global row, see RowLayout
     double inv_r;         // 1/R
@@ -824,8 +826,9 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
     const int strip = blockIdx.x;
     const int nvalid = min(kLanes, nx - strip * kLanes);
     const bool owned = lane < nvalid;
-    const int jb = kp.j_begin + blockIdx.y * kp.rc;
-    const int je = min(jb + kp.rc, kp.j_end);
+    const bool second = (int)blockIdx.y >= kp.nchunk1;   // one launch can cover two row ranges
+    const int jb = second ? kp.j_begin2 + ((int)blockIdx.y - kp.nchunk1) * kp.rc : kp.j_begin + blockIdx.y * kp.rc;
+    const int je = min(jb + kp.rc, second ? kp.j_end2 : kp.j_end);
     if (jb >= je) return;
 
     double *const ringS = smem + SM::XR0;          // [slot][var][mode][lane]

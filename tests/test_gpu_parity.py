@@ -261,8 +261,7 @@ def test_band_decomposition_bitwise(P, oracle_mod, world):
         y2 = bop.empty()
         if L.owned > 2:
             bop._launch(0.75, u, 0.25, x1, 1.75, y2, 0, L.jlo + 1, L.jhi - 1)
-            bop._launch(0.75, u, 0.25, x1, 1.75, y2, 0, L.jlo, L.jlo + 1)
-            bop._launch(0.75, u, 0.25, x1, 1.75, y2, 0, L.jhi - 1, L.jhi)
+            bop._launch2(0.75, u, 0.25, x1, 1.75, y2, 0, L.jlo, L.jlo + 1, L.jhi - 1, L.jhi)
         else:
             bop._launch(0.75, u, 0.25, x1, 1.75, y2, 0, L.jlo, L.jhi)
         assert np.array_equal(y1.cpu().numpy()[:, 1:L.jhi], want1[:, L.j0:L.j1])
