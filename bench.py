@@ -188,9 +188,15 @@ def run_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    same_gpu = os.environ.get("DGSWE_BENCH_SAME_GPU") == "1"   # test mode: all ranks on GPU 0
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     case, nx, ny, p, dt, label = CONFIGS[args.config]
     setup = P.build_case(P.default_config(case).override(nx=nx, ny=ny, p=p))
     op = P.SpatialOperator(setup.mesh, p, setup.model)
@@ -206,15 +212,47 @@ def run_gpu(args):
         state_bytes = state.data.numel() * 8
     else:
         L = BandLayout(ny, world, rank)
-        bop = BandOperator(op, L, transport="p2p")
         full = state.data.cpu().numpy()
-        u = torch.from_numpy(L.scatter(full)).cuda()
-        w1, w2 = bop.empty(), bop.empty()
+        transport = os.environ.get("DGSWE_BAND_TRANSPORT", "fused")
+        ok, bop = 1, None
+        if transport == "fused":
+            try:
+                bop = BandOperator(op, L, transport="fused")
+                u = bop.empty()
+                u.copy_(torch.from_numpy(L.scatter(full)))
+                w1, w2 = bop.empty(), bop.empty()
+                bop.attach(u, w1, w2)
+            except Exception as exc:                 # no peer mappings on this rank
+                log(f"rank {rank}: fused exchange unavailable ({exc})")
+                ok = 0
+            flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:                # every rank falls back together
+                if bop is not None:
+                    torch.cuda.synchronize()
+                    bop.close()
+                transport = "p2p"
+        if transport != "fused":
+            bop = BandOperator(op, L, transport="p2p")
+            u = torch.from_numpy(L.scatter(full)).cuda()
+            w1, w2 = bop.empty(), bop.empty()
         del state
+        graphs = {}
 
-        def steps(k):
+        def eager(k):
             for _ in range(k):
                 bop.ssprk3_step(u, w1, w2, dt)
+
+        def steps(k):
+            if transport != "fused":
+                return eager(k)
+            # no host collective on the fused path: K steps replay as one CUDA graph
+            if k not in graphs:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    eager(k)
+                graphs[k] = g
+            graphs[k].replay()
         counter = bop.launch_count
         state_bytes = u.numel() * 8
 
@@ -355,7 +393,8 @@ def run_gpu(args):
             "data": "synthetic (analytic Williamson initial condition projected on the mesh)",
             "config": {"workload": label, "case": case, "nx": nx, "ny": ny, "p": p, "dofs": dofs,
                        "dt": dt, "rk": "SSPRK3, Shu-Osher fused stages (== tableau(3))",
-                       "parallelism": f"latitude bands x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"latitude bands x{world}, halo exchange: {transport}"
+                                       if world > 1 else "single GPU"),
                        "l2": f"no flush; per-stage working set {3 * dofs * 8 / 1e6:.0f} MB "
                              f"(3 states) > 126 MB L2" if args.config != "c2" else
                              "C2 states (25 MB each) fit in L2; roofline inflated"},

@@ -48,6 +48,7 @@
 #ifndef DGSWE_B200_H
 #define DGSWE_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -124,6 +125,33 @@ int dgswe_stage(dgswe_ctx *ctx, double a, const double *U, double b, const doubl
 /* Same, restricted to local rows [r0, r1) (for interior/boundary overlap). */
 int dgswe_stage_rows(dgswe_ctx *ctx, double a, const double *U, double b, const double *X,
                      double g, double *Y, int tag, int r0, int r1, void *stream);
+
+/* ---- fused halo exchange over peer memory (one process per GPU) ----
+ * The band's two edge rows (jlo, jhi-1) are computed by dgswe_stage_edge,
+ * which also stores them straight into the neighbours' halo rows (peer
+ * pointers from CUDA IPC: dgswe_ipc_handle / dgswe_ipc_open) and counts
+ * each delivered strip block in the neighbour's receive counter
+ * (system-scope atomic after a system fence).  Before computing, an edge
+ * row waits until its own receive counter shows the neighbour's edge rows
+ * of the previous stage -- so interior rows (dgswe_stage_rows) need no halo
+ * at all and run concurrently on another stream, and no host collective is
+ * left on the path.  dgswe_set_exchange registers, once per context: the
+ * neighbours' level strides and receive counters (NULL at a pole), and this
+ * band's own counters: recv_count[2] (south, north deliveries) and
+ * stage_ctr[2] (completed edge launches, CTA completion scratch), zeroed.
+ * peer_row_s / peer_row_n: level-0 base of the neighbour's halo row in the
+ * buffer that plays Y's role there (NULL at a pole). */
+int dgswe_set_exchange(dgswe_ctx *ctx, long long peer_zstride_s, unsigned long long *peer_count_s,
+                       long long peer_zstride_n, unsigned long long *peer_count_n,
+                       unsigned long long *recv_count, unsigned long long *stage_ctr);
+int dgswe_stage_edge(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g, double *Y,
+                     int tag, double *peer_row_s, double *peer_row_n, void *stream);
+/* device memory the neighbours can map (zero-filled), and its IPC handles */
+int dgswe_dev_alloc(size_t bytes, void **out);
+int dgswe_dev_free(void *p);
+int dgswe_ipc_handle(void *p, char *out64);
+int dgswe_ipc_open(const char *in64, void **out);
+int dgswe_ipc_close(void *p);
 
 /* Same over two row ranges [r0, r1) and [r2, r3) (r1 <= r2) in ONE launch:
  * a band's two boundary rows after its halo exchange. */

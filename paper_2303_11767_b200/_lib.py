@@ -54,6 +54,13 @@ SIGNATURES = {
     "dgswe_stage": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _VP]),
     "dgswe_stage_rows": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _I, _I, _VP]),
     "dgswe_stage_rows2": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _I, _I, _I, _I, _VP]),
+    "dgswe_set_exchange": (_I, [_VP, ctypes.c_longlong, _VP, ctypes.c_longlong, _VP, _VP, _VP]),
+    "dgswe_stage_edge": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _VP, _VP, _VP]),
+    "dgswe_dev_alloc": (_I, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "dgswe_dev_free": (_I, [_VP]),
+    "dgswe_ipc_handle": (_I, [_VP, ctypes.c_char_p]),
+    "dgswe_ipc_open": (_I, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "dgswe_ipc_close": (_I, [_VP]),
     "dgswe_axpy": (_I, [_VP, _D, _VP, _VP, _I, _I, _VP]),
     "dgswe_ssprk3": (_I, [_VP, _VP, _VP, _VP, _D, _I, _I, _VP]),
     "dgswe_rk_steps": (_I, [_VP, _I, _VP, _VP, _VP, _VP, _D, _I, _I, _VP]),

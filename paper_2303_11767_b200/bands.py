@@ -16,10 +16,20 @@ strip-blocked layout of operator.py); buffer row 0
 is the southern halo (global row j0-1), rows 1..owned are owned, the last
 row is the northern halo.  Halo rows at a pole are never read.
 
-Transports: ``"p2p"`` -- torch.distributed batched isend/irecv on the
-device tensors (NCCL over NVLink/NVSwitch on a B200 node; also gloo for
-CPU tensors); ``"host"`` -- rows staged through host memory and exchanged
-with gloo (test transport: lets several ranks share one GPU).
+Transports:
+* ``"fused"`` -- no host collective on the path: each stage's two edge rows
+  are computed by one small launch (``dgswe_stage_edge``) that also stores
+  them straight into the neighbours' halo rows over peer memory (CUDA IPC
+  mappings: NVLink/NVSwitch on a B200 node) and bumps the neighbours'
+  receive counters; an edge row first waits for its own counter to show the
+  neighbour's previous-stage rows.  The interior rows need no halo and run
+  concurrently on a second stream.  Buffers must come from
+  :meth:`BandOperator.empty` (IPC-mappable) and be registered with
+  :meth:`BandOperator.attach`;
+* ``"p2p"`` -- torch.distributed batched isend/irecv on the device tensors
+  (NCCL over NVLink/NVSwitch; also gloo for CPU tensors);
+* ``"host"`` -- rows staged through host memory and exchanged with gloo
+  (test transport: lets several ranks share one GPU).
 """
 
 from __future__ import annotations
@@ -126,7 +136,7 @@ class HaloExchange:
     rows; finish() makes the current stream wait for it."""
 
     def __init__(self, layout: BandLayout, transport: str = "p2p", group=None):
-        if transport not in ("p2p", "host"):
+        if transport not in ("p2p", "host", "fused"):
             raise ValueError(f"unknown transport {transport!r}")
         self.layout, self.transport, self.group = layout, transport, group
         self._pending = None
@@ -183,11 +193,104 @@ class BandOperator:
         self.global_alpha = op_host.rusanov.mode == "global" and op_host.rusanov.alpha is None
         if self.global_alpha:
             _lib.check(self.ctx.lib.dgswe_set_external_alpha(self.ctx.h, 1), "set_external_alpha")
-        self.halo = HaloExchange(layout, transport, group)
+        if transport == "fused" and self.global_alpha:
+            raise ValueError("transport 'fused' supports local / pinned alpha only")
+        self.halo = HaloExchange(layout, transport if transport != "fused" else "p2p", group)
+        self._owned_mem = []       # (ptr, keep-alive) of library allocations
+        self._opened = []          # peer mappings to close
+        self._peer_rows = {}       # data_ptr of our buffer -> (south row ptr, north row ptr)
+        self._aux = None
 
     def empty(self, device=None):
-        return torch.zeros(self.shape, dtype=torch.float64,
-                           device=device or torch.device("cuda", torch.cuda.current_device()))
+        if self.transport != "fused":
+            return torch.zeros(self.shape, dtype=torch.float64,
+                               device=device or torch.device("cuda", torch.cuda.current_device()))
+        # IPC-mappable, zero-filled library allocation viewed as a tensor
+        lib = self.ctx.lib
+        nbytes = int(np.prod(self.shape)) * 8
+        ptr = ctypes.c_void_p()
+        _lib.check(lib.dgswe_dev_alloc(nbytes, ctypes.byref(ptr)), "dgswe_dev_alloc")
+        shape = self.shape
+
+        class _Mem:
+            __cuda_array_interface__ = {"shape": shape, "typestr": "<f8", "data": (ptr.value, False),
+                                        "version": 3}
+        t = torch.as_tensor(_Mem(), device="cuda")
+        self._owned_mem.append((ptr.value, t))
+        return t
+
+    def attach(self, *buffers):
+        """Fused transport: exchange CUDA IPC handles of this rank's state
+        buffers (their order is their role, identical on every rank) and of
+        the receive counters, and register the peer mappings."""
+        if self.transport != "fused":
+            return
+        lib, L = self.ctx.lib, self.layout
+        ctrl = self.empty_ctrl()
+        ptrs = [b.data_ptr() for b in buffers] + [ctrl]
+        handles = []
+        for ptr in ptrs:
+            buf = ctypes.create_string_buffer(64)
+            _lib.check(lib.dgswe_ipc_handle(ctypes.c_void_p(ptr), buf), "dgswe_ipc_handle")
+            handles.append(buf.raw)
+        mine = {"rank": L.rank, "nrows": L.nrows, "handles": handles}
+        allinfo = [None] * L.world
+        dist.all_gather_object(allinfo, mine, group=self.group)
+        rstride = int(np.prod(self.shape[2:]))                  # doubles per buffer row
+        peers = {}
+        for side, nb in ((0, L.south), (1, L.north)):
+            if nb is None:
+                continue
+            info = allinfo[nb]
+            opened = []
+            for h in info["handles"]:
+                p = ctypes.c_void_p()
+                _lib.check(lib.dgswe_ipc_open(h, ctypes.byref(p)), "dgswe_ipc_open")
+                opened.append(p.value)
+                self._opened.append(p.value)
+            peers[side] = (info["nrows"], opened)
+        # our edge row goes to the south neighbour's NORTH halo (its last row)
+        # and to the north neighbour's SOUTH halo (its row 0)
+        for k, b in enumerate(buffers):
+            rows = []
+            for side in (0, 1):
+                if side not in peers:
+                    rows.append(None)
+                    continue
+                nrows, opened = peers[side]
+                row = nrows - 1 if side == 0 else 0
+                rows.append(opened[k] + row * rstride * 8)
+            self._peer_rows[b.data_ptr()] = rows
+        cnt = [None, None]
+        zs = [0, 0]
+        for side in (0, 1):
+            if side in peers:
+                nrows, opened = peers[side]
+                # the neighbour's counter of deliveries from OUR side of it
+                cnt[side] = opened[-1] + (8 if side == 0 else 0)
+                zs[side] = nrows * rstride
+        _lib.check(lib.dgswe_set_exchange(self.ctx.h, zs[0], ctypes.c_void_p(cnt[0] or 0), zs[1],
+                                          ctypes.c_void_p(cnt[1] or 0), ctypes.c_void_p(ctrl),
+                                          ctypes.c_void_p(ctrl + 16)), "dgswe_set_exchange")
+        self._aux = torch.cuda.Stream()
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)          # every rank mapped before any delivery
+
+    def empty_ctrl(self):
+        """recv_count[2] (south, north deliveries) + stage_ctr[2], zeroed."""
+        ptr = ctypes.c_void_p()
+        _lib.check(self.ctx.lib.dgswe_dev_alloc(32, ctypes.byref(ptr)), "dgswe_dev_alloc")
+        self._owned_mem.append((ptr.value, None))
+        return ptr.value
+
+    def close(self):
+        lib = self.ctx.lib
+        for p in self._opened:
+            lib.dgswe_ipc_close(ctypes.c_void_p(p))
+        self._opened = []
+        for p, _ in self._owned_mem:
+            lib.dgswe_dev_free(ctypes.c_void_p(p))
+        self._owned_mem = []
 
     def _alpha_tensor(self):
         ptr = self.ctx.lib.dgswe_alpha_buffer(self.ctx.h)
@@ -211,9 +314,28 @@ class BandOperator:
             ctypes.c_void_p(X.data_ptr()), float(g), ctypes.c_void_p(Y.data_ptr()), int(tag),
             int(r0), int(r1), int(r2), int(r3), c.stream()), "dgswe_stage_rows2")
 
+    def _stage_fused(self, a, U, b, X, g, Y, tag):
+        L, c = self.layout, self.ctx
+        rows = self._peer_rows.get(Y.data_ptr())
+        if rows is None:
+            raise ValueError("fused transport: Y was not registered with attach()")
+        cur = torch.cuda.current_stream()
+        self._aux.wait_stream(cur)
+        with torch.cuda.stream(self._aux):
+            _lib.check(c.lib.dgswe_stage_edge(
+                c.h, float(a), ctypes.c_void_p(U.data_ptr() if U is not None else 0), float(b),
+                ctypes.c_void_p(X.data_ptr()), float(g), ctypes.c_void_p(Y.data_ptr()), int(tag),
+                ctypes.c_void_p(rows[0] or 0), ctypes.c_void_p(rows[1] or 0),
+                ctypes.c_void_p(self._aux.cuda_stream)), "dgswe_stage_edge")
+        if L.owned > 2:
+            self._launch(a, U, b, X, g, Y, tag, L.jlo + 1, L.jhi - 1)    # no halo needed
+        cur.wait_stream(self._aux)
+
     def stage(self, a, U, b, X, g, Y, tag=0):
         """Halo exchange of X, then Y = a U + b X + g RHS(X) on owned rows."""
         L = self.layout
+        if self.transport == "fused":
+            return self._stage_fused(a, U, b, X, g, Y, tag)
         self.halo.start(X)
         if self.global_alpha:
             self.halo.finish()

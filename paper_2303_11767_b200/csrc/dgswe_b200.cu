@@ -157,6 +157,12 @@ struct dgswe_ctx {
     int device = 0;
     int sms = 148;
     int smem_pad = 0;             // experiment knob: extra dynamic smem per CTA
+    // fused halo exchange (bands.py transport "fused"): set by dgswe_set_exchange
+    long long peer_zstride[2] = {0, 0};
+    unsigned long long *peer_count[2] = {nullptr, nullptr};
+    unsigned long long *recv_count = nullptr, *stage_ctr = nullptr;
+    double *edge_row[2] = {nullptr, nullptr};
+    int edge_pending = 0;
     std::map<GraphKey, cudaGraphExec_t> graphs;
     double *diag = nullptr;       // device scratch for diagnostics (row partials + tables)
     size_t diag_bytes = 0;
@@ -211,7 +217,7 @@ int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, c
     // whose strips alone outnumber the slots, get several waves of short
     // chunks instead of one under-filled wave of very long ones.
     const int strips = c->nstrip;
-    int rc = kp.rc;
+    int rc = kp.edge ? 1 : kp.rc;
     if (rc <= 0) {
         constexpr double kChunkOverhead = 1.5;
         const long long slots = (long long)c->sms * o;
@@ -266,7 +272,7 @@ int launch_stage(dgswe_ctx *c, double a, const double *U, double b, const double
     if (a != 0.0 && !U) return fail(DGSWE_EINVAL, "U is required when a != 0");
     if (r0 < c->cfg.jlo || r1 > c->cfg.jhi || r0 > r1)
         return fail(DGSWE_EINVAL, "row range [%d,%d) outside [%d,%d)", r0, r1, c->cfg.jlo, c->cfg.jhi);
-    dgswe::StageParams kp;
+    dgswe::StageParams kp = {};
     kp.X = X;
     kp.U = (a != 0.0) ? U : nullptr;
     kp.Y = Y;
@@ -310,6 +316,18 @@ int launch_stage(dgswe_ctx *c, double a, const double *U, double b, const double
     kp.tag = tag;
     kp.check_finite = check_finite;
     kp.check_mean = check_mean;
+    if (c->edge_pending) {
+        kp.edge = 1;
+        kp.band_lo = c->cfg.jlo;
+        kp.band_hi = c->cfg.jhi;
+        for (int k = 0; k < 2; ++k) {
+            kp.peer_row[k] = c->edge_row[k];
+            kp.peer_zstride[k] = c->peer_zstride[k];
+            kp.peer_count[k] = c->edge_row[k] ? c->peer_count[k] : nullptr;
+        }
+        kp.recv_count = c->recv_count;
+        kp.stage_ctr = c->stage_ctr;
+    }
     if (c->cfg.alpha_mode == DGSWE_ALPHA_GLOBAL && !c->external_alpha) {
         int rc = dgswe_alpha_prepass(c, X, s);
         if (rc) return rc;
@@ -488,6 +506,75 @@ int dgswe_stage_rows(dgswe_ctx *ctx, double a, const double *U, double b, const 
     if (!ctx) return fail(DGSWE_EINVAL, "null context");
     return launch_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, r0, r1, 0, 0,
                         (cudaStream_t)stream);
+}
+
+int dgswe_set_exchange(dgswe_ctx *ctx, long long peer_zstride_s, unsigned long long *peer_count_s,
+                       long long peer_zstride_n, unsigned long long *peer_count_n,
+                       unsigned long long *recv_count, unsigned long long *stage_ctr)
+{
+    if (!ctx || !recv_count || !stage_ctr) return fail(DGSWE_EINVAL, "null argument");
+    ctx->peer_zstride[0] = peer_zstride_s;
+    ctx->peer_zstride[1] = peer_zstride_n;
+    ctx->peer_count[0] = peer_count_s;
+    ctx->peer_count[1] = peer_count_n;
+    ctx->recv_count = recv_count;
+    ctx->stage_ctr = stage_ctr;
+    return DGSWE_OK;
+}
+
+int dgswe_stage_edge(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g, double *Y,
+                     int tag, double *peer_row_s, double *peer_row_n, void *stream)
+{
+    if (!ctx) return fail(DGSWE_EINVAL, "null context");
+    if (!ctx->stage_ctr) return fail(DGSWE_EINVAL, "dgswe_set_exchange first");
+    const int lo = ctx->cfg.jlo, hi = ctx->cfg.jhi;
+    ctx->edge_row[0] = peer_row_s;
+    ctx->edge_row[1] = peer_row_n;
+    ctx->edge_pending = 1;
+    const int rc = hi - lo >= 2 ? launch_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, lo, lo + 1, 0, 0,
+                                               (cudaStream_t)stream, hi - 1, hi)
+                                : launch_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, lo, hi, 0, 0,
+                                               (cudaStream_t)stream);
+    ctx->edge_pending = 0;
+    return rc;
+}
+
+int dgswe_dev_alloc(size_t bytes, void **out)
+{
+    if (!out) return fail(DGSWE_EINVAL, "null argument");
+    CUDA_TRY(cudaMalloc(out, bytes));
+    CUDA_TRY(cudaMemset(*out, 0, bytes));
+    return DGSWE_OK;
+}
+
+int dgswe_dev_free(void *p)
+{
+    CUDA_TRY(cudaFree(p));
+    return DGSWE_OK;
+}
+
+int dgswe_ipc_handle(void *p, char *out64)
+{
+    if (!p || !out64) return fail(DGSWE_EINVAL, "null argument");
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, p));
+    memcpy(out64, &h, sizeof h);
+    return DGSWE_OK;
+}
+
+int dgswe_ipc_open(const char *in64, void **out)
+{
+    if (!in64 || !out) return fail(DGSWE_EINVAL, "null argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, in64, sizeof h);
+    CUDA_TRY(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+    return DGSWE_OK;
+}
+
+int dgswe_ipc_close(void *p)
+{
+    CUDA_TRY(cudaIpcCloseMemHandle(p));
+    return DGSWE_OK;
 }
 
 int dgswe_stage_rows2(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g,

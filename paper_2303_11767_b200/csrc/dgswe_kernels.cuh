@@ -73,7 +73,23 @@ struct StageParams {
     int tag;
     int check_finite;
     int check_mean;
+    // fused halo exchange over peer memory (edge launches of a latitude
+    // band, bands.py transport "fused"): [0] south, [1] north neighbour
+    int edge;                           // 1: this launch computes the band's edge rows
+    int band_lo, band_hi;               // the band's computed rows [band_lo, band_hi)
+    double *peer_row[2];                // neighbour's halo row (level 0) our edge row is copied to
+    long long peer_zstride[2];
+    unsigned long long *peer_count[2];  // neighbour's receive counter for that halo
+    const unsigned long long *recv_count;   // own receive counters [2] (system-scope atomics)
+    unsigned long long *stage_ctr;      // own [0] completed edge launches, [1] CTA completions
 };
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 
 // per-row table layout (doubles): crc[n] srs[n] fcs[n] cr_b cos_b T[n][n]
 template <int P>
@@ -673,7 +689,8 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
                                              const double *sFX, const double *sF0,
                                              const double *sFtop, const double *sFbot, bool has_top,
                                              bool has_bot, const double *row, int lane, bool owned,
-                                             double *Yv, const StageParams &kp)
+                                             double *Yv, const StageParams &kp, double *Ypeer = nullptr,
+                                             double *Ypeer2 = nullptr)
 {
     constexpr int N = P + 1;
     using RL = RowLayout<P>;
@@ -725,6 +742,8 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
             double y = fma(kp.b, cur[(a * N + b) * kLanes + lane], (kp.g * (double)(2 * a + 1)) * k);
             if (HAS_U) y = fma(kp.a, un[a][b], y);
             if (owned) Yv[(a * N + b) * kLanes] = y;
+            if (owned && Ypeer) Ypeer[(a * N + b) * kLanes] = y;   // fused halo exchange (NVLink store)
+            if (owned && Ypeer2) Ypeer2[(a * N + b) * kLanes] = y;
             fexp = max(fexp, __double2hiint(y) & 0x7ff00000);
             if constexpr (HAS_Y2) {
                 const double y2 = fma(kp.g2 * (double)(2 * a + 1), k, an[a][b]);
@@ -830,6 +849,22 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
     const int jb = second ? kp.j_begin2 + ((int)blockIdx.y - kp.nchunk1) * kp.rc : kp.j_begin + blockIdx.y * kp.rc;
     const int je = min(jb + kp.rc, second ? kp.j_end2 : kp.j_end);
     if (jb >= je) return;
+    // fused halo exchange: an edge row first waits until the neighbour has
+    // delivered this stage's halo row (its previous stage's edge row):
+    // nstrip deliveries per completed stage, counted in our memory
+    if (kp.edge) {
+        if (threadIdx.x == 0) {
+            const unsigned long long need =
+                ld_acquire_sys(kp.stage_ctr) * (unsigned long long)kp.nstrip * gridDim.z;
+            const int g = kp.row0 + jb;
+            if (jb == kp.band_lo && g > 0)
+                while (ld_acquire_sys(kp.recv_count) < need) __nanosleep(64);
+            if (jb == kp.band_hi - 1 && g + 1 < kp.ny)
+                while (ld_acquire_sys(kp.recv_count + 1) < need) __nanosleep(64);
+            asm volatile("fence.proxy.async.global;" ::: "memory");   // peer stores -> TMA reads
+        }
+        __syncthreads();
+    }
 
     double *const ringS = smem + SM::XR0;          // [slot][var][mode][lane]
     double *const ring0 = ringS + v * NP * kLanes;   // this warp's variable
@@ -1028,10 +1063,20 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
             __syncthreads();                           // barrier 2
             TSTAMP(4);
             const size_t roff = (size_t)jl * kp.rstride;
+            // fused exchange: an edge row is also stored into the neighbour's
+            // halo row (south: band_lo, north: band_hi-1; a one-row band feeds both)
+            double *Ypeer = nullptr, *Ypeer2 = nullptr;
+            if (kp.edge) {
+                const size_t off = (size_t)strip * NP * kLanes + (size_t)v * kp.vstride + lane;
+                if (jl == kp.band_lo && kp.peer_row[0])
+                    Ypeer = kp.peer_row[0] + (size_t)blockIdx.z * kp.peer_zstride[0] + off;
+                if (jl == kp.band_hi - 1 && kp.peer_row[1])
+                    Ypeer2 = kp.peer_row[1] + (size_t)blockIdx.z * kp.peer_zstride[1] + off;
+            }
             bad |= finalize<P, HAS_U, HAS_Y2>(vol, cur, HAS_U ? Uz + roff : nullptr,
                                               HAS_Y2 ? Az + roff : nullptr, HAS_Y2 ? Y2z + roff : nullptr, v, sFX,
                                       smem + SM::F0 + slot * 3 * N, sFa, sFb, has_top, has_bot, row, lane,
-                                      owned, Yz + roff, kp);
+                                      owned, Yz + roff, kp, Ypeer, Ypeer2);
             // X(jl) is consumed: stream row jl+2 into its slot (L2-warm by now)
             __syncwarp();
             if (lane == 0 && jl + 2 <= last_fetch) {
@@ -1061,6 +1106,24 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
     if (bad && lane == 0) {
         atomicOr(kp.status, bad);
         atomicMin(kp.first_tag, kp.tag);
+    }
+    if (kp.edge) {
+        // publish the edge rows stored into the neighbours' halos, then count
+        // this CTA; the last one advances the band's stage counter
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence_system();
+            for (int side = 0; side < 2; ++side) {
+                const int r = side == 0 ? kp.band_lo : kp.band_hi - 1;
+                if (kp.peer_count[side] && jb <= r && r < je) atomicAdd_system(kp.peer_count[side], 1ull);
+            }
+            const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+            if (atomicAdd(kp.stage_ctr + 1, 1ull) == total - 1) {
+                kp.stage_ctr[1] = 0;
+                __threadfence();
+                atomicAdd(kp.stage_ctr, 1ull);
+            }
+        }
     }
 }
 

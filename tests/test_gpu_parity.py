@@ -285,6 +285,27 @@ def test_multiprocess_bands_on_one_gpu(P, tmp_path):
     assert np.array_equal(got, st.data.cpu().numpy())
 
 
+@pytest.mark.parametrize("world,graph", [(2, False), (3, False), (2, True)])
+def test_fused_exchange_bands_on_one_gpu(P, tmp_path, world, graph):
+    """Fused halo exchange (edge rows stored into the neighbours' halo rows
+    over CUDA-IPC peer mappings, system-scope counters, interior rows on a
+    second stream), all ranks sharing GPU 0: equals the single-GPU run
+    bitwise."""
+    out = tmp_path / "fused.npy"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={29540 + world + 10 * graph}",
+           os.path.join(ROOT, "tools", "band_run.py"), "--transport", "fused", "--same-gpu",
+           "--out", str(out)] + (["--graph"] if graph else [])
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    got = np.load(out)
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=48, ny=16, p=3))
+    op = P.SpatialOperator(setup.mesh, 3, setup.model)
+    st = op.project_state(setup.ic)
+    op.ssprk3_steps(st, 5.0, 4)
+    assert np.array_equal(got, st.data.cpu().numpy())
+
+
 def test_positivity_raises(P):
     setup = P.build_case(P.default_config("williamson_tc6").override(nx=12, ny=6, p=2))
     op = P.SpatialOperator(setup.mesh, 2, setup.model)

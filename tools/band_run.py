@@ -5,7 +5,8 @@
 Every rank owns a band of TC6 48x16 p=3, steps it with a halo exchange per
 stage, and rank 0 gathers the owned rows into one (nz, ny, 3, nphi, nx)
 array.  ``--transport host`` lets all ranks share GPU 0 (gloo);
-``--transport p2p`` uses NCCL with one GPU per rank.
+``--transport p2p`` uses NCCL with one GPU per rank; ``--transport fused``
+the in-kernel peer-memory exchange (``--same-gpu``: all ranks on GPU 0).
 """
 
 from __future__ import annotations
@@ -29,20 +30,34 @@ def main():
     ap.add_argument("--transport", default="host")
     ap.add_argument("--out", required=True)
     ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--same-gpu", action="store_true", help="all ranks on GPU 0 (gloo process group)")
+    ap.add_argument("--graph", action="store_true", help="capture the steps in one CUDA graph (fused)")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    dev = 0 if args.transport == "host" else int(os.environ.get("LOCAL_RANK", 0))
+    same = args.transport == "host" or args.same_gpu
+    dev = 0 if same else int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
-    dist.init_process_group("gloo" if args.transport == "host" else "nccl")
+    dist.init_process_group("gloo" if same else "nccl")
     setup = P.build_case(P.default_config("williamson_tc6").override(nx=48, ny=16, p=3))
     op = P.SpatialOperator(setup.mesh, 3, setup.model)
     full = op.project_state(setup.ic).data.cpu().numpy()
     L = BandLayout(16, world, rank)
     bop = BandOperator(op, L, transport=args.transport)
-    u = torch.from_numpy(L.scatter(full)).cuda()
+    u = bop.empty()
+    u.copy_(torch.from_numpy(L.scatter(full)))
     w1, w2 = bop.empty(), bop.empty()
-    for k in range(args.steps):
-        bop.ssprk3_step(u, w1, w2, 5.0, tag=k)
+    bop.attach(u, w1, w2)
+    if args.graph:
+        bop.ssprk3_step(u, w1, w2, 5.0, tag=0)            # eager first step
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for k in range(1, args.steps):
+                bop.ssprk3_step(u, w1, w2, 5.0, tag=k)
+        g.replay()
+    else:
+        for k in range(args.steps):
+            bop.ssprk3_step(u, w1, w2, 5.0, tag=k)
     flags, _ = bop.status()
     assert flags == 0, flags
     mine = u[:, L.jlo:L.jhi].cpu().contiguous()
@@ -57,6 +72,8 @@ def main():
     else:
         dist.send(mine, dst=0)
     dist.barrier()
+    torch.cuda.synchronize()
+    bop.close()
     dist.destroy_process_group()
 
 
