@@ -172,15 +172,15 @@ struct dgswe_ctx {
 
 namespace {
 
-template <int P, bool HU, bool HY>
-int setup_variant(int dev, size_t smem, int (&occ)[64][4])
+template <int P, bool HU, bool HY, bool ED>
+int setup_variant(int dev, size_t smem, int (&occ)[64][6])
 {
-    const int var = (HU ? 1 : 0) + (HY ? 2 : 0);
+    const int var = ED ? 4 + (HU ? 1 : 0) : (HU ? 1 : 0) + (HY ? 2 : 0);
     if (!occ[dev][var]) {
-        CUDA_TRY(cudaFuncSetAttribute(dgswe::stage_kernel<P, HU, HY>,
+        CUDA_TRY(cudaFuncSetAttribute(dgswe::stage_kernel<P, HU, HY, ED>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int o = 0;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, dgswe::stage_kernel<P, HU, HY>,
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, dgswe::stage_kernel<P, HU, HY, ED>,
                                                                dgswe::kThreads, smem));
         occ[dev][var] = o > 0 ? o : 1;
     }
@@ -194,19 +194,25 @@ int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, c
     const int rows = (r1 - r0) > (kp.j_end2 - kp.j_begin2) ? (r1 - r0) : (kp.j_end2 - kp.j_begin2);
     if (rows <= 0) return DGSWE_OK;
     const size_t smem = (size_t)SM::TOTAL * sizeof(double) + (size_t)c->smem_pad;
-    static int occ[64][4] = {};     // resident CTAs per SM, per device and variant
+    static int occ[64][6] = {};     // resident CTAs per SM, per device and variant
     static size_t occ_smem[64] = {};
     const int dev = c->device & 63;
     if (occ_smem[dev] != smem) {
-        for (int k = 0; k < 4; ++k) occ[dev][k] = 0;
+        for (int k = 0; k < 6; ++k) occ[dev][k] = 0;
         occ_smem[dev] = smem;
     }
-    const bool hu = kp.U != nullptr, hy = kp.Y2 != nullptr;
+    const bool hu = kp.U != nullptr, hy = kp.Y2 != nullptr, ed = kp.edge != 0;
+    if (ed && hy) return fail(DGSWE_EUNSUPPORTED, "edge launches have one output");
     int o;
-    if (hy)
-        o = hu ? setup_variant<P, true, true>(dev, smem, occ) : setup_variant<P, false, true>(dev, smem, occ);
+    if (ed)
+        o = hu ? setup_variant<P, true, false, true>(dev, smem, occ)
+               : setup_variant<P, false, false, true>(dev, smem, occ);
+    else if (hy)
+        o = hu ? setup_variant<P, true, true, false>(dev, smem, occ)
+               : setup_variant<P, false, true, false>(dev, smem, occ);
     else
-        o = hu ? setup_variant<P, true, false>(dev, smem, occ) : setup_variant<P, false, false>(dev, smem, occ);
+        o = hu ? setup_variant<P, true, false, false>(dev, smem, occ)
+               : setup_variant<P, false, false, false>(dev, smem, occ);
     if (o < 0) return o;
     // Row chunking: every (strip, level) column of rows is split into
     // contiguous chunks, one CTA each.  The chunk count minimises the
@@ -245,16 +251,21 @@ int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, c
         nchunks += (kp.j_end2 - kp.j_begin2 + rc - 1) / rc;
     }
     dim3 grid(strips, nchunks, c->cfg.nz);
-    if (hy) {
+    if (ed) {
         if (hu)
-            dgswe::stage_kernel<P, true, true><<<grid, dgswe::kThreads, smem, s>>>(kq);
+            dgswe::stage_kernel<P, true, false, true><<<grid, dgswe::kThreads, smem, s>>>(kq);
         else
-            dgswe::stage_kernel<P, false, true><<<grid, dgswe::kThreads, smem, s>>>(kq);
+            dgswe::stage_kernel<P, false, false, true><<<grid, dgswe::kThreads, smem, s>>>(kq);
+    } else if (hy) {
+        if (hu)
+            dgswe::stage_kernel<P, true, true, false><<<grid, dgswe::kThreads, smem, s>>>(kq);
+        else
+            dgswe::stage_kernel<P, false, true, false><<<grid, dgswe::kThreads, smem, s>>>(kq);
     } else {
         if (hu)
-            dgswe::stage_kernel<P, true, false><<<grid, dgswe::kThreads, smem, s>>>(kq);
+            dgswe::stage_kernel<P, true, false, false><<<grid, dgswe::kThreads, smem, s>>>(kq);
         else
-            dgswe::stage_kernel<P, false, false><<<grid, dgswe::kThreads, smem, s>>>(kq);
+            dgswe::stage_kernel<P, false, false, false><<<grid, dgswe::kThreads, smem, s>>>(kq);
     }
     CUDA_TRY(cudaGetLastError());
     c->launches += 1;

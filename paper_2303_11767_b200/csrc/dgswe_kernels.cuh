@@ -825,7 +825,7 @@ __device__ __forceinline__ void bottom_traces(const double *ring_row, int lane, 
     }
 }
 
-template <int P, bool HAS_U, bool HAS_Y2>
+template <int P, bool HAS_U, bool HAS_Y2, bool EDGE>
 __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel(StageParams kp)
 {
     constexpr int N = P + 1;
@@ -852,7 +852,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
     // fused halo exchange: an edge row first waits until the neighbour has
     // delivered this stage's halo row (its previous stage's edge row):
     // nstrip deliveries per completed stage, counted in our memory
-    if (kp.edge) {
+    if constexpr (EDGE) {
         if (threadIdx.x == 0) {
             const unsigned long long need =
                 ld_acquire_sys(kp.stage_ctr) * (unsigned long long)kp.nstrip * gridDim.z;
@@ -1066,7 +1066,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
             // fused exchange: an edge row is also stored into the neighbour's
             // halo row (south: band_lo, north: band_hi-1; a one-row band feeds both)
             double *Ypeer = nullptr, *Ypeer2 = nullptr;
-            if (kp.edge) {
+            if constexpr (EDGE) {
                 const size_t off = (size_t)strip * NP * kLanes + (size_t)v * kp.vstride + lane;
                 if (jl == kp.band_lo && kp.peer_row[0])
                     Ypeer = kp.peer_row[0] + (size_t)blockIdx.z * kp.peer_zstride[0] + off;
@@ -1107,7 +1107,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
         atomicOr(kp.status, bad);
         atomicMin(kp.first_tag, kp.tag);
     }
-    if (kp.edge) {
+    if constexpr (EDGE) {
         // publish the edge rows stored into the neighbours' halos, then count
         // this CTA; the last one advances the band's stage counter
         __syncthreads();
