@@ -561,6 +561,77 @@ __device__ __forceinline__ void face_flux_rt(const double (&in)[3][P + 1], const
     }
 }
 
+// Scalars of one face-flux call, by value (no pointer to the kernel
+// parameters may escape into a non-inlined function).
+struct FaceArgs {
+    double h_floor, inv_floor, sqrt_g, half_g, inv_r;
+    int alpha_mode, dir;
+    double cr_e, cos_e, alpha_glob, scale;
+};
+
+// ONE non-inlined copy of the Rusanov face flux serves the h warp's
+// x-faces, the face warp's y-faces and the strip's border face: traces and
+// result are addressed as (offset, leading dimension, column) in the
+// kernel's dynamic shared memory, so no register array crosses the call.
+// (Three inlined copies cost ~1k SASS instructions of a kernel whose speed
+// tracks its instruction-cache footprint.)
+template <int P>
+__device__ __noinline__ void face_flux_call(int in_off, int in_ld, int in_col, int out_off, int out_ld,
+                                            int out_col, int dst_off, int dst_ld, int dst_col, FaceArgs fa)
+{
+    constexpr int N = P + 1;
+    extern __shared__ double smem[];
+    double in[3][N], out[3][N];
+#pragma unroll
+    for (int v = 0; v < 3; ++v)
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            in[v][k] = smem[in_off + (v * N + k) * in_ld + in_col];
+            out[v][k] = smem[out_off + (v * N + k) * out_ld + out_col];
+        }
+    double rin[N], rout[N], mi[N], mo[N];
+    double am[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        double ci, co;
+        inv_and_celerity(in[0][k], fa.h_floor, fa.inv_floor, fa.sqrt_g, rin[k], ci);
+        inv_and_celerity(out[0][k], fa.h_floor, fa.inv_floor, fa.sqrt_g, rout[k], co);
+        mi[k] = fa.dir == 0 ? in[1][k] : in[2][k];     // normal momentum
+        mo[k] = fa.dir == 0 ? out[1][k] : out[2][k];
+        am[k] = max_nn(fabs(mi[k] * rin[k]) + ci, fabs(mo[k] * rout[k]) + co);
+    }
+#pragma unroll
+    for (int w = 1; w < N; w *= 2)
+#pragma unroll
+        for (int k = 0; k + w < N; k += 2 * w) am[k] = max_nn(am[k], am[k + w]);
+    double alpha = am[0] * fa.inv_r;
+    if (fa.dir == 1) alpha *= fa.cos_e;
+    if (fa.alpha_mode != 0) alpha = fa.alpha_glob;
+    const double ha = (0.5 * fa.scale) * alpha;
+    const double hs = (0.5 * fa.scale) * (fa.dir == 0 ? fa.inv_r : fa.cr_e);
+    const double sx = fa.dir == 0 ? 1.0 : 0.0, sy = 1.0 - sx;
+    double fs[3][N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const double hi = in[0][k], ui = in[1][k], vi = in[2][k];
+        const double ho = out[0][k], uo = out[1][k], vo = out[2][k];
+        const double gi = hi * hi * fa.half_g, go = ho * ho * fa.half_g;
+        const double wi = mi[k] * rin[k], wo = mo[k] * rout[k];
+        const double fi1 = fma(ui, wi, sx * gi), fo1 = fma(uo, wo, sx * go);
+        const double fi2 = fma(vi, wi, sy * gi), fo2 = fma(vo, wo, sy * go);
+        fs[0][k] = fma(hs, mi[k] + mo[k], -ha * (ho - hi));
+        fs[1][k] = fma(hs, fi1 + fo1, -ha * (uo - ui));
+        fs[2][k] = fma(hs, fi2 + fo2, -ha * (vo - vi));
+    }
+#pragma unroll
+    for (int v = 0; v < 3; ++v) {
+        double g[N];
+        n2m<P, 2>(fs[v], g);
+#pragma unroll
+        for (int b = 0; b < N; ++b) smem[dst_off + (v * N + b) * dst_ld + dst_col] = g[b];
+    }
+}
+
 // traces [3][N] from shared memory: element column `col` of a [3][N][ld] array
 template <int P>
 __device__ __forceinline__ void traces_from_smem(double (&tr)[3][P + 1], const double *s, int ld, int col)
@@ -967,11 +1038,17 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
                 for (int q = 0; q < N; ++q) bad |= owned && !(bt[0][q] > 0.0);
                 const bool face = pre ? below : (kp.row0 + it + 1 < kp.ny);
                 if (face) {
-                    double tt[3][N];
-                    traces_from_smem<P>(tt, sT, kLanes, lane);
+                    // bottom traces staged in the face's output slot, read back by the call
+                    const int dst = (int)((pre ? fb : fa) - smem);
+#pragma unroll
+                    for (int vv = 0; vv < 3; ++vv)
+#pragma unroll
+                        for (int q = 0; q < N; ++q) smem[dst + (vv * N + q) * kLanes + lane] = bt[vv][q];
                     const double *above = sRow + ((k + 1) % 3) * RL::STRIDE;
-                    face_flux_rt<P>(tt, bt, pre ? fb : fa, kLanes, lane, kp, 1, above[RL::CRB],
-                                    above[RL::COSB], alpha_y, kp.bdx);
+                    face_flux_call<P>(SM::TT, kLanes, lane, dst, kLanes, lane, dst, kLanes, lane,
+                                      FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
+                                               kp.alpha_mode, 1, above[RL::CRB], above[RL::COSB], alpha_y,
+                                               kp.bdx});
                 }
             }
             if (!pre && it + 2 <= je && kp.row0 + it + 2 < kp.ny) {
@@ -1002,12 +1079,10 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
                 }
                 border_traces<P>(Xrow, next_tile, eL, eR, smem + SM::HL, smem + SM::E0, smem + SM::HR,
                                  lane, kp);
-                double in[3][N], out[3][N];
-                traces_from_smem<P>(in, smem + SM::HL, 1, 0);
-                traces_from_smem<P>(out, smem + SM::E0, 1, 0);
                 // every lane computes the same face (uniform control flow, identical stores)
-                face_flux_rt<P>(in, out, smem + SM::F0 + ((k + 1) & 1) * 3 * N, 1, 0, kp, 0, 0.0, 0.0,
-                                alpha_x, kp.bdy);
+                face_flux_call<P>(SM::HL, 1, 0, SM::E0, 1, 0, SM::F0 + ((k + 1) & 1) * 3 * N, 1, 0,
+                                  FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
+                                           kp.alpha_mode, 0, 0.0, 0.0, alpha_x, kp.bdy});
             }
             TSTAMP(e);
             if (!pre) {
@@ -1049,13 +1124,11 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
             if (v == 0) {
                 // the h warp has the lightest volume work: it takes the x-faces 1..32
                 // (right face of every lane; the last valid lane's neighbour is the halo)
-                double in[3][N], out[3][N];
-                traces_from_smem<P>(in, sXR, kLanes, lane);
-                if (lane == nvalid - 1)
-                    traces_from_smem<P>(out, smem + SM::HR, 1, 0);
-                else
-                    traces_from_smem<P>(out, sXL, kLanes, min(lane + 1, kLanes - 1));
-                face_flux<P, 0>(in, out, sFX, kLanes + 1, lane + 1, kp, 0.0, 0.0, alpha_x, kp.bdy);
+                const bool last = lane == nvalid - 1;
+                face_flux_call<P>(SM::XRT, kLanes, lane, last ? SM::HR : SM::XL, last ? 1 : kLanes,
+                                  last ? 0 : min(lane + 1, kLanes - 1), SM::FX, kLanes + 1, lane + 1,
+                                  FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
+                                           kp.alpha_mode, 0, 0.0, 0.0, alpha_x, kp.bdy});
             }
             double vol[N][N];
             volume<P>(vol, v, sU, row, lane, kp);
