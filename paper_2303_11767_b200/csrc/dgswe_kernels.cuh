@@ -840,7 +840,7 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
 template <int P>
 __device__ __forceinline__ void border_traces(const double *Xrow, const double *ring_slot, int eL, int eR,
                                               double *sHL, double *sE0, double *sHR, int lane,
-                                              const StageParams &kp)
+                                              long long vstride)
 {
     constexpr int N = P + 1;
     constexpr int NP = N * N;
@@ -855,7 +855,7 @@ __device__ __forceinline__ void border_traces(const double *Xrow, const double *
                 for (int b = 0; b < N; ++b) c[a][b] = src[(a * N + b) * kLanes];
         } else {
             const int e = side == 0 ? eL : eR;
-            const double *src = Xrow + (size_t)v * kp.vstride + (size_t)(e >> 5) * NP * kLanes + (e & 31);
+            const double *src = Xrow + (size_t)v * vstride + (size_t)(e >> 5) * NP * kLanes + (e & 31);
 #pragma unroll
             for (int a = 0; a < N; ++a)
 #pragma unroll
@@ -1078,7 +1078,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
                     }
                 }
                 border_traces<P>(Xrow, next_tile, eL, eR, smem + SM::HL, smem + SM::E0, smem + SM::HR,
-                                 lane, kp);
+                                 lane, kp.vstride);
                 // every lane computes the same face (uniform control flow, identical stores)
                 face_flux_call<P>(SM::HL, 1, 0, SM::E0, 1, 0, SM::F0 + ((k + 1) & 1) * 3 * N, 1, 0,
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
