@@ -576,8 +576,8 @@ struct FaceArgs {
 // (Three inlined copies cost ~1k SASS instructions of a kernel whose speed
 // tracks its instruction-cache footprint.)
 template <int P>
-__device__ __noinline__ void face_flux_call(int in_off, int in_ld, int in_col, int out_off, int out_ld,
-                                            int out_col, int dst_off, int dst_ld, int dst_col, FaceArgs fa)
+__device__ __forceinline__ void face_flux_body(int in_off, int in_ld, int in_col, int out_off, int out_ld,
+                                               int out_col, int dst_off, int dst_ld, int dst_col, FaceArgs fa)
 {
     constexpr int N = P + 1;
     extern __shared__ double smem[];
@@ -630,6 +630,25 @@ __device__ __noinline__ void face_flux_call(int in_off, int in_ld, int in_col, i
 #pragma unroll
         for (int b = 0; b < N; ++b) smem[dst_off + (v * N + b) * dst_ld + dst_col] = g[b];
     }
+}
+
+template <int P>
+__device__ __noinline__ void face_flux_noinline(int in_off, int in_ld, int in_col, int out_off, int out_ld,
+                                                int out_col, int dst_off, int dst_ld, int dst_col, FaceArgs fa)
+{
+    face_flux_body<P>(in_off, in_ld, in_col, out_off, out_ld, out_col, dst_off, dst_ld, dst_col, fa);
+}
+
+// p >= 2: the shared non-inlined copy; p <= 1: inlined (the face work is a
+// large share of a low-order element and the call's overhead shows, measured)
+template <int P>
+__device__ __forceinline__ void face_flux_call(int in_off, int in_ld, int in_col, int out_off, int out_ld,
+                                               int out_col, int dst_off, int dst_ld, int dst_col, FaceArgs fa)
+{
+    if constexpr (P <= 1)
+        face_flux_body<P>(in_off, in_ld, in_col, out_off, out_ld, out_col, dst_off, dst_ld, dst_col, fa);
+    else
+        face_flux_noinline<P>(in_off, in_ld, in_col, out_off, out_ld, out_col, dst_off, dst_ld, dst_col, fa);
 }
 
 // traces [3][N] from shared memory: element column `col` of a [3][N][ld] array
