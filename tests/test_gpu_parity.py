@@ -285,23 +285,25 @@ def test_multiprocess_bands_on_one_gpu(P, tmp_path):
     assert np.array_equal(got, st.data.cpu().numpy())
 
 
-@pytest.mark.parametrize("world,graph", [(2, False), (3, False), (2, True)])
-def test_fused_exchange_bands_on_one_gpu(P, tmp_path, world, graph):
+@pytest.mark.parametrize("world,graph,nz", [(2, False, 1), (3, False, 1), (2, True, 1), (3, True, 2)])
+def test_fused_exchange_bands_on_one_gpu(P, tmp_path, world, graph, nz):
     """Fused halo exchange (edge rows stored into the neighbours' halo rows
     over CUDA-IPC peer mappings, system-scope counters, interior rows on a
     second stream), all ranks sharing GPU 0: equals the single-GPU run
     bitwise."""
     out = tmp_path / "fused.npy"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr=127.0.0.1", f"--master-port={29540 + world + 10 * graph}",
+           "--master-addr=127.0.0.1", f"--master-port={29540 + world + 10 * graph + 20 * nz}",
            os.path.join(ROOT, "tools", "band_run.py"), "--transport", "fused", "--same-gpu",
-           "--out", str(out)] + (["--graph"] if graph else [])
+           "--out", str(out), "--nz", str(nz)] + (["--graph"] if graph else [])
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     got = np.load(out)
-    setup = P.build_case(P.default_config("williamson_tc6").override(nx=48, ny=16, p=3))
-    op = P.SpatialOperator(setup.mesh, 3, setup.model)
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=48, ny=16, p=3, nz=nz))
+    op = P.SpatialOperator(setup.mesh, 3, setup.model, nz=nz)
     st = op.project_state(setup.ic)
+    if nz > 1:
+        st.data[1:] *= 1.0001
     op.ssprk3_steps(st, 5.0, 4)
     assert np.array_equal(got, st.data.cpu().numpy())
 

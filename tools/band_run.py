@@ -32,15 +32,18 @@ def main():
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--same-gpu", action="store_true", help="all ranks on GPU 0 (gloo process group)")
     ap.add_argument("--graph", action="store_true", help="capture the steps in one CUDA graph (fused)")
+    ap.add_argument("--nz", type=int, default=1)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     same = args.transport == "host" or args.same_gpu
     dev = 0 if same else int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
     dist.init_process_group("gloo" if same else "nccl")
-    setup = P.build_case(P.default_config("williamson_tc6").override(nx=48, ny=16, p=3))
-    op = P.SpatialOperator(setup.mesh, 3, setup.model)
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=48, ny=16, p=3, nz=args.nz))
+    op = P.SpatialOperator(setup.mesh, 3, setup.model, nz=args.nz)
     full = op.project_state(setup.ic).data.cpu().numpy()
+    if args.nz > 1:
+        full[1:] *= 1.0001                        # distinct levels
     L = BandLayout(16, world, rank)
     bop = BandOperator(op, L, transport=args.transport)
     u = bop.empty()
