@@ -272,8 +272,6 @@ struct Smem {
     static constexpr int TOTAL = MBAR + 6;
 };
 
-__device__ __forceinline__ double sgn(int k) { return (k & 1) ? -1.0 : 1.0; }
-
 // max(x, y) for y > 0 on the integer pipe: the signed 64-bit order of the
 // bit patterns equals the floating-point order for non-negative values and
 // puts every negative x below y (fp64 fmax is a DSETP + select sequence,
@@ -444,123 +442,6 @@ __device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], do
     return bad;
 }
 
-// Rusanov flux over one face from register traces: "in" = lower/left
-// element, "out" = upper/right element, [var][node].  Stored is the face's
-// boundary-integral projection g[var][k'] = scale * sum_k w_k P_k'(x_k) f*[k]
-// (dg.py:206-212, 465-495): both neighbours lift it with their own
-// outward-normal sign and mode parity, so each face is projected once.
-// DIR 0: x-face, physical flux F, alpha = (|u|+c)/R.
-// DIR 1: y-face, physical flux G = cos/R * (...), alpha = cos (|v|+c)/R.
-template <int P, int DIR>
-__device__ __forceinline__ void face_flux(const double (&in)[3][P + 1], const double (&out)[3][P + 1],
-                                          double *sF, int ld, int col, const StageParams &kp,
-                                          double cr_e, double cos_e, double alpha_glob,
-                                          double scale)
-{
-    constexpr int N = P + 1;
-    constexpr int M = DIR == 0 ? 1 : 2;   // normal momentum
-    double rin[N], rout[N];
-    double am[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-        double ci, co;
-        inv_and_celerity(in[0][k], kp.h_floor, kp.inv_floor, kp.sqrt_g, rin[k], ci);
-        inv_and_celerity(out[0][k], kp.h_floor, kp.inv_floor, kp.sqrt_g, rout[k], co);
-        am[k] = max_nn(fabs(in[M][k] * rin[k]) + ci, fabs(out[M][k] * rout[k]) + co);
-    }
-#pragma unroll
-    for (int w = 1; w < N; w *= 2)     // pairwise tree: log2(N) dependent maxima
-#pragma unroll
-        for (int k = 0; k + w < N; k += 2 * w) am[k] = max_nn(am[k], am[k + w]);
-    const double amax = am[0];
-    double alpha = amax * kp.inv_r;
-    if (DIR == 1) alpha *= cos_e;
-    if (kp.alpha_mode != 0) alpha = alpha_glob;
-    // the face's lift scale (bd_det) is folded into both halves of f*
-    const double ha = (0.5 * scale) * alpha;
-    const double hs = (0.5 * scale) * (DIR == 0 ? kp.inv_r : cr_e);
-    double fs[3][N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-        const double hi = in[0][k], ui = in[1][k], vi = in[2][k];
-        const double ho = out[0][k], uo = out[1][k], vo = out[2][k];
-        const double gi = hi * hi * kp.half_g, go = ho * ho * kp.half_g;
-        double fi0, fi1, fi2, fo0, fo1, fo2;
-        if (DIR == 0) {
-            const double ui_ = ui * rin[k], vi_ = vi * rin[k];
-            const double uo_ = uo * rout[k], vo_ = vo * rout[k];
-            fi0 = ui; fi1 = fma(ui, ui_, gi); fi2 = ui * vi_;
-            fo0 = uo; fo1 = fma(uo, uo_, go); fo2 = uo * vo_;
-        } else {
-            const double vi_ = vi * rin[k], vo_ = vo * rout[k];
-            fi0 = vi; fi1 = ui * vi_; fi2 = fma(vi, vi_, gi);
-            fo0 = vo; fo1 = uo * vo_; fo2 = fma(vo, vo_, go);
-        }
-        fs[0][k] = fma(hs, fi0 + fo0, -ha * (ho - hi));
-        fs[1][k] = fma(hs, fi1 + fo1, -ha * (uo - ui));
-        fs[2][k] = fma(hs, fi2 + fo2, -ha * (vo - vi));
-    }
-#pragma unroll
-    for (int v = 0; v < 3; ++v) {
-        double g[N];
-        n2m<P, 2>(fs[v], g);
-#pragma unroll
-        for (int b = 0; b < N; ++b) sF[(v * N + b) * ld + col] = g[b];
-    }
-}
-
-// The same flux with the direction a runtime value: the face warp serves
-// its y-faces and the strip's border x-face from ONE inlined copy (the
-// stage kernel is instruction-cache sensitive, measured).
-template <int P>
-__device__ __forceinline__ void face_flux_rt(const double (&in)[3][P + 1], const double (&out)[3][P + 1],
-                                             double *sF, int ld, int col, const StageParams &kp, int dir,
-                                             double cr_e, double cos_e, double alpha_glob, double scale)
-{
-    constexpr int N = P + 1;
-    double rin[N], rout[N], mi[N], mo[N];
-    double am[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-        double ci, co;
-        inv_and_celerity(in[0][k], kp.h_floor, kp.inv_floor, kp.sqrt_g, rin[k], ci);
-        inv_and_celerity(out[0][k], kp.h_floor, kp.inv_floor, kp.sqrt_g, rout[k], co);
-        mi[k] = dir == 0 ? in[1][k] : in[2][k];     // normal momentum
-        mo[k] = dir == 0 ? out[1][k] : out[2][k];
-        am[k] = max_nn(fabs(mi[k] * rin[k]) + ci, fabs(mo[k] * rout[k]) + co);
-    }
-#pragma unroll
-    for (int w = 1; w < N; w *= 2)
-#pragma unroll
-        for (int k = 0; k + w < N; k += 2 * w) am[k] = max_nn(am[k], am[k + w]);
-    double alpha = am[0] * kp.inv_r;
-    if (dir == 1) alpha *= cos_e;
-    if (kp.alpha_mode != 0) alpha = alpha_glob;
-    const double ha = (0.5 * scale) * alpha;
-    const double hs = (0.5 * scale) * (dir == 0 ? kp.inv_r : cr_e);
-    const double sx = dir == 0 ? 1.0 : 0.0, sy = 1.0 - sx;   // where g h^2 / 2 enters
-    double fs[3][N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-        const double hi = in[0][k], ui = in[1][k], vi = in[2][k];
-        const double ho = out[0][k], uo = out[1][k], vo = out[2][k];
-        const double gi = hi * hi * kp.half_g, go = ho * ho * kp.half_g;
-        const double wi = mi[k] * rin[k], wo = mo[k] * rout[k];   // normal velocities
-        const double fi1 = fma(ui, wi, sx * gi), fo1 = fma(uo, wo, sx * go);
-        const double fi2 = fma(vi, wi, sy * gi), fo2 = fma(vo, wo, sy * go);
-        fs[0][k] = fma(hs, mi[k] + mo[k], -ha * (ho - hi));
-        fs[1][k] = fma(hs, fi1 + fo1, -ha * (uo - ui));
-        fs[2][k] = fma(hs, fi2 + fo2, -ha * (vo - vi));
-    }
-#pragma unroll
-    for (int v = 0; v < 3; ++v) {
-        double g[N];
-        n2m<P, 2>(fs[v], g);
-#pragma unroll
-        for (int b = 0; b < N; ++b) sF[(v * N + b) * ld + col] = g[b];
-    }
-}
-
 // Scalars of one face-flux call, by value (no pointer to the kernel
 // parameters may escape into a non-inlined function).
 struct FaceArgs {
@@ -569,12 +450,22 @@ struct FaceArgs {
     double cr_e, cos_e, alpha_glob, scale;
 };
 
-// ONE non-inlined copy of the Rusanov face flux serves the h warp's
-// x-faces, the face warp's y-faces and the strip's border face: traces and
-// result are addressed as (offset, leading dimension, column) in the
-// kernel's dynamic shared memory, so no register array crosses the call.
-// (Three inlined copies cost ~1k SASS instructions of a kernel whose speed
-// tracks its instruction-cache footprint.)
+// Rusanov flux over one face per lane (dg.py:92-119, 385-453): "in" =
+// lower/left element's traces, "out" = upper/right element's, [var][node];
+// local alpha = max over both sides' nodes of (|normal velocity| + c)/R
+// (y-faces scaled by cos of the edge latitude, models.py:254-280), or the
+// global / pinned alpha.  Stored is the face's boundary-integral projection
+// g[var][k'] = scale * sum_k w_k P_k'(x_k) f*[k] (dg.py:206-212, 465-495):
+// both neighbours lift it with their own outward-normal sign and mode
+// parity, so each face is evaluated and projected once.
+// dir 0: x-face, physical flux F; dir 1: y-face, G = cos/R * (...).
+//
+// ONE non-inlined copy serves the h warp's x-faces, the face warp's y-faces
+// and the strip's border face: traces and result are addressed as (offset,
+// leading dimension, column) in the kernel's dynamic shared memory, so no
+// register array crosses the call.  (Three inlined copies cost ~1k SASS
+// instructions of a kernel whose speed tracks its instruction-cache
+// footprint; sF may alias the "out" traces.)
 template <int P>
 __device__ __forceinline__ void face_flux_body(int in_off, int in_ld, int in_col, int out_off, int out_ld,
                                                int out_col, int dst_off, int dst_ld, int dst_col, FaceArgs fa)
@@ -651,16 +542,6 @@ __device__ __forceinline__ void face_flux_call(int in_off, int in_ld, int in_col
         face_flux_noinline<P>(in_off, in_ld, in_col, out_off, out_ld, out_col, dst_off, dst_ld, dst_col, fa);
 }
 
-// traces [3][N] from shared memory: element column `col` of a [3][N][ld] array
-template <int P>
-__device__ __forceinline__ void traces_from_smem(double (&tr)[3][P + 1], const double *s, int ld, int col)
-{
-    constexpr int N = P + 1;
-#pragma unroll
-    for (int v = 0; v < 3; ++v)
-#pragma unroll
-        for (int k = 0; k < N; ++k) tr[v][k] = s[(v * N + k) * ld + col];
-}
 
 // Pointwise flux / source of variable v at the N nodes (qi, qj), qj = 0..N-1
 // (models.py:161-252): F = x-flux (its cx/R goes into the xi weights),
