@@ -543,11 +543,17 @@ __device__ __forceinline__ void face_flux_call(int in_off, int in_ld, int in_col
 }
 
 
-// Pointwise flux / source of variable v at the N nodes (qi, qj), qj = 0..N-1
+// Pointwise flux / source at the N nodes (qi, qj), qj = 0..N-1
 // (models.py:161-252): F = x-flux (its cx/R goes into the xi weights),
-// G = y-flux * cy cos/R, S = source.
-template <int P>
-__device__ __forceinline__ void node_physics(int v, int qi, const double *sU, const double *row, int lane,
+// G = y-flux * cy cos/R, S = source.  MOM = false: the h equation
+// (F = hu, G = hv cos/R, no source).  MOM = true: one branch-free code path
+// for both momentum equations, the variable (is_v: hv) entering only
+// through uniform selects, so the nodes' instructions interleave:
+//   hu: F = hu u + g h^2/2,  G = hu w cos/R,             S = t hv
+//   hv: F = hu w,            G = (hv w + g h^2/2) cos/R, S = -(g h^2/2 sin/R + t hu)
+// with u = hu/hf, w = hv/hf, t = u sin/R + 2 Omega sin cos.
+template <int P, bool MOM>
+__device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU, const double *row, int lane,
                                              const StageParams &kp, double (&F)[P + 1],
                                              double (&G)[P + 1], double (&S)[P + 1])
 {
@@ -560,7 +566,7 @@ __device__ __forceinline__ void node_physics(int v, int qi, const double *sU, co
         const double hu = sU[(1 * NP + q) * kLanes + lane];
         const double hv = sU[(2 * NP + q) * kLanes + lane];
         const double crc = row[RL::CRC + qj];
-        if (v == 0) {
+        if constexpr (!MOM) {
             F[qj] = hu;
             G[qj] = hv * crc;
             S[qj] = 0.0;
@@ -569,28 +575,23 @@ __device__ __forceinline__ void node_physics(int v, int qi, const double *sU, co
             const double r = rcp64(max_pos(h, kp.h_floor));
             const double gh2 = h * h * kp.half_g;
             const double u = hu * r, w = hv * r;
-            const double t = fma(u, row[RL::SRS + qj], row[RL::FCS + qj]);
-            if (v == 1) {
-                F[qj] = fma(hu, u, gh2);
-                G[qj] = hu * w * crc;
-                S[qj] = t * hv;
-            } else {
-                F[qj] = hu * w;
-                G[qj] = fma(hv, w, gh2) * crc;
-                S[qj] = -fma(gh2, row[RL::SRS + qj], t * hu);
-            }
+            const double srs = row[RL::SRS + qj];
+            const double t = fma(u, srs, row[RL::FCS + qj]);
+            F[qj] = fma(hu, is_v ? w : u, is_v ? 0.0 : gh2);
+            G[qj] = fma(is_v ? hv : hu, w, is_v ? gh2 : 0.0) * crc;
+            S[qj] = fma(is_v ? -gh2 : 0.0, srs, t * (is_v ? -hu : hv));
         }
     }
 }
 
 // eta projections of one xi node line: f[b] = sum_qj wP_b F, g[b] = sum_qj (wP'_b G + wP_b S)
-template <int P>
-__device__ __forceinline__ void line_project(int v, const double (&F)[P + 1], const double (&G)[P + 1],
+template <int P, bool MOM>
+__device__ __forceinline__ void line_project(const double (&F)[P + 1], const double (&G)[P + 1],
                                              const double (&S)[P + 1], double (&f)[P + 1],
                                              double (&g)[P + 1])
 {
     n2m<P, 2>(F, f);
-    if (v == 0)
+    if constexpr (!MOM)
         n2m<P, 3>(G, g);
     else
         n2m2<P, 3, 2>(G, S, g);
@@ -600,7 +601,7 @@ __device__ __forceinline__ void line_project(int v, const double (&F)[P + 1], co
 // over pairs of xi node lines (qi, N-1-qi) so that the xi contraction also
 // uses the even/odd split:
 // vol[a][b] = sum_q (cx dphi/dxi F + cy dphi/deta G + cs phi S)[q]
-template <int P>
+template <int P, bool MOM>
 __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const double *sU,
                                        const double *row, int lane, const StageParams &kp)
 {
@@ -615,10 +616,10 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
         double f0[N], g0[N], f1[N], g1[N];
         {
             double F[N], G[N], S[N];
-            node_physics<P>(v, ip, sU, row, lane, kp, F, G, S);
-            line_project<P>(v, F, G, S, f0, g0);
-            node_physics<P>(v, N - 1 - ip, sU, row, lane, kp, F, G, S);
-            line_project<P>(v, F, G, S, f1, g1);
+            node_physics<P, MOM>(v == 2, ip, sU, row, lane, kp, F, G, S);
+            line_project<P, MOM>(F, G, S, f0, g0);
+            node_physics<P, MOM>(v == 2, N - 1 - ip, sU, row, lane, kp, F, G, S);
+            line_project<P, MOM>(F, G, S, f1, g1);
         }
         double pd[N], pp[N];
 #pragma unroll
@@ -638,8 +639,8 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
     }
     if constexpr (N & 1) {   // middle line xi = 0: wP'_a vanishes for even a, wP_a for odd a
         double F[N], G[N], S[N], f[N], g[N];
-        node_physics<P>(v, H, sU, row, lane, kp, F, G, S);
-        line_project<P>(v, F, G, S, f, g);
+        node_physics<P, MOM>(v == 2, H, sU, row, lane, kp, F, G, S);
+        line_project<P, MOM>(F, G, S, f, g);
 #pragma unroll
         for (int b = 0; b < N; ++b)
 #pragma unroll
@@ -1031,7 +1032,10 @@ __global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel
                                            kp.alpha_mode, 0, 0.0, 0.0, alpha_x, kp.bdy});
             }
             double vol[N][N];
-            volume<P>(vol, v, sU, row, lane, kp);
+            if (v == 0)
+                volume<P, false>(vol, v, sU, row, lane, kp);
+            else
+                volume<P, true>(vol, v, sU, row, lane, kp);
             TSTAMP(3);
             __syncthreads();                           // barrier 2
             TSTAMP(4);
