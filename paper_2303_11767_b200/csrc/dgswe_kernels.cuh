@@ -115,8 +115,15 @@ __host__ __device__ inline int row_stride(int p) { return 3 * (p + 1) + 2 + (p +
 //   T(a, N-1-q) = (-1)^(a + PAR) T(a, q)   exactly,
 // PAR = 0 for P and wP, 1 for P' and wP'.  Every 1-D contraction below
 // uses this even/odd split: N adds + N*ceil(N/2) FMA instead of N*N.
+#ifndef DG_SELFLOOR
+#define DG_SELFLOOR 1   // 1/max(h, floor) as rcp(h) + select: the reciprocal starts at once
+#endif
+#ifndef DG_VOL_UNROLL
+#define DG_VOL_UNROLL 0
+#endif
 #ifndef DG_MINB
-#define DG_MINB 4   // resident CTAs per SM the p <= 3 build is register-capped for
+#define DG_MINB 3   // resident CTAs per SM the p <= 3 build is register-capped for (~160 registers;
+                    // 4 CTAs at 128 registers measured 7% slower at C3 once the code was compact)
 #endif
 
 // DG_TIMING builds record per-role phase durations (clock cycles) of every
@@ -572,7 +579,12 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
             S[qj] = 0.0;
         } else {
             const double h = sU[(0 * NP + q) * kLanes + lane];
+#if DG_SELFLOOR
+            const double r0 = rcp64(h);
+            const double r = h >= kp.h_floor ? r0 : kp.inv_floor;
+#else
             const double r = rcp64(max_pos(h, kp.h_floor));
+#endif
             const double gh2 = h * h * kp.half_g;
             const double u = hu * r, w = hv * r;
             const double srs = row[RL::SRS + qj];
@@ -611,7 +623,11 @@ __device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const
     for (int a = 0; a < N; ++a)
 #pragma unroll
         for (int b = 0; b < N; ++b) vol[a][b] = 0.0;
+#if DG_VOL_UNROLL
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
     for (int ip = 0; ip < H; ++ip) {
         double f0[N], g0[N], f1[N], g1[N];
         {
