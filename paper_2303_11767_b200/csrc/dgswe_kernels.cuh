@@ -814,7 +814,7 @@ __device__ __forceinline__ void bottom_traces(const double *ring_row, int lane, 
 }
 
 template <int P, bool HAS_U, bool HAS_Y2, bool EDGE>
-__global__ void __launch_bounds__(kThreads, (P <= 3 ? DG_MINB : 2)) stage_kernel(StageParams kp)
+__global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2)) stage_kernel(StageParams kp)
 {
     constexpr int N = P + 1;
     constexpr int NP = N * N;
