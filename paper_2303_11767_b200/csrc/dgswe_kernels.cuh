@@ -274,7 +274,8 @@ struct Smem {
     static constexpr int HR = HL + 3 * N;                // right-halo L trace [3][N]
     static constexpr int E0 = HR + 3 * N;                // element 0's L trace [3][N] (face warp)
     static constexpr int F0 = E0 + 3 * N;                // face 0 flux [row parity][3][N]
-    static constexpr int ROW = F0 + 6 * N;               // row-table ring, 3 rows
+    static constexpr int HB = F0 + 6 * N;                // next row's neighbour coefficients [2][3][NP]
+    static constexpr int ROW = HB + 6 * NP;              // row-table ring, 3 rows
     static constexpr int MBAR = ROW + 3 * RowLayout<P>::STRIDE;   // 6 mbarriers [slot][var]
     static constexpr int TOTAL = MBAR + 6;
 };
@@ -363,6 +364,14 @@ __device__ __forceinline__ void fence_proxy_async()
 {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+
+// per-lane 8-byte async copies (the face warp's small gathers)
+__device__ __forceinline__ void cp_async8(double *dst, const double *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void prefetch_l2_bulk(const double *src, unsigned bytes)
 {
@@ -748,16 +757,30 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
     return bad;
 }
 
+// Face warp: the neighbour elements' coefficients of row r (left eL =
+// (32 s - 1) mod nx, right eR = (32 s + nvalid) mod nx; 3 vars x nphi each)
+// gathered into shared memory with per-lane async copies, one phase ahead
+// of their use, so no global latency sits on the face warp's critical path.
+template <int P>
+__device__ __forceinline__ void fetch_neighbours(const double *Xrow, int eL, int eR, double *sHB, int lane,
+                                                 long long vstride)
+{
+    constexpr int NP = (P + 1) * (P + 1);
+    for (int t = lane; t < 6 * NP; t += kLanes) {
+        const int side = t / (3 * NP), r = t - side * 3 * NP, vv = r / NP, m = r - vv * NP;
+        const int e = side ? eR : eL;
+        cp_async8(sHB + t, Xrow + (size_t)vv * vstride + (size_t)(e >> 5) * NP * kLanes + m * kLanes + (e & 31));
+    }
+}
+
 // Face warp: the traces of the strip's left border face for one row.
 // Lanes 0..5 each build one trace: (side 0) R trace of the left neighbour
-// element eL = (32 s - 1) mod nx, from global memory (L2-warmed a row
-// ahead); (side 1) L trace of the strip's element 0, from the coefficient
-// ring.  Also the L trace of the right neighbour eR = (32 s + nvalid) mod nx
-// (lanes 6..8), which the h warp needs for the last lane's right face.
+// element, from the gathered coefficients; (side 1) L trace of the strip's
+// element 0, from the coefficient ring.  Also the L trace of the right
+// neighbour (lanes 6..8), which the h warp needs for the last lane's right face.
 template <int P>
-__device__ __forceinline__ void border_traces(const double *Xrow, const double *ring_slot, int eL, int eR,
-                                              double *sHL, double *sE0, double *sHR, int lane,
-                                              long long vstride)
+__device__ __forceinline__ void border_traces(const double *sHB, const double *ring_slot, double *sHL,
+                                              double *sE0, double *sHR, int lane)
 {
     constexpr int N = P + 1;
     constexpr int NP = N * N;
@@ -771,12 +794,11 @@ __device__ __forceinline__ void border_traces(const double *Xrow, const double *
 #pragma unroll
                 for (int b = 0; b < N; ++b) c[a][b] = src[(a * N + b) * kLanes];
         } else {
-            const int e = side == 0 ? eL : eR;
-            const double *src = Xrow + (size_t)v * vstride + (size_t)(e >> 5) * NP * kLanes + (e & 31);
+            const double *src = sHB + ((side == 0 ? 0 : 3) + v) * NP;
 #pragma unroll
             for (int a = 0; a < N; ++a)
 #pragma unroll
-                for (int b = 0; b < N; ++b) c[a][b] = __ldg(src + (a * N + b) * kLanes);
+                for (int b = 0; b < N; ++b) c[a][b] = src[a * N + b];
         }
         double t[N][N];
 #pragma unroll
@@ -930,6 +952,11 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
     // periodic neighbours of the strip's border elements
     const int eL = (strip * kLanes - 1 + nx) % nx;
     const int eR = (strip * kLanes + nvalid) % nx;
+    if (face_warp) {   // the first row's neighbour coefficients (used after the pre-iteration's face)
+        fetch_neighbours<P>(kp.X + (size_t)blockIdx.z * kp.zstride + (size_t)jb * kp.rstride, eL, eR,
+                            smem + SM::HB, lane, kp.vstride);
+        cp_commit();
+    }
     __syncthreads();                               // prologue barrier A
 #ifdef DG_TIMING
     unsigned tacc[6] = {0, 0, 0, 0, 0, 0};
@@ -947,6 +974,19 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             TSTAMP(a);
             if (!pre) __syncthreads();                 // barrier 1 of row it
             TSTAMP(b);
+            if (!pre) {
+                // async gathers, consumed after barrier 2: the next row's neighbour
+                // coefficients and the table of row it+2 (its slot held row it-1)
+                if (it + 1 < je)
+                    fetch_neighbours<P>(kp.X + (size_t)blockIdx.z * kp.zstride + (size_t)(it + 1) * kp.rstride,
+                                        eL, eR, smem + SM::HB, lane, kp.vstride);
+                if (it + 2 <= je && kp.row0 + it + 2 < kp.ny) {
+                    double *dst = sRow + ((k + 2) % 3) * RL::STRIDE;
+                    const double *src = kp.rowtab + (size_t)(kp.row0 + it + 2) * RL::STRIDE;
+                    for (int idx = lane; idx < RL::STRIDE; idx += kLanes) cp_async8(dst + idx, src + idx);
+                }
+                cp_commit();
+            }
             const double *next_tile = ringS + ((k + 1) & 1) * SM::TILE;   // X(it+1)
             if (it + 1 <= last_fetch) {
                 double bt[3][N];
@@ -968,12 +1008,6 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
                                                kp.bdx});
                 }
             }
-            if (!pre && it + 2 <= je && kp.row0 + it + 2 < kp.ny) {
-                // stage the table of row it+2 (its slot held row it-1, no longer read)
-                double *dst = sRow + ((k + 2) % 3) * RL::STRIDE;
-                const double *src = kp.rowtab + (size_t)(kp.row0 + it + 2) * RL::STRIDE;
-                for (int idx = lane; idx < RL::STRIDE; idx += kLanes) dst[idx] = src[idx];
-            }
             TSTAMP(c);
             __syncthreads();                           // barrier 2 of row it (prologue barrier B)
             TSTAMP(d);
@@ -982,20 +1016,10 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
                 fa = fb;
                 fb = t;
             }
+            cp_wait_all();                             // gathers of this row's phase B (and row tables)
+            __syncwarp();
             if (it + 1 < je) {
-                const double *Xrow = kp.X + (size_t)blockIdx.z * kp.zstride + (size_t)(it + 1) * kp.rstride;
-                if (it + 2 < je) {
-                    // warm L2 for the next row's two neighbour elements
-                    for (int t = lane; t < 6 * NP; t += kLanes) {
-                        const int side = t / (3 * NP), r = t - side * 3 * NP, vv = r / NP, m = r - vv * NP;
-                        const int e = side ? eR : eL;
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(
-                            Xrow + kp.rstride + (size_t)vv * kp.vstride + (size_t)(e >> 5) * NP * kLanes +
-                            m * kLanes + (e & 31)));
-                    }
-                }
-                border_traces<P>(Xrow, next_tile, eL, eR, smem + SM::HL, smem + SM::E0, smem + SM::HR,
-                                 lane, kp.vstride);
+                border_traces<P>(smem + SM::HB, next_tile, smem + SM::HL, smem + SM::E0, smem + SM::HR, lane);
                 // every lane computes the same face (uniform control flow, identical stores)
                 face_flux_call<P>(SM::HL, 1, 0, SM::E0, 1, 0, SM::F0 + ((k + 1) & 1) * 3 * N, 1, 0,
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
