@@ -41,6 +41,20 @@
  *   [jlo, jhi) (local); a band's halo rows jlo-1 and jhi must hold the
  *   neighbour band's coefficients whenever they are inside the sphere.
  *
+ * State basis.  The reference's states are modal coefficients, and so are
+ * this ABI's by default.  Inside a step the kernels carry the values at the
+ * (p+1)^2 Gauss nodes instead (u[i][j] in place of mode (a, b), same
+ * layout): with every integral of the reference on that Gauss rule the
+ * nodal form is the same linear operator with a diagonal mass matrix.
+ * dgswe_rk_steps converts u in place before and after its steps; the
+ * single-stage entry points convert around each launch.  A caller that
+ * keeps its states nodal across many stages (a band driver) calls
+ * dgswe_set_basis(ctx, 1) and dgswe_convert itself: then dgswe_rhs,
+ * dgswe_stage*, dgswe_alpha_prepass and dgswe_rk_steps take and return
+ * nodal states unchanged.  dgswe_stage_edge requires the nodal basis.
+ * Diagnostics (dgswe_mass, dgswe_l2_sums) and dgswe_project always use
+ * modal states.
+ *
  * All calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy
  * default) except dgswe_status, which synchronises it.  Return 0 on success,
  * a negative DGSWE_E* code otherwise; dgswe_last_error() describes it.
@@ -55,7 +69,7 @@
 extern "C" {
 #endif
 
-#define DGSWE_ABI_VERSION 2
+#define DGSWE_ABI_VERSION 3
 #define DGSWE_STRIP 32          /* longitude elements per strip block */
 
 /* status bits (dgswe_status) */
@@ -112,6 +126,13 @@ void dgswe_destroy(dgswe_ctx *ctx);
 
 /* elements of one state buffer (nz * nrows * 3 * nstrip * nphi * DGSWE_STRIP) */
 int64_t dgswe_state_elems(const dgswe_ctx *ctx);
+
+/* 0: modal states at the stage entry points (default), 1: nodal. */
+int dgswe_set_basis(dgswe_ctx *ctx, int nodal);
+
+/* In-place change of basis (to_nodal 1: modal -> nodal, 0: back) of local
+ * rows [r0, r1) of every level; padding lanes stay zero. */
+int dgswe_convert(dgswe_ctx *ctx, double *X, int to_nodal, int r0, int r1, void *stream);
 
 /* K = M^-1 (volume - boundary + source)(X) on rows [jlo, jhi). */
 int dgswe_rhs(dgswe_ctx *ctx, const double *X, double *K, void *stream);

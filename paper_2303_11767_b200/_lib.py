@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdgswe_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "dgswe_b200.h")
 
-ABI_VERSION = 2            # DGSWE_ABI_VERSION
+ABI_VERSION = 3            # DGSWE_ABI_VERSION
 STRIP = 32                 # DGSWE_STRIP: longitude elements per strip block
 STATUS_POSITIVITY = 0x1
 STATUS_NONFINITE = 0x2
@@ -51,6 +51,8 @@ SIGNATURES = {
     "dgswe_destroy": (None, [_VP]),
     "dgswe_state_elems": (ctypes.c_int64, [_VP]),
     "dgswe_rhs": (_I, [_VP, _VP, _VP, _VP]),
+    "dgswe_set_basis": (_I, [_VP, _I]),
+    "dgswe_convert": (_I, [_VP, _VP, _I, _I, _I, _VP]),
     "dgswe_stage": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _VP]),
     "dgswe_stage_rows": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _I, _I, _VP]),
     "dgswe_stage_rows2": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _I, _I, _I, _I, _VP]),

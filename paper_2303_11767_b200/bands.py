@@ -195,7 +195,12 @@ class BandOperator:
             _lib.check(self.ctx.lib.dgswe_set_external_alpha(self.ctx.h, 1), "set_external_alpha")
         if transport == "fused" and self.global_alpha:
             raise ValueError("transport 'fused' supports local / pinned alpha only")
-        self.halo = HaloExchange(layout, transport if transport != "fused" else "p2p", group)
+        # the fused transport still exchanges u's halos once per step batch
+        # (begin), over NCCL -- or the host when the group is gloo
+        hx = transport
+        if transport == "fused":
+            hx = "host" if dist.is_initialized() and dist.get_backend(group) == "gloo" else "p2p"
+        self.halo = HaloExchange(layout, hx, group)
         self._owned_mem = []       # (ptr, keep-alive) of library allocations
         self._opened = []          # peer mappings to close
         self._peer_rows = {}       # data_ptr of our buffer -> (south row ptr, north row ptr)
@@ -354,10 +359,41 @@ class BandOperator:
             self.halo.finish()
             self._launch(a, U, b, X, g, Y, tag, L.jlo, L.jhi)
 
+    # Step batches run on nodal values (include/dgswe_b200.h, "State basis"):
+    # begin() converts the owned rows of u in place and refreshes its halo
+    # rows from the neighbours' converted rows, the stages then exchange
+    # nodal rows, end() converts the owned rows back.  Between begin() and
+    # end(), stage() / _launch*() take nodal states.
+    def begin(self, u):
+        L = self.layout
+        self.ctx.convert(u, True, L.jlo, L.jhi)
+        self.ctx.set_basis(True)
+        if L.world > 1:
+            self.halo.start(u)
+            self.halo.finish()
+
+    def end(self, u):
+        L = self.layout
+        self.ctx.convert(u, False, L.jlo, L.jhi)
+        self.ctx.set_basis(False)
+
+    def nodal_steps(self, u, w1, w2, dt, k, tag=0):
+        """k SSPRK3 steps on a nodal u (between begin and end; capturable
+        in a CUDA graph for the fused transport)."""
+        for i in range(k):
+            t = tag + i
+            self.stage(0.0, None, 1.0, u, dt, w1, t)
+            self.stage(0.75, u, 0.25, w1, 0.25 * dt, w2, t)
+            self.stage(1.0 / 3.0, u, 2.0 / 3.0, w2, (2.0 / 3.0) * dt, u, t)
+
+    def ssprk3_steps(self, u, w1, w2, dt, k, tag=0):
+        """k SSPRK3 steps of the band's modal state u (one conversion each way)."""
+        self.begin(u)
+        self.nodal_steps(u, w1, w2, dt, k, tag)
+        self.end(u)
+
     def ssprk3_step(self, u, w1, w2, dt, tag=0):
-        self.stage(0.0, None, 1.0, u, dt, w1, tag)
-        self.stage(0.75, u, 0.25, w1, 0.25 * dt, w2, tag)
-        self.stage(1.0 / 3.0, u, 2.0 / 3.0, w2, (2.0 / 3.0) * dt, u, tag)
+        self.ssprk3_steps(u, w1, w2, dt, 1, tag)
 
     def status(self, reset=True):
         return self.ctx.status(reset)

@@ -51,7 +51,7 @@ struct DevStatus {
     int first_tag;
 };
 
-// global-mode alpha: max over all traces (dg.py:389-411, models.py:271-280)
+// global-mode alpha: max over all traces (dg.py:389-411, models.py:271-280), nodal state
 template <int P>
 __global__ void alpha_prepass_kernel(const double *__restrict__ X, long long zstride,
                                      long long rstride, long long vstride, int nx, int ny, int row0,
@@ -66,25 +66,20 @@ __global__ void alpha_prepass_kernel(const double *__restrict__ X, long long zst
     if (i >= nx || jl >= jhi) return;
     const double *base = X + (size_t)blockIdx.z * zstride + (size_t)jl * rstride;
     const int jg = row0 + jl;
-    double tr[4][3][N];   // L R B T
+    double tr[4][3][N];   // L R B T, from the nodal tile u[i][j]
     for (int v = 0; v < 3; ++v) {
-        double c[N][N];
+        double u[N][N];
         for (int a = 0; a < N; ++a)
             for (int b = 0; b < N; ++b)
-                c[a][b] = base[(size_t)v * vstride + (size_t)(i >> 5) * NP * 32 + (a * N + b) * 32 + (i & 31)];
+                u[a][b] = base[(size_t)v * vstride + (size_t)(i >> 5) * NP * 32 + (a * N + b) * 32 + (i & 31)];
         for (int q = 0; q < N; ++q) {
             double l = 0, r = 0, bo = 0, t = 0;
-            for (int a = 0; a < N; ++a) {
-                double ta = 0, sb = 0, st = 0;
-                for (int b = 0; b < N; ++b) {
-                    ta = fma(c[a][b], dgswe::c_tab[P][0][b][q], ta);
-                    sb = fma((b & 1) ? -1.0 : 1.0, c[a][b], sb);
-                    st += c[a][b];
-                }
-                r += ta;
-                l = fma((a & 1) ? -1.0 : 1.0, ta, l);
-                bo = fma(dgswe::c_tab[P][0][a][q], sb, bo);
-                t = fma(dgswe::c_tab[P][0][a][q], st, t);
+            for (int k = 0; k < N; ++k) {
+                const double lo = dgswe::c_nod[P].lm[k], hi = dgswe::c_nod[P].lm[N - 1 - k];
+                l = fma(lo, u[k][q], l);
+                r = fma(hi, u[k][q], r);
+                bo = fma(lo, u[q][k], bo);
+                t = fma(hi, u[q][k], t);
             }
             tr[0][v][q] = l;
             tr[1][v][q] = r;
@@ -135,11 +130,11 @@ struct GraphKey {
     int order;
     double *u, *w1, *w2, *w3;
     double dt;
-    int nsteps, check_mean;
+    int nsteps, check_mean, basis;
     bool operator<(const GraphKey &o) const
     {
-        return std::tie(order, u, w1, w2, w3, dt, nsteps, check_mean) <
-               std::tie(o.order, o.u, o.w1, o.w2, o.w3, o.dt, o.nsteps, o.check_mean);
+        return std::tie(order, u, w1, w2, w3, dt, nsteps, check_mean, basis) <
+               std::tie(o.order, o.u, o.w1, o.w2, o.w3, o.dt, o.nsteps, o.check_mean, o.basis);
     }
 };
 
@@ -168,6 +163,12 @@ struct dgswe_ctx {
     size_t diag_bytes = 0;
     // derived scalars
     double inv_r, inv_r_cx, half_g, bdx, bdy;
+    double dx[dgswe::kMaxP + 1][dgswe::kMaxP + 1];   // inv_r_cx * dh (StageParams::dx)
+    // state basis of the stage entry points: 0 modal (the reference's
+    // coefficients; converted around every launch), 1 nodal (as stored
+    // inside dgswe_rk_steps; dgswe_set_basis)
+    int basis = 0;
+    double *scr[3] = {nullptr, nullptr, nullptr};   // modal-basis staging (X, U, A)
 };
 
 namespace {
@@ -272,7 +273,10 @@ int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, c
     return DGSWE_OK;
 }
 
-// Y = a U + b X + g RHS(X) [, Y2 = A + g2 RHS(X)] on local rows [r0, r1)
+int alpha_prepass_nodal(dgswe_ctx *c, const double *X, cudaStream_t s);
+
+// Y = a U + b X + g RHS(X) [, Y2 = A + g2 RHS(X)] on local rows [r0, r1),
+// every state in the nodal basis
 int launch_stage(dgswe_ctx *c, double a, const double *U, double b, const double *X, double g,
                  double *Y, const double *A, double g2, double *Y2, int tag, int r0, int r1,
                  int check_finite, int check_mean, cudaStream_t s, int r2 = 0, int r3 = 0)
@@ -309,6 +313,7 @@ int launch_stage(dgswe_ctx *c, double a, const double *U, double b, const double
     kp.a = a;
     kp.b = b;
     kp.g = g;
+    memcpy(kp.dx, c->dx, sizeof kp.dx);
     kp.rowtab = c->rowtab;
     kp.inv_r = c->inv_r;
     kp.inv_r_cx = c->inv_r_cx;
@@ -340,7 +345,7 @@ int launch_stage(dgswe_ctx *c, double a, const double *U, double b, const double
         kp.stage_ctr = c->stage_ctr;
     }
     if (c->cfg.alpha_mode == DGSWE_ALPHA_GLOBAL && !c->external_alpha) {
-        int rc = dgswe_alpha_prepass(c, X, s);
+        int rc = alpha_prepass_nodal(c, X, s);
         if (rc) return rc;
     }
     switch (c->cfg.p) {
@@ -367,6 +372,93 @@ int launch_alpha_p(dgswe_ctx *c, const double *X, cudaStream_t s)
     CUDA_TRY(cudaGetLastError());
     c->launches += 1;
     return DGSWE_OK;
+}
+
+int alpha_prepass_nodal(dgswe_ctx *ctx, const double *X, cudaStream_t s)
+{
+    CUDA_TRY(cudaMemsetAsync(ctx->alpha, 0, 2 * sizeof(double), s));
+    switch (ctx->cfg.p) {
+    case 0: return launch_alpha_p<0>(ctx, X, s);
+    case 1: return launch_alpha_p<1>(ctx, X, s);
+    case 2: return launch_alpha_p<2>(ctx, X, s);
+    case 3: return launch_alpha_p<3>(ctx, X, s);
+    case 4: return launch_alpha_p<4>(ctx, X, s);
+    case 5: return launch_alpha_p<5>(ctx, X, s);
+    case 6: return launch_alpha_p<6>(ctx, X, s);
+    default: return fail(DGSWE_EUNSUPPORTED, "degree not supported");
+    }
+}
+
+template <int P>
+int convert_p(dgswe_ctx *c, const double *in, double *out, bool to_nodal, int r0, int r1, cudaStream_t s)
+{
+    dim3 grid(c->nstrip, r1 - r0, c->cfg.nz);
+    if (to_nodal)
+        dgswe::convert_kernel<P, true><<<grid, 96, 0, s>>>(in, out, c->zstride, c->rstride, c->vstride, r0);
+    else
+        dgswe::convert_kernel<P, false><<<grid, 96, 0, s>>>(in, out, c->zstride, c->rstride, c->vstride, r0);
+    CUDA_TRY(cudaGetLastError());
+    c->launches += 1;
+    return DGSWE_OK;
+}
+
+// change of basis of local rows [r0, r1), every level (in may equal out)
+int convert_rows(dgswe_ctx *c, const double *in, double *out, bool to_nodal, int r0, int r1, cudaStream_t s)
+{
+    if (r1 <= r0) return DGSWE_OK;
+    switch (c->cfg.p) {
+    case 0: return convert_p<0>(c, in, out, to_nodal, r0, r1, s);
+    case 1: return convert_p<1>(c, in, out, to_nodal, r0, r1, s);
+    case 2: return convert_p<2>(c, in, out, to_nodal, r0, r1, s);
+    case 3: return convert_p<3>(c, in, out, to_nodal, r0, r1, s);
+    case 4: return convert_p<4>(c, in, out, to_nodal, r0, r1, s);
+    case 5: return convert_p<5>(c, in, out, to_nodal, r0, r1, s);
+    case 6: return convert_p<6>(c, in, out, to_nodal, r0, r1, s);
+    default: return fail(DGSWE_EUNSUPPORTED, "degree not supported");
+    }
+}
+
+int scratch_state(dgswe_ctx *c, int k, double **out)
+{
+    if (!c->scr[k]) CUDA_TRY(cudaMalloc(&c->scr[k], sizeof(double) * (size_t)c->zstride * c->cfg.nz));
+    *out = c->scr[k];
+    return DGSWE_OK;
+}
+
+// A stage through the public entry points: in the modal basis the inputs
+// are converted into staging buffers (all local rows: X's halo rows are
+// read), the nodal kernel writes Y / Y2, whose computed rows are converted
+// back in place.  U may alias Y and A may alias Y2, as in launch_stage.
+int api_stage(dgswe_ctx *c, double a, const double *U, double b, const double *X, double g, double *Y,
+              const double *A, double g2, double *Y2, int tag, int r0, int r1, cudaStream_t s, int r2 = 0,
+              int r3 = 0)
+{
+    if (c->basis) return launch_stage(c, a, U, b, X, g, Y, A, g2, Y2, tag, r0, r1, 0, 0, s, r2, r3);
+    if (!X || !Y) return fail(DGSWE_EINVAL, "null state pointer");
+    if (X == Y || X == Y2) return fail(DGSWE_EINVAL, "outputs must not alias the stage input");
+    if (Y2 && (Y2 == Y || !A)) return fail(DGSWE_EINVAL, "second output needs its own buffer and an addend");
+    if (a != 0.0 && !U) return fail(DGSWE_EINVAL, "U is required when a != 0");
+    if (r0 < c->cfg.jlo || r1 > c->cfg.jhi || r0 > r1)
+        return fail(DGSWE_EINVAL, "row range [%d,%d) outside [%d,%d)", r0, r1, c->cfg.jlo, c->cfg.jhi);
+    const int nr = c->cfg.nrows;
+    double *xs = nullptr, *us = nullptr, *as = nullptr;
+    int rc = scratch_state(c, 0, &xs);
+    if (!rc) rc = convert_rows(c, X, xs, true, 0, nr, s);
+    if (!rc && a != 0.0) {
+        rc = scratch_state(c, 1, &us);
+        if (!rc) rc = convert_rows(c, U, us, true, r0, r3 > r2 ? r3 : r1, s);
+    }
+    if (!rc && Y2) {
+        rc = scratch_state(c, 2, &as);
+        if (!rc) rc = convert_rows(c, A, as, true, r0, r3 > r2 ? r3 : r1, s);
+    }
+    if (!rc) rc = launch_stage(c, a, us, b, xs, g, Y, as, g2, Y2, tag, r0, r1, 0, 0, s, r2, r3);
+    for (double *o : {Y, Y2}) {
+        if (rc || !o) continue;
+        rc = convert_rows(c, o, o, false, r0, r1, s);
+        if (!rc && r3 > r2) rc = convert_rows(c, o, o, false, r2, r3, s);
+    }
+    return rc;
 }
 
 }  // namespace
@@ -437,10 +529,34 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
             tab[3][a][q] = w * D;
         }
     cudaError_t e = cudaMemcpyToSymbol(dgswe::c_tab, tab, sizeof tab, sizeof tab * c.p);
+    // nodal tables (dgswe_kernels.cuh NodTab) from the Legendre ones, in
+    // long double: l_i(x) = sum_a (2a+1)/2 w_i P_a(x_i) P_a(x) (the Gauss
+    // rule projects the degree-p Lagrange polynomial exactly)
+    dgswe::NodTab nt;
+    memset(&nt, 0, sizeof nt);
+    for (int i = 0; i < n; ++i) {
+        const long double wi = t->weights[i];
+        long double lm = 0.0L;
+        for (int a = 0; a < n; ++a)
+            lm += 0.5L * (2 * a + 1) * wi * t->leg[a * n + i] * ((a & 1) ? -1.0L : 1.0L);
+        nt.lm[i] = (double)lm;
+        nt.mu[i] = (double)(lm / wi);
+        nt.w[i] = (double)wi;
+        for (int k = 0; k < n; ++k) {
+            long double d = 0.0L;   // w_k l_i'(x_k) / w_i
+            for (int a = 0; a < n; ++a)
+                d += 0.5L * (2 * a + 1) * (long double)t->leg[a * n + i] * t->weights[k] * t->dleg[a * n + k];
+            nt.dh[i][k] = (double)d;
+        }
+    }
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(dgswe::c_nod, &nt, sizeof nt, sizeof nt * c.p);
     if (e != cudaSuccess) {
         delete ctx;
         return fail(DGSWE_ECUDA, "constant upload: %s", cudaGetErrorString(e));
     }
+
+    for (int i = 0; i <= dgswe::kMaxP; ++i)
+        for (int k = 0; k <= dgswe::kMaxP; ++k) ctx->dx[i][k] = ctx->inv_r_cx * nt.dh[i][k];
 
     // per-row tables (global rows), layout RowLayout<P>
     const int rs = dgswe::row_stride(c.p);
@@ -457,6 +573,9 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
         const double *M = t->minv + (size_t)j * ctx->nphi * ctx->nphi;
         for (int b = 0; b < n; ++b)
             for (int bb = 0; bb < n; ++bb) r[3 * n + 2 + b * n + bb] = M[(size_t)b * ctx->nphi + bb];
+        // nodal mass 1 / (determ cos_j) (the w_i w_j factors live in dh, mu)
+        for (int q = 0; q < n; ++q)
+            r[3 * n + 2 + n * n + q] = 1.0 / (determ * (t->cos_r_int[j * n + q] * c.radius));
     }
     bool ok = cudaMalloc(&ctx->rowtab, rt.size() * sizeof(double)) == cudaSuccess &&
               cudaMalloc(&ctx->cos_edge, (c.ny + 1) * sizeof(double)) == cudaSuccess &&
@@ -487,6 +606,7 @@ void dgswe_destroy(dgswe_ctx *ctx)
     cudaFree(ctx->alpha);
     cudaFree(ctx->status);
     cudaFree(ctx->diag);
+    for (double *p : ctx->scr) cudaFree(p);
     delete ctx;
 }
 
@@ -498,25 +618,23 @@ int64_t dgswe_state_elems(const dgswe_ctx *ctx)
 int dgswe_rhs(dgswe_ctx *ctx, const double *X, double *K, void *stream)
 {
     if (!ctx) return fail(DGSWE_EINVAL, "null context");
-    return launch_stage(ctx, 0.0, nullptr, 0.0, X, 1.0, K, nullptr, 0.0, nullptr, 0, ctx->cfg.jlo,
-                        ctx->cfg.jhi, 0, 0,
-                        (cudaStream_t)stream);
+    return api_stage(ctx, 0.0, nullptr, 0.0, X, 1.0, K, nullptr, 0.0, nullptr, 0, ctx->cfg.jlo, ctx->cfg.jhi,
+                     (cudaStream_t)stream);
 }
 
 int dgswe_stage(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g,
                 double *Y, int tag, void *stream)
 {
     if (!ctx) return fail(DGSWE_EINVAL, "null context");
-    return launch_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, ctx->cfg.jlo, ctx->cfg.jhi, 0, 0,
-                        (cudaStream_t)stream);
+    return api_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, ctx->cfg.jlo, ctx->cfg.jhi,
+                     (cudaStream_t)stream);
 }
 
 int dgswe_stage_rows(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g,
                      double *Y, int tag, int r0, int r1, void *stream)
 {
     if (!ctx) return fail(DGSWE_EINVAL, "null context");
-    return launch_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, r0, r1, 0, 0,
-                        (cudaStream_t)stream);
+    return api_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, r0, r1, (cudaStream_t)stream);
 }
 
 int dgswe_set_exchange(dgswe_ctx *ctx, long long peer_zstride_s, unsigned long long *peer_count_s,
@@ -538,6 +656,7 @@ int dgswe_stage_edge(dgswe_ctx *ctx, double a, const double *U, double b, const 
 {
     if (!ctx) return fail(DGSWE_EINVAL, "null context");
     if (!ctx->stage_ctr) return fail(DGSWE_EINVAL, "dgswe_set_exchange first");
+    if (!ctx->basis) return fail(DGSWE_EINVAL, "edge launches take nodal states (dgswe_set_basis)");
     const int lo = ctx->cfg.jlo, hi = ctx->cfg.jhi;
     ctx->edge_row[0] = peer_row_s;
     ctx->edge_row[1] = peer_row_n;
@@ -592,15 +711,14 @@ int dgswe_stage_rows2(dgswe_ctx *ctx, double a, const double *U, double b, const
                       double *Y, int tag, int r0, int r1, int r2, int r3, void *stream)
 {
     if (!ctx) return fail(DGSWE_EINVAL, "null context");
-    return launch_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, r0, r1, 0, 0,
-                        (cudaStream_t)stream, r2, r3);
+    return api_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, r0, r1, (cudaStream_t)stream, r2, r3);
 }
 
 int dgswe_stage2(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g,
                  double *Y, const double *A, double g2, double *Y2, int tag, int r0, int r1, void *stream)
 {
     if (!ctx) return fail(DGSWE_EINVAL, "null context");
-    return launch_stage(ctx, a, U, b, X, g, Y, A, g2, Y2, tag, r0, r1, 0, 0, (cudaStream_t)stream);
+    return api_stage(ctx, a, U, b, X, g, Y, A, g2, Y2, tag, r0, r1, (cudaStream_t)stream);
 }
 
 int dgswe_axpy(dgswe_ctx *ctx, double coef, const double *x, double *y, int check_finite, int tag,
@@ -623,17 +741,25 @@ int dgswe_alpha_prepass(dgswe_ctx *ctx, const double *X, void *stream)
 {
     if (!ctx || !X) return fail(DGSWE_EINVAL, "null argument");
     cudaStream_t s = (cudaStream_t)stream;
-    CUDA_TRY(cudaMemsetAsync(ctx->alpha, 0, 2 * sizeof(double), s));
-    switch (ctx->cfg.p) {
-    case 0: return launch_alpha_p<0>(ctx, X, s);
-    case 1: return launch_alpha_p<1>(ctx, X, s);
-    case 2: return launch_alpha_p<2>(ctx, X, s);
-    case 3: return launch_alpha_p<3>(ctx, X, s);
-    case 4: return launch_alpha_p<4>(ctx, X, s);
-    case 5: return launch_alpha_p<5>(ctx, X, s);
-    case 6: return launch_alpha_p<6>(ctx, X, s);
-    default: return fail(DGSWE_EUNSUPPORTED, "degree not supported");
-    }
+    if (ctx->basis) return alpha_prepass_nodal(ctx, X, s);
+    double *xs = nullptr;
+    int rc = scratch_state(ctx, 0, &xs);
+    if (!rc) rc = convert_rows(ctx, X, xs, true, 0, ctx->cfg.nrows, s);
+    return rc ? rc : alpha_prepass_nodal(ctx, xs, s);
+}
+
+int dgswe_set_basis(dgswe_ctx *ctx, int nodal)
+{
+    if (!ctx) return fail(DGSWE_EINVAL, "null context");
+    ctx->basis = nodal ? 1 : 0;
+    return DGSWE_OK;
+}
+
+int dgswe_convert(dgswe_ctx *ctx, double *X, int to_nodal, int r0, int r1, void *stream)
+{
+    if (!ctx || !X) return fail(DGSWE_EINVAL, "null argument");
+    if (r0 < 0 || r1 > ctx->cfg.nrows || r0 > r1) return fail(DGSWE_EINVAL, "bad row range [%d,%d)", r0, r1);
+    return convert_rows(ctx, X, X, to_nodal != 0, r0, r1, (cudaStream_t)stream);
 }
 
 double *dgswe_alpha_buffer(dgswe_ctx *ctx) { return ctx ? ctx->alpha : nullptr; }
@@ -657,6 +783,10 @@ static int enqueue_rk(dgswe_ctx *ctx, int order, double *u, double *w1, double *
                       int nsteps, int check_mean, cudaStream_t s)
 {
     const int lo = ctx->cfg.jlo, hi = ctx->cfg.jhi;
+    if (!ctx->basis) {   // the steps run on the nodal values; u is converted in place around them
+        int rc = convert_rows(ctx, u, u, true, 0, ctx->cfg.nrows, s);
+        if (rc) return rc;
+    }
     for (int k = 0; k < nsteps; ++k) {
         int rc = DGSWE_OK;
         switch (order) {
@@ -698,6 +828,7 @@ static int enqueue_rk(dgswe_ctx *ctx, int order, double *u, double *w1, double *
     if (order == 1 && (nsteps & 1))
         CUDA_TRY(cudaMemcpyAsync(u, w1, sizeof(double) * (size_t)ctx->zstride * ctx->cfg.nz,
                                  cudaMemcpyDeviceToDevice, s));
+    if (!ctx->basis) return convert_rows(ctx, u, u, false, 0, ctx->cfg.nrows, s);
     return DGSWE_OK;
 }
 
@@ -715,7 +846,7 @@ int dgswe_rk_steps(dgswe_ctx *ctx, int order, double *u, double *w1, double *w2,
         return fail(DGSWE_EINVAL, "fused RK steps need a single-band context; use dgswe_stage per band");
     cudaStream_t s = (cudaStream_t)stream;
     if (getenv("DGSWE_NO_GRAPH")) return enqueue_rk(ctx, order, u, w1, w2, w3, dt, nsteps, check_mean, s);
-    GraphKey key{order, u, w1, w2, w3, dt, nsteps, check_mean};
+    GraphKey key{order, u, w1, w2, w3, dt, nsteps, check_mean, ctx->basis};
     auto it = ctx->graphs.find(key);
     if (it == ctx->graphs.end()) {
         if (ctx->graphs.size() >= 8) {
@@ -748,7 +879,7 @@ int dgswe_rk_steps(dgswe_ctx *ctx, int order, double *u, double *w1, double *w2,
     }
     CUDA_TRY(cudaGraphLaunch(it->second, s));
     const int per_stage = 1 + (ctx->cfg.alpha_mode == DGSWE_ALPHA_GLOBAL ? 1 : 0);
-    ctx->launches += (long long)stages_of(order) * nsteps * per_stage;
+    ctx->launches += (long long)stages_of(order) * nsteps * per_stage + (ctx->basis ? 0 : 2);
     return DGSWE_OK;
 }
 

@@ -60,6 +60,7 @@ struct StageParams {
     int nchunk1;              // chunks of the first range; later chunks cover [j_begin2, j_end2)
     int j_begin2, j_end2;
     double a, b, g;       // Y = a U + b X + g RHS(X)
+    double dx[kMaxP + 1][kMaxP + 1];   // (1/R)(determ/bd_det_x) dh: the xi derivative of F
     const double *rowtab; // per global row, see RowLayout
     double inv_r;         // 1/R
     double inv_r_cx;      // (1/R) * determ/bd_det_x
@@ -91,7 +92,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     return v;
 }
 
-// per-row table layout (doubles): crc[n] srs[n] fcs[n] cr_b cos_b T[n][n]
+// per-row table layout (doubles): crc[n] srs[n] fcs[n] cr_b cos_b T[n][n] rj[n]
 template <int P>
 struct RowLayout {
     static constexpr int N = P + 1;
@@ -100,11 +101,12 @@ struct RowLayout {
     static constexpr int FCS = 2 * N;
     static constexpr int CRB = 3 * N;
     static constexpr int COSB = 3 * N + 1;
-    static constexpr int T = 3 * N + 2;
-    static constexpr int STRIDE = 3 * N + 2 + N * N;
+    static constexpr int T = 3 * N + 2;      // theta block of M^-1 (modal; device IC projection)
+    static constexpr int RJ = T + N * N;     // 1 / (determ cos_j): the nodal mass
+    static constexpr int STRIDE = RJ + N;
 };
 
-__host__ __device__ inline int row_stride(int p) { return 3 * (p + 1) + 2 + (p + 1) * (p + 1); }
+__host__ __device__ inline int row_stride(int p) { return 4 * (p + 1) + 2 + (p + 1) * (p + 1); }
 
 #define LEG(a, q) c_tab[P][0][a][q]
 #define WP(a, q) c_tab[P][2][a][q]
@@ -139,119 +141,37 @@ __device__ unsigned long long g_timing[4][7];
 #define TACC(i, d)
 #endif
 
-template <int TAB>
-struct TabPar {
-    static constexpr int v = (TAB == 1 || TAB == 3) ? 1 : 0;
+// Nodal (Gauss-Lagrange) tables of degree P, built on the host from the
+// Legendre tables (dgswe_b200.cu, dgswe_create): with l_i the Lagrange
+// polynomial of Gauss node x_i,
+//   lm[i]    = l_i(-1)                (l_i(+1) = l_{N-1-i}(-1))
+//   mu[i]    = l_i(-1) / w_i          (boundary lift of a face value)
+//   dh[i][k] = w_k l_i'(x_k) / w_i    (weak derivative, W^-1 D^T W)
+//   w[i]     = w_i
+// The state is carried at the (p+1)^2 Gauss nodes inside a step: the
+// reference's modal scheme with every integral on the same (p+1)-point Gauss
+// rule (dg.py:186-213, basis.py:159-177) is, in the Lagrange basis of those
+// nodes, the same linear operator with a diagonal mass matrix
+// determ w_i w_j cos_j (exact algebra; only the rounding differs).
+struct NodTab {
+    double lm[kMaxP + 1];
+    double mu[kMaxP + 1];
+    double dh[kMaxP + 1][kMaxP + 1];
+    double w[kMaxP + 1];
 };
+__constant__ NodTab c_nod[kMaxP + 1];
 
-// sum over a = S, S+2, ... < N of T(a, q) in[a]
-template <int P, int TAB, int S>
-__device__ __forceinline__ double dot_step2(const double (&in)[P + 1], int q)
-{
-    double acc = c_tab[P][TAB][S][q] * in[S];
-#pragma unroll
-    for (int a = S + 2; a < P + 1; a += 2) acc = fma(c_tab[P][TAB][a][q], in[a], acc);
-    return acc;
-}
-
-// modes -> nodes: out[q] = sum_a T(a, q) in[a]
-template <int P, int TAB>
-__device__ __forceinline__ void m2n(const double (&in)[P + 1], double (&out)[P + 1])
-{
-    constexpr int N = P + 1, H = N / 2, PAR = TabPar<TAB>::v;
-#pragma unroll
-    for (int q = 0; q < H; ++q) {
-        const double e = dot_step2<P, TAB, 0>(in, q);
-        const double o = dot_step2<P, TAB, 1>(in, q);
-        out[q] = e + o;
-        out[N - 1 - q] = PAR == 0 ? e - o : o - e;
-    }
-    if constexpr (N & 1) {   // middle node x = 0: only (a + PAR) even survives
-        if constexpr (PAR == 0)
-            out[H] = dot_step2<P, TAB, 0>(in, H);
-        else if constexpr (N > 1)
-            out[H] = dot_step2<P, TAB, 1>(in, H);
-        else
-            out[H] = 0.0;
-    }
-}
-
-// node-pair folds of a nodal line: ip[q] = x[q] + x[N-1-q], im[q] = x[q] - x[N-1-q]
-template <int P>
-__device__ __forceinline__ void fold(const double (&x)[P + 1], double (&ip)[(P + 1) / 2],
-                                     double (&im)[(P + 1) / 2])
+// value at xi = -1 (LO) or +1 of the nodal line x
+template <int P, bool LO>
+__device__ __forceinline__ double line_trace(const double (&x)[P + 1])
 {
     constexpr int N = P + 1;
+    double s = c_nod[P].lm[LO ? 0 : N - 1] * x[0];
 #pragma unroll
-    for (int q = 0; q < N / 2; ++q) {
-        ip[q] = x[q] + x[N - 1 - q];
-        im[q] = x[q] - x[N - 1 - q];
-    }
+    for (int i = 1; i < N; ++i) s = fma(c_nod[P].lm[LO ? i : N - 1 - i], x[i], s);
+    return s;
 }
 
-// nodes -> modes: out[b] = sum_q T(b, q) x[q], from the folds of x
-template <int P, int TAB>
-__device__ __forceinline__ double n2m_one(const double *ip, const double *im, const double (&x)[P + 1],
-                                          int b)
-{
-    constexpr int N = P + 1, H = N / 2, PAR = TabPar<TAB>::v;
-    const bool sym = ((b + PAR) & 1) == 0;
-    double acc = 0.0;
-    if constexpr (H > 0) {
-        acc = c_tab[P][TAB][b][0] * (sym ? ip[0] : im[0]);
-#pragma unroll
-        for (int q = 1; q < H; ++q) acc = fma(c_tab[P][TAB][b][q], sym ? ip[q] : im[q], acc);
-        if constexpr (N & 1)
-            if (sym) acc = fma(c_tab[P][TAB][b][H], x[H], acc);
-    } else {
-        if (sym) acc = c_tab[P][TAB][b][0] * x[0];
-    }
-    return acc;
-}
-
-template <int P, int TAB>
-__device__ __forceinline__ void n2m(const double (&x)[P + 1], double (&out)[P + 1])
-{
-    constexpr int N = P + 1, H = N / 2;
-    double ip[H > 0 ? H : 1], im[H > 0 ? H : 1];
-    if constexpr (H > 0) fold<P>(x, ip, im);
-#pragma unroll
-    for (int b = 0; b < N; ++b) out[b] = n2m_one<P, TAB>(ip, im, x, b);
-}
-
-// out[b] = sum_q TA(b, q) x[q] + TB(b, q) y[q] in one accumulation chain
-template <int P, int TA, int TB>
-__device__ __forceinline__ void n2m2(const double (&x)[P + 1], const double (&y)[P + 1],
-                                     double (&out)[P + 1])
-{
-    constexpr int N = P + 1, H = N / 2;
-    double xp[H > 0 ? H : 1], xm[H > 0 ? H : 1], yp[H > 0 ? H : 1], ym[H > 0 ? H : 1];
-    if constexpr (H > 0) {
-        fold<P>(x, xp, xm);
-        fold<P>(y, yp, ym);
-    }
-#pragma unroll
-    for (int b = 0; b < N; ++b) {
-        const bool sx = ((b + TabPar<TA>::v) & 1) == 0, sy = ((b + TabPar<TB>::v) & 1) == 0;
-        double acc = 0.0;
-        bool first = true;
-#pragma unroll
-        for (int q = 0; q < H; ++q) {
-            acc = first ? c_tab[P][TA][b][q] * (sx ? xp[q] : xm[q])
-                        : fma(c_tab[P][TA][b][q], sx ? xp[q] : xm[q], acc);
-            first = false;
-            acc = fma(c_tab[P][TB][b][q], sy ? yp[q] : ym[q], acc);
-        }
-        if constexpr (N & 1) {
-            if (sx) {
-                acc = first ? c_tab[P][TA][b][H] * x[H] : fma(c_tab[P][TA][b][H], x[H], acc);
-                first = false;
-            }
-            if (sy) acc = first ? c_tab[P][TB][b][H] * y[H] : fma(c_tab[P][TB][b][H], y[H], acc);
-        }
-        out[b] = acc;
-    }
-}
 
 template <int P>
 struct Smem {
@@ -262,13 +182,12 @@ struct Smem {
     // offsets in doubles
     static constexpr int XR0 = 0;                        // coefficient ring slot 0 [var][mode][lane]
     static constexpr int XR1 = XR0 + TILE;               // slot 1
-    static constexpr int U = XR1 + TILE;                 // nodal values [3][NP][32]
-    static constexpr int XL = U + TILE;                  // [3][N][32]
+    static constexpr int XL = XR1 + TILE;                // L traces [3][N][32]
     static constexpr int XRT = XL + TR;
     static constexpr int TT = XRT + TR;                  // top traces of current row
-    static constexpr int FX = TT + TR;                   // x-face fluxes [3][N][33], face f left of lane f
+    static constexpr int FX = TT + TR;                   // x-face fluxes [3][N][32], column c = right face of lane c
                                                          // (face 0 lives in F0, double-buffered)
-    static constexpr int FY0 = FX + 3 * N * (kLanes + 1);   // y-face flux buffers [3][N][32]
+    static constexpr int FY0 = FX + TR;                  // y-face flux buffers [3][N][32]
     static constexpr int FY1 = FY0 + TR;
     static constexpr int HL = FY1 + TR;                  // left-halo R trace [3][N]
     static constexpr int HR = HL + 3 * N;                // right-halo L trace [3][N]
@@ -378,29 +297,6 @@ __device__ __forceinline__ void prefetch_l2_bulk(const double *src, unsigned byt
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
-// bottom (sign -1) or top (sign +1) trace at the n edge nodes from modes
-template <int P, bool TOP>
-__device__ __forceinline__ void ytrace(const double (&c)[P + 1][P + 1], double (&tr)[P + 1])
-{
-    constexpr int N = P + 1;
-    double s[N];
-#pragma unroll
-    for (int a = 0; a < N; ++a) {
-        double e = c[a][0], o = 0.0;
-#pragma unroll
-        for (int b = 2; b < N; b += 2) e += c[a][b];
-        if constexpr (N > 1) {
-            o = c[a][1];
-#pragma unroll
-            for (int b = 3; b < N; b += 2) o += c[a][b];
-            s[a] = TOP ? e + o : e - o;
-        } else {
-            s[a] = e;
-        }
-    }
-    m2n<P, 0>(s, tr);
-}
-
 template <int P>
 __device__ __forceinline__ void tile_read(double (&c)[P + 1][P + 1], const double *s, int lane)
 {
@@ -411,52 +307,57 @@ __device__ __forceinline__ void tile_read(double (&c)[P + 1][P + 1], const doubl
         for (int b = 0; b < N; ++b) c[a][b] = s[(a * N + b) * kLanes + lane];
 }
 
-// Interior nodal values and L/R/T traces of one variable -> shared memory.
+// bottom (eta = -1, LO) or top trace of a nodal tile u[i][j]: per xi node i
+template <int P, bool LO>
+__device__ __forceinline__ void ytrace(const double (&u)[P + 1][P + 1], double (&tr)[P + 1])
+{
+#pragma unroll
+    for (int i = 0; i < P + 1; ++i) tr[i] = line_trace<P, LO>(u[i]);
+}
+
+// left (xi = -1, LO) or right trace of a nodal tile: per eta node j
+template <int P, bool LO>
+__device__ __forceinline__ void xtrace(const double (&u)[P + 1][P + 1], double (&tr)[P + 1])
+{
+    constexpr int N = P + 1;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        double col[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) col[i] = u[i][j];
+        tr[j] = line_trace<P, LO>(col);
+    }
+}
+
+// L/R/T traces of one variable's nodal tile -> shared memory (+ positivity
+// of the h nodes and traces when `check`)
 template <int P>
-__device__ __forceinline__ unsigned eval_row(const double (&c)[P + 1][P + 1], double *sU, double *sXL,
-                                             double *sXR, double *sT, int lane, bool check)
+__device__ __forceinline__ unsigned traces_row(const double (&u)[P + 1][P + 1], double *sXL, double *sXR,
+                                               double *sT, int lane, bool check)
 {
     constexpr int N = P + 1;
     unsigned bad = 0;
-    double t[N][N];   // t[a][qj] = sum_b c[a][b] P_b(x_qj)
-#pragma unroll
-    for (int a = 0; a < N; ++a) m2n<P, 0>(c[a], t[a]);
-#pragma unroll
-    for (int q = 0; q < N; ++q) {   // xi = -1 / +1 traces: parity of a
-        double e = t[0][q], o = 0.0;
-#pragma unroll
-        for (int a = 2; a < N; a += 2) e += t[a][q];
-        if constexpr (N > 1) {
-            o = t[1][q];
-#pragma unroll
-            for (int a = 3; a < N; a += 2) o += t[a][q];
-        }
-        const double l = e - o, r = e + o;
-        sXL[q * kLanes + lane] = l;
-        sXR[q * kLanes + lane] = r;
-        if (check) bad |= !(l > 0.0) | !(r > 0.0);
-    }
-    double tt[N];
-    ytrace<P, true>(c, tt);
+    double l[N], r[N], t[N];
+    xtrace<P, true>(u, l);
+    xtrace<P, false>(u, r);
+    ytrace<P, false>(u, t);
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-        sT[q * kLanes + lane] = tt[q];
-        if (check) bad |= !(tt[q] > 0.0);
+        sXL[q * kLanes + lane] = l[q];
+        sXR[q * kLanes + lane] = r[q];
+        sT[q * kLanes + lane] = t[q];
     }
+    if (check) {
 #pragma unroll
-    for (int qj = 0; qj < N; ++qj) {
-        double col[N], u[N];
+        for (int q = 0; q < N; ++q) bad |= !(l[q] > 0.0) | !(r[q] > 0.0) | !(t[q] > 0.0);
 #pragma unroll
-        for (int a = 0; a < N; ++a) col[a] = t[a][qj];
-        m2n<P, 0>(col, u);
+        for (int i = 0; i < N; ++i)
 #pragma unroll
-        for (int qi = 0; qi < N; ++qi) {
-            sU[(qi * N + qj) * kLanes + lane] = u[qi];
-            if (check) bad |= !(u[qi] > 0.0);
-        }
+            for (int j = 0; j < N; ++j) bad |= !(u[i][j] > 0.0);
     }
     return bad;
 }
+
 
 // Scalars of one face-flux call, by value (no pointer to the kernel
 // parameters may escape into a non-inlined function).
@@ -531,12 +432,9 @@ __device__ __forceinline__ void face_flux_body(int in_off, int in_ld, int in_col
         fs[2][k] = fma(hs, fi2 + fo2, -ha * (vo - vi));
     }
 #pragma unroll
-    for (int v = 0; v < 3; ++v) {
-        double g[N];
-        n2m<P, 2>(fs[v], g);
+    for (int v = 0; v < 3; ++v)
 #pragma unroll
-        for (int b = 0; b < N; ++b) smem[dst_off + (v * N + b) * dst_ld + dst_col] = g[b];
-    }
+        for (int k = 0; k < N; ++k) smem[dst_off + (v * N + k) * dst_ld + dst_col] = fs[v][k];
 }
 
 template <int P>
@@ -605,83 +503,45 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
     }
 }
 
-// eta projections of one xi node line: f[b] = sum_qj wP_b F, g[b] = sum_qj (wP'_b G + wP_b S)
+// Volume + source terms of variable v at the row's nodes, nodal form:
+//   acc[i][j] = sum_k Dx[i][k] F[k][j] + sum_k dh[j][k] G[i][k] + S[i][j]
+// with Dx = (1/R) (determ/bd_det_x) dh (kernel parameter), G carrying its
+// cos/R * determ/bd_det_y factor and S its determ factor (row table); the
+// common 1/(determ cos_j) is applied in finalize.  Node row i (fixed xi
+// node) is evaluated at once: its G/S terms land in acc[i][.], its F
+// scatters into every acc[.][j].
 template <int P, bool MOM>
-__device__ __forceinline__ void line_project(const double (&F)[P + 1], const double (&G)[P + 1],
-                                             const double (&S)[P + 1], double (&f)[P + 1],
-                                             double (&g)[P + 1])
-{
-    n2m<P, 2>(F, f);
-    if constexpr (!MOM)
-        n2m<P, 3>(G, g);
-    else
-        n2m2<P, 3, 2>(G, S, g);
-}
-
-// Volume + source projection of variable v at the current row, streamed
-// over pairs of xi node lines (qi, N-1-qi) so that the xi contraction also
-// uses the even/odd split:
-// vol[a][b] = sum_q (cx dphi/dxi F + cy dphi/deta G + cs phi S)[q]
-template <int P, bool MOM>
-__device__ __forceinline__ void volume(double (&vol)[P + 1][P + 1], int v, const double *sU,
+__device__ __forceinline__ void volume(double (&acc)[P + 1][P + 1], int v, const double *sU,
                                        const double *row, int lane, const StageParams &kp)
 {
     constexpr int N = P + 1;
-    constexpr int H = N / 2;
 #pragma unroll
-    for (int a = 0; a < N; ++a)
+    for (int i = 0; i < N; ++i) {
+        double F[N], G[N], S[N];
+        node_physics<P, MOM>(v == 2, i, sU, row, lane, kp, F, G, S);
 #pragma unroll
-        for (int b = 0; b < N; ++b) vol[a][b] = 0.0;
-#if DG_VOL_UNROLL
+        for (int j = 0; j < N; ++j) {
+            double e = MOM ? S[j] : 0.0;
+            if (i > 0) e += acc[i][j];
 #pragma unroll
-#else
-#pragma unroll 1
-#endif
-    for (int ip = 0; ip < H; ++ip) {
-        double f0[N], g0[N], f1[N], g1[N];
-        {
-            double F[N], G[N], S[N];
-            node_physics<P, MOM>(v == 2, ip, sU, row, lane, kp, F, G, S);
-            line_project<P, MOM>(F, G, S, f0, g0);
-            node_physics<P, MOM>(v == 2, N - 1 - ip, sU, row, lane, kp, F, G, S);
-            line_project<P, MOM>(F, G, S, f1, g1);
-        }
-        double pd[N], pp[N];
-#pragma unroll
-        for (int a = 0; a < N; ++a) {
-            pd[a] = WD(a, ip) * kp.inv_r_cx;   // F's 1/R * determ/bd_det_x folded in here
-            pp[a] = WP(a, ip);
+            for (int k = 0; k < N; ++k) e = fma(c_nod[P].dh[j][k], G[k], e);
+            acc[i][j] = e;
         }
 #pragma unroll
-        for (int b = 0; b < N; ++b) {
-            // wP'_a(N-1-i) = -(-1)^a wP'_a(i), wP_a(N-1-i) = (-1)^a wP_a(i)
-            const double fp = f0[b] + f1[b], fm = f0[b] - f1[b];
-            const double gp = g0[b] + g1[b], gm = g0[b] - g1[b];
+        for (int ii = 0; ii < N; ++ii)
 #pragma unroll
-            for (int a = 0; a < N; ++a)
-                vol[a][b] = fma(pd[a], (a & 1) ? fp : fm, fma(pp[a], (a & 1) ? gm : gp, vol[a][b]));
-        }
-    }
-    if constexpr (N & 1) {   // middle line xi = 0: wP'_a vanishes for even a, wP_a for odd a
-        double F[N], G[N], S[N], f[N], g[N];
-        node_physics<P, MOM>(v == 2, H, sU, row, lane, kp, F, G, S);
-        line_project<P, MOM>(F, G, S, f, g);
-#pragma unroll
-        for (int b = 0; b < N; ++b)
-#pragma unroll
-            for (int a = 0; a < N; ++a)
-                vol[a][b] = (a & 1) ? fma(WD(a, H) * kp.inv_r_cx, f[b], vol[a][b])
-                                    : fma(WP(a, H), g[b], vol[a][b]);
+            for (int j = 0; j < N; ++j)
+                acc[ii][j] = (i == 0 && ii > 0) ? kp.dx[ii][i] * F[j] : fma(kp.dx[ii][i], F[j], acc[ii][j]);
     }
 }
 
-// Boundary lifts, inverse mass, stage combination and store for variable v.
-// The mass block is applied column by column (one row of T from shared
-// memory at a time) so that vol, c and u^n are the only tiles held.
+// Boundary lifts, diagonal mass, stage combination and store for variable v.
+// Face values are scale * f* at the face's nodes (bd_det folded in by the
+// face warps); x lifts run along xi with mu, y lifts along eta.
 // Uv / Yv point at this lane's element of the variable's strip block
-// (mode stride 32 doubles: immediate offsets).
+// (node stride 32 doubles: immediate offsets).
 template <int P, bool HAS_U, bool HAS_Y2>
-__device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const double *cur,
+__device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const double *cur,
                                              const double *Uv, const double *Av, double *Y2v, int v,
                                              const double *sFX, const double *sF0,
                                              const double *sFtop, const double *sFbot, bool has_top,
@@ -705,57 +565,60 @@ __device__ __forceinline__ unsigned finalize(double (&vol)[P + 1][P + 1], const 
 #pragma unroll
             for (int b = 0; b < N; ++b) an[a][b] = Av[(a * N + b) * kLanes];
     }
-    constexpr int LDX = kLanes + 1;    // x-face columns: face f is the left face of lane f
-    const int o = (v * N) * kLanes, ox = (v * N) * LDX;
+    const int o = (v * N) * kLanes;    // x-face column c: right face of lane c (lane 0's left face: F0)
 #pragma unroll
-    for (int b = 0; b < N; ++b) {
-        // projected face lifts (bdy / bdx folded in by the face warps)
-        const double l = lane == 0 ? sF0[v * N + b] : sFX[ox + b * LDX + lane];
-        const double r = sFX[ox + b * LDX + lane + 1];
-        const double t = has_top ? sFtop[o + b * kLanes + lane] : 0.0;   // pole faces carry
-        const double bo = has_bot ? sFbot[o + b * kLanes + lane] : 0.0;  // no flux (dg.py:483-495)
-        // x lifts broadcast along a (parity of a), y lifts along b (parity of b)
-        const double xe = l - r, xo = -l - r;
-        const double ye = bo - t, yo = -bo - t;
+    for (int q = 0; q < N; ++q) {
+        const double l = lane == 0 ? sF0[v * N + q] : sFX[o + q * kLanes + ((lane + kLanes - 1) & (kLanes - 1))];
+        const double r = sFX[o + q * kLanes + lane];
+        const double t = has_top ? sFtop[o + q * kLanes + lane] : 0.0;   // pole faces carry
+        const double bo = has_bot ? sFbot[o + q * kLanes + lane] : 0.0;  // no flux (dg.py:483-495)
 #pragma unroll
-        for (int a = 0; a < N; ++a) {
-            vol[a][b] += (a & 1) ? xo : xe;   // x lift: column b
-            vol[b][a] += (a & 1) ? yo : ye;   // y lift of row b: column a parity
+        for (int k = 0; k < N; ++k) {
+            // x faces at eta node q lift along xi (column q); y faces at xi node q along eta (row q)
+            acc[k][q] = fma(c_nod[P].mu[k], l, fma(-c_nod[P].mu[N - 1 - k], r, acc[k][q]));
+            acc[q][k] = fma(c_nod[P].mu[k], bo, fma(-c_nod[P].mu[N - 1 - k], t, acc[q][k]));
         }
     }
-    const double *T = row + RL::T;
+    const double *rj = row + RL::RJ;
     int fexp = 0;                     // max exponent field of the outputs (integer pipe)
-    double mean = 1.0;
 #pragma unroll
-    for (int b = 0; b < N; ++b) {
-        double tb[N];
+    for (int j = 0; j < N; ++j) {
+        const double gr = kp.g * rj[j];
+        const double g2r = HAS_Y2 ? kp.g2 * rj[j] : 0.0;
 #pragma unroll
-        for (int bb = 0; bb < N; ++bb) tb[bb] = T[b * N + bb];
-#pragma unroll
-        for (int a = 0; a < N; ++a) {
-            double k = tb[0] * vol[a][0];
-#pragma unroll
-            for (int bb = 1; bb < N; ++bb) k = fma(tb[bb], vol[a][bb], k);
-            double y = fma(kp.b, cur[(a * N + b) * kLanes + lane], (kp.g * (double)(2 * a + 1)) * k);
-            if (HAS_U) y = fma(kp.a, un[a][b], y);
-            if (owned) Yv[(a * N + b) * kLanes] = y;
-            if (owned && Ypeer) Ypeer[(a * N + b) * kLanes] = y;   // fused halo exchange (NVLink store)
-            if (owned && Ypeer2) Ypeer2[(a * N + b) * kLanes] = y;
+        for (int i = 0; i < N; ++i) {
+            const double k = acc[i][j];
+            double y = fma(kp.b, cur[(i * N + j) * kLanes + lane], gr * k);
+            if (HAS_U) y = fma(kp.a, un[i][j], y);
+            if (owned) Yv[(i * N + j) * kLanes] = y;
+            if (owned && Ypeer) Ypeer[(i * N + j) * kLanes] = y;   // fused halo exchange (NVLink store)
+            if (owned && Ypeer2) Ypeer2[(i * N + j) * kLanes] = y;
             fexp = max(fexp, __double2hiint(y) & 0x7ff00000);
             if constexpr (HAS_Y2) {
-                const double y2 = fma(kp.g2 * (double)(2 * a + 1), k, an[a][b]);
-                if (owned) Y2v[(a * N + b) * kLanes] = y2;
+                const double y2 = fma(g2r, k, an[i][j]);
+                if (owned) Y2v[(i * N + j) * kLanes] = y2;
             }
-            if (a == 0 && b == 0) mean = y;
+            acc[i][j] = y;
         }
     }
     unsigned bad = 0;
     if (owned) {
         bad |= (kp.check_finite && fexp == 0x7ff00000) ? 2u : 0u;   // Inf or NaN
-        bad |= (v == 0 && kp.check_mean && !(mean > 0.0)) ? 4u : 0u;
+        if (v == 0 && kp.check_mean) {   // cell mean = modal c_00 = sum w_i w_j u_ij / 4
+            double m = 0.0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int j = 0; j < N; ++j) s = fma(c_nod[P].w[j], acc[i][j], s);
+                m = fma(c_nod[P].w[i], s, m);
+            }
+            bad |= !(m > 0.0) ? 4u : 0u;
+        }
     }
     return bad;
 }
+
 
 // Face warp: the neighbour elements' coefficients of row r (left eL =
 // (32 s - 1) mod nx, right eR = (32 s + nvalid) mod nx; 3 vars x nphi each)
@@ -775,8 +638,8 @@ __device__ __forceinline__ void fetch_neighbours(const double *Xrow, int eL, int
 
 // Face warp: the traces of the strip's left border face for one row.
 // Lanes 0..5 each build one trace: (side 0) R trace of the left neighbour
-// element, from the gathered coefficients; (side 1) L trace of the strip's
-// element 0, from the coefficient ring.  Also the L trace of the right
+// element, from its gathered nodal values; (side 1) L trace of the strip's
+// element 0, from the ring.  Also the L trace of the right
 // neighbour (lanes 6..8), which the h warp needs for the last lane's right face.
 template <int P>
 __device__ __forceinline__ void border_traces(const double *sHB, const double *ring_slot, double *sHL,
@@ -800,39 +663,34 @@ __device__ __forceinline__ void border_traces(const double *sHB, const double *r
 #pragma unroll
                 for (int b = 0; b < N; ++b) c[a][b] = src[a * N + b];
         }
-        double t[N][N];
-#pragma unroll
-        for (int a = 0; a < N; ++a) m2n<P, 0>(c[a], t[a]);
-        const double sg = side == 0 ? 1.0 : -1.0;    // R trace: sum_a t, L trace: sum_a (-1)^a t
+        double tr[N];
+        if (side == 0)
+            xtrace<P, false>(c, tr);                 // R trace of the left neighbour
+        else
+            xtrace<P, true>(c, tr);                  // L traces of element 0 / the right neighbour
         double *dst = side == 0 ? sHL : side == 1 ? sE0 : sHR;
 #pragma unroll
-        for (int q = 0; q < N; ++q) {
-            double e = t[0][q], o = 0.0;
-#pragma unroll
-            for (int a = 2; a < N; a += 2) e += t[a][q];
-            if constexpr (N > 1) {
-                o = t[1][q];
-#pragma unroll
-                for (int a = 3; a < N; a += 2) o += t[a][q];
-            }
-            dst[v * N + q] = fma(sg, o, e);
-        }
+        for (int q = 0; q < N; ++q) dst[v * N + q] = tr[q];
     }
     __syncwarp();
 }
 
-// bottom traces (eta = -1) of one row, all three variables, from its ring tile
+// one variable's bottom traces of a row (its nodal ring tile) -> the
+// y-face buffer the face warp evaluates in place (+ h positivity)
 template <int P>
-__device__ __forceinline__ void bottom_traces(const double *ring_row, int lane, double (&bt)[3][P + 1])
+__device__ __forceinline__ unsigned stage_bottom(const double *tile, double *dst, int lane, bool check)
 {
     constexpr int N = P + 1;
-    constexpr int NP = N * N;
+    double c[N][N], bt[N];
+    tile_read<P>(c, tile, lane);
+    ytrace<P, true>(c, bt);
+    unsigned bad = 0;
 #pragma unroll
-    for (int v = 0; v < 3; ++v) {
-        double cv[N][N];
-        tile_read<P>(cv, ring_row + v * NP * kLanes, lane);
-        ytrace<P, false>(cv, bt[v]);
+    for (int q = 0; q < N; ++q) {
+        dst[q * kLanes + lane] = bt[q];
+        if (check) bad |= !(bt[q] > 0.0);
     }
+    return bad;
 }
 
 template <int P, bool HAS_U, bool HAS_Y2, bool EDGE>
@@ -847,7 +705,20 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
     // fixed roles: warp w runs on sub-partition w of its SM, so every
     // sub-partition executes a single code path (better I-cache locality
     // than rotating roles, measured)
+#if DG_ROLEMIX
+    // experiment: rotate the role map by the CTA's warp-slot group so the
+    // resident CTAs spread each role over the sub-partitions
+    __shared__ int s_rot;
+    if (threadIdx.x == 0) {
+        unsigned wid;
+        asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+        s_rot = (int)((wid >> 2) & 3u);
+    }
+    __syncthreads();
+    const int role = ((int)(threadIdx.x >> 5) + s_rot) & 3;
+#else
     const int role = threadIdx.x >> 5;
+#endif
     const int v = role < kVarWarps ? role : 0;     // face warp borrows var 0's addressing
     const bool face_warp = role == kVarWarps;
     const int lane = threadIdx.x & 31;
@@ -878,7 +749,6 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
 
     double *const ringS = smem + SM::XR0;          // [slot][var][mode][lane]
     double *const ring0 = ringS + v * NP * kLanes;   // this warp's variable
-    double *sU = smem + SM::U;
     double *sXL = smem + SM::XL;
     double *sXR = smem + SM::XRT;
     double *sT = smem + SM::TT;
@@ -944,11 +814,15 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
 #pragma unroll
             for (int b = 0; b < N; ++b) c[a][b] = __ldg(src + (a * N + b) * kLanes);
         double tt[N];
-        ytrace<P, true>(c, tt);
+        ytrace<P, false>(c, tt);
 #pragma unroll
         for (int q = 0; q < N; ++q) sT[(v * N + q) * kLanes + lane] = tt[q];
     }
-    if (!face_warp) mbar_wait(mbar + v, 0);        // row jb landed (this variable)
+    if (!face_warp) {
+        mbar_wait(mbar + v, 0);                    // row jb landed (this variable)
+        // its bottom traces: the face below row jb (the face warp's pre-iteration)
+        bad |= owned & stage_bottom<P>(ring0, sFb + v * N * kLanes, lane, chk);
+    }
     // periodic neighbours of the strip's border elements
     const int eL = (strip * kLanes - 1 + nx) % nx;
     const int eR = (strip * kLanes + nvalid) % nx;
@@ -988,25 +862,15 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
                 cp_commit();
             }
             const double *next_tile = ringS + ((k + 1) & 1) * SM::TILE;   // X(it+1)
-            if (it + 1 <= last_fetch) {
-                double bt[3][N];
-                bottom_traces<P>(next_tile, lane, bt);
-#pragma unroll
-                for (int q = 0; q < N; ++q) bad |= owned && !(bt[0][q] > 0.0);
-                const bool face = pre ? below : (kp.row0 + it + 1 < kp.ny);
-                if (face) {
-                    // bottom traces staged in the face's output slot, read back by the call
-                    const int dst = (int)((pre ? fb : fa) - smem);
-#pragma unroll
-                    for (int vv = 0; vv < 3; ++vv)
-#pragma unroll
-                        for (int q = 0; q < N; ++q) smem[dst + (vv * N + q) * kLanes + lane] = bt[vv][q];
-                    const double *above = sRow + ((k + 1) % 3) * RL::STRIDE;
-                    face_flux_call<P>(SM::TT, kLanes, lane, dst, kLanes, lane, dst, kLanes, lane,
-                                      FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
-                                               kp.alpha_mode, 1, above[RL::CRB], above[RL::COSB], alpha_y,
-                                               kp.bdx});
-                }
+            // the y-face above row it, from row it's top traces and row it+1's
+            // bottom traces (staged in the face's output slot by the var warps)
+            if (it + 1 <= last_fetch && (!pre || below)) {
+                const int dst = (int)((pre ? fb : fa) - smem);
+                const double *above = sRow + ((k + 1) % 3) * RL::STRIDE;
+                face_flux_call<P>(SM::TT, kLanes, lane, dst, kLanes, lane, dst, kLanes, lane,
+                                  FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
+                                           kp.alpha_mode, 1, above[RL::CRB], above[RL::COSB], alpha_y,
+                                           kp.bdx});
             }
             TSTAMP(c);
             __syncthreads();                           // barrier 2 of row it (prologue barrier B)
@@ -1053,11 +917,15 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             {
                 double c[N][N];
                 tile_read<P>(c, cur, lane);            // X(jl)
-                bad |= owned & eval_row<P>(c, sU + v * NP * kLanes, sXL + v * N * kLanes,
-                                           sXR + v * N * kLanes, sT + v * N * kLanes, lane, chk);
+                bad |= owned & traces_row<P>(c, sXL + v * N * kLanes, sXR + v * N * kLanes, sT + v * N * kLanes,
+                                             lane, chk);
             }
             TSTAMP(0);
-            if (jl + 1 <= last_fetch) mbar_wait(mbar + (slot ^ 1) * 3 + v, ((k + 1) >> 1) & 1);   // X(jl+1)
+            if (jl + 1 <= last_fetch) {
+                mbar_wait(mbar + (slot ^ 1) * 3 + v, ((k + 1) >> 1) & 1);   // X(jl+1)
+                // its bottom traces for the face warp's y-face above row jl
+                bad |= owned & stage_bottom<P>(ring0 + (slot ^ 1) * SM::TILE, sFa + v * N * kLanes, lane, chk);
+            }
             TSTAMP(1);
             __syncthreads();                           // barrier 1
             TSTAMP(2);
@@ -1067,15 +935,15 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
                 // (right face of every lane; the last valid lane's neighbour is the halo)
                 const bool last = lane == nvalid - 1;
                 face_flux_call<P>(SM::XRT, kLanes, lane, last ? SM::HR : SM::XL, last ? 1 : kLanes,
-                                  last ? 0 : min(lane + 1, kLanes - 1), SM::FX, kLanes + 1, lane + 1,
+                                  last ? 0 : min(lane + 1, kLanes - 1), SM::FX, kLanes, lane,
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
                                            kp.alpha_mode, 0, 0.0, 0.0, alpha_x, kp.bdy});
             }
             double vol[N][N];
             if (v == 0)
-                volume<P, false>(vol, v, sU, row, lane, kp);
+                volume<P, false>(vol, v, ringS + slot * SM::TILE, row, lane, kp);
             else
-                volume<P, true>(vol, v, sU, row, lane, kp);
+                volume<P, true>(vol, v, ringS + slot * SM::TILE, row, lane, kp);
             TSTAMP(3);
             __syncthreads();                           // barrier 2
             TSTAMP(4);
@@ -1142,6 +1010,49 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             }
         }
     }
+}
+
+// Modal <-> nodal change of basis of one element and variable per thread,
+// grid (nstrip, rows, nz), block 96 = 3 variables x 32 lanes; in may equal
+// out (every thread reads its element before writing it):
+//   nodal u[i][j] = sum_ab P_a(x_i) P_b(x_j) c[a][b]                (basis.py:118-133)
+//   modal c[a][b] = (2a+1)(2b+1)/4 sum_ij w_i P_a(x_i) w_j P_b(x_j) u[i][j]
+// (the Gauss rule is exact for the degree-2p products, so the pair is an
+// exact inverse up to rounding).
+template <int P, bool TO_NODAL>
+__global__ void __launch_bounds__(96) convert_kernel(const double *in, double *out, long long zstride,
+                                                     long long rstride, long long vstride, int r0)
+{
+    constexpr int N = P + 1;
+    constexpr int NP = N * N;
+    const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
+    const size_t off = (size_t)blockIdx.z * zstride + (size_t)(r0 + (int)blockIdx.y) * rstride +
+                       (size_t)v * vstride + (size_t)blockIdx.x * NP * kLanes + lane;
+    double x[N][N], t[N][N];
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int b = 0; b < N; ++b) x[a][b] = in[off + (a * N + b) * kLanes];
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int q = 0; q < N; ++q) {   // contract the second index
+            double s = 0.0;
+#pragma unroll
+            for (int b = 0; b < N; ++b)
+                s = fma(TO_NODAL ? LEG(b, q) : WP(q, b), x[a][b], s);
+            t[a][q] = s;
+        }
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+        for (int r = 0; r < N; ++r) {   // then the first
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < N; ++a) s = fma(TO_NODAL ? LEG(a, q) : WP(q, a), t[a][r], s);
+            if (!TO_NODAL) s *= 0.25 * (double)((2 * q + 1) * (2 * r + 1));
+            out[off + (q * N + r) * kLanes] = s;
+        }
 }
 
 #undef LEG

@@ -209,6 +209,15 @@ class _Context:
     def launches(self) -> int:
         return int(self.lib.dgswe_launch_count(self.h))
 
+    def set_basis(self, nodal: bool):
+        """Basis of the states the stage entry points take (include/dgswe_b200.h)."""
+        _lib.check(self.lib.dgswe_set_basis(self.h, int(bool(nodal))), "dgswe_set_basis")
+
+    def convert(self, data: torch.Tensor, to_nodal: bool, r0: int, r1: int):
+        """In-place modal <-> nodal change of basis of local rows [r0, r1)."""
+        _lib.check(self.lib.dgswe_convert(self.h, ctypes.c_void_p(data.data_ptr()), int(bool(to_nodal)),
+                                          int(r0), int(r1), self.stream()), "dgswe_convert")
+
 
 def _ptr(t: torch.Tensor | None):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)

@@ -50,17 +50,18 @@ def main():
     u.copy_(torch.from_numpy(L.scatter(full)))
     w1, w2 = bop.empty(), bop.empty()
     bop.attach(u, w1, w2)
+    # one batch of args.steps steps (one modal <-> nodal conversion each way)
     if args.graph:
-        bop.ssprk3_step(u, w1, w2, 5.0, tag=0)            # eager first step
+        bop.begin(u)
+        bop.nodal_steps(u, w1, w2, 5.0, 1, tag=0)        # eager first step
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            for k in range(1, args.steps):
-                bop.ssprk3_step(u, w1, w2, 5.0, tag=k)
+            bop.nodal_steps(u, w1, w2, 5.0, args.steps - 1, tag=1)
         g.replay()
+        bop.end(u)
     else:
-        for k in range(args.steps):
-            bop.ssprk3_step(u, w1, w2, 5.0, tag=k)
+        bop.ssprk3_steps(u, w1, w2, 5.0, args.steps)
     flags, _ = bop.status()
     assert flags == 0, flags
     mine = u[:, L.jlo:L.jhi].cpu().contiguous()
