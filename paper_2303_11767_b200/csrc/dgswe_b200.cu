@@ -571,11 +571,11 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
         r[3 * n] = t->cos_r_edge[j];
         r[3 * n + 1] = t->cos_edge[j];
         const double *M = t->minv + (size_t)j * ctx->nphi * ctx->nphi;
-        for (int b = 0; b < n; ++b)
-            for (int bb = 0; bb < n; ++bb) r[3 * n + 2 + b * n + bb] = M[(size_t)b * ctx->nphi + bb];
         // nodal mass 1 / (determ cos_j) (the w_i w_j factors live in dh, mu)
         for (int q = 0; q < n; ++q)
-            r[3 * n + 2 + n * n + q] = 1.0 / (determ * (t->cos_r_int[j * n + q] * c.radius));
+            r[3 * n + 2 + q] = 1.0 / (determ * (t->cos_r_int[j * n + q] * c.radius));
+        for (int b = 0; b < n; ++b)
+            for (int bb = 0; bb < n; ++bb) r[4 * n + 2 + b * n + bb] = M[(size_t)b * ctx->nphi + bb];
     }
     bool ok = cudaMalloc(&ctx->rowtab, rt.size() * sizeof(double)) == cudaSuccess &&
               cudaMalloc(&ctx->cos_edge, (c.ny + 1) * sizeof(double)) == cudaSuccess &&

@@ -92,7 +92,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     return v;
 }
 
-// per-row table layout (doubles): crc[n] srs[n] fcs[n] cr_b cos_b T[n][n] rj[n]
+// per-row table layout (doubles): crc[n] srs[n] fcs[n] cr_b cos_b rj[n] T[n][n]
 template <int P>
 struct RowLayout {
     static constexpr int N = P + 1;
@@ -101,9 +101,10 @@ struct RowLayout {
     static constexpr int FCS = 2 * N;
     static constexpr int CRB = 3 * N;
     static constexpr int COSB = 3 * N + 1;
-    static constexpr int T = 3 * N + 2;      // theta block of M^-1 (modal; device IC projection)
-    static constexpr int RJ = T + N * N;     // 1 / (determ cos_j): the nodal mass
-    static constexpr int STRIDE = RJ + N;
+    static constexpr int RJ = 3 * N + 2;     // 1 / (determ cos_j): the nodal mass
+    static constexpr int SSTRIDE = RJ + N;   // the part staged in shared memory
+    static constexpr int T = SSTRIDE;        // theta block of M^-1 (modal; device IC projection only)
+    static constexpr int STRIDE = T + N * N;
 };
 
 __host__ __device__ inline int row_stride(int p) { return 4 * (p + 1) + 2 + (p + 1) * (p + 1); }
@@ -123,9 +124,16 @@ __host__ __device__ inline int row_stride(int p) { return 4 * (p + 1) + 2 + (p +
 #ifndef DG_VOL_UNROLL
 #define DG_VOL_UNROLL 0
 #endif
+#ifndef DG_VROLL
+#define DG_VROLL -1  // volume loop over node rows kept rolled (row-local terms through shared memory):
+                     // -1 = for p >= 3 (a quarter of the unrolled code: measured +1% at p=3, +6% at
+                     // p=4, -2% at p=2), 0 = never, 1 = always
+#endif
+template <int P>
+__host__ __device__ constexpr bool vol_rolled() { return DG_VROLL < 0 ? P >= 3 : DG_VROLL != 0; }
 #ifndef DG_MINB
-#define DG_MINB 3   // resident CTAs per SM the p <= 3 build is register-capped for (~160 registers;
-                    // 4 CTAs at 128 registers measured 7% slower at C3 once the code was compact)
+#define DG_MINB 4   // resident CTAs per SM the p = 3 build is register-capped for (128 registers
+                    // with the rolled volume loop; 3 at ~160 measured 1-2% slower)
 #endif
 
 // DG_TIMING builds record per-role phase durations (clock cycles) of every
@@ -182,7 +190,8 @@ struct Smem {
     // offsets in doubles
     static constexpr int XR0 = 0;                        // coefficient ring slot 0 [var][mode][lane]
     static constexpr int XR1 = XR0 + TILE;               // slot 1
-    static constexpr int XL = XR1 + TILE;                // L traces [3][N][32]
+    static constexpr int E = XR1 + TILE;                 // row-local volume terms [3][NP][32] (rolled volume)
+    static constexpr int XL = E + (vol_rolled<P>() ? TILE : 0);   // L traces [3][N][32]
     static constexpr int XRT = XL + TR;
     static constexpr int TT = XRT + TR;                  // top traces of current row
     static constexpr int FX = TT + TR;                   // x-face fluxes [3][N][32], column c = right face of lane c
@@ -195,7 +204,7 @@ struct Smem {
     static constexpr int F0 = E0 + 3 * N;                // face 0 flux [row parity][3][N]
     static constexpr int HB = F0 + 6 * N;                // next row's neighbour coefficients [2][3][NP]
     static constexpr int ROW = HB + 6 * NP;              // row-table ring, 3 rows
-    static constexpr int MBAR = ROW + 3 * RowLayout<P>::STRIDE;   // 6 mbarriers [slot][var]
+    static constexpr int MBAR = ROW + 3 * RowLayout<P>::SSTRIDE;  // 6 mbarriers [slot][var]
     static constexpr int TOTAL = MBAR + 6;
 };
 
@@ -295,6 +304,12 @@ __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_grou
 __device__ __forceinline__ void prefetch_l2_bulk(const double *src, unsigned bytes)
 {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ double *smem_base()
+{
+    extern __shared__ double smem[];
+    return smem;
 }
 
 template <int P>
@@ -535,6 +550,39 @@ __device__ __forceinline__ void volume(double (&acc)[P + 1][P + 1], int v, const
     }
 }
 
+// Same terms with the loop over node rows kept rolled (a quarter of the
+// code): the row-local G/S terms of row i go to shared memory sE (this
+// warp's [NP][32] block) and are added in finalize; F still scatters into
+// the register tile through the i-th column of Dx.
+template <int P, bool MOM>
+__device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v, const double *sU,
+                                              const double *row, int lane, const StageParams &kp, double *sE)
+{
+    constexpr int N = P + 1;
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii)
+#pragma unroll
+        for (int j = 0; j < N; ++j) acc[ii][j] = 0.0;
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) {
+        double F[N], G[N], S[N];
+        node_physics<P, MOM>(v == 2, i, sU, row, lane, kp, F, G, S);
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            double e = MOM ? S[j] : 0.0;
+#pragma unroll
+            for (int k = 0; k < N; ++k) e = fma(c_nod[P].dh[j][k], G[k], e);
+            sE[(i * N + j) * kLanes + lane] = e;
+        }
+#pragma unroll
+        for (int ii = 0; ii < N; ++ii) {
+            const double d = kp.dx[ii][i];
+#pragma unroll
+            for (int j = 0; j < N; ++j) acc[ii][j] = fma(d, F[j], acc[ii][j]);
+        }
+    }
+}
+
 // Boundary lifts, diagonal mass, stage combination and store for variable v.
 // Face values are scale * f* at the face's nodes (bd_det folded in by the
 // face warps); x lifts run along xi with mu, y lifts along eta.
@@ -564,6 +612,13 @@ __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const 
         for (int a = 0; a < N; ++a)
 #pragma unroll
             for (int b = 0; b < N; ++b) an[a][b] = Av[(a * N + b) * kLanes];
+    }
+    if constexpr (vol_rolled<P>()) {
+        const double *sE = smem_base() + Smem<P>::E + v * N * N * kLanes;
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+            for (int j = 0; j < N; ++j) acc[i][j] += sE[(i * N + j) * kLanes + lane];
     }
     const int o = (v * N) * kLanes;    // x-face column c: right face of lane c (lane 0's left face: F0)
 #pragma unroll
@@ -794,8 +849,10 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
     const int gfirst = kp.row0 + jb;
     {
         const int nload = min(2, kp.ny - gfirst);
-        for (int idx = threadIdx.x; idx < nload * RL::STRIDE; idx += kThreads)
-            sRow[idx] = kp.rowtab[(size_t)gfirst * RL::STRIDE + idx];
+        for (int idx = threadIdx.x; idx < nload * RL::SSTRIDE; idx += kThreads) {
+            const int r = idx / RL::SSTRIDE;
+            sRow[idx] = kp.rowtab[(size_t)(gfirst + r) * RL::STRIDE + (idx - r * RL::SSTRIDE)];
+        }
     }
 
     double alpha_x = kp.alpha, alpha_y = kp.alpha;
@@ -855,9 +912,9 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
                     fetch_neighbours<P>(kp.X + (size_t)blockIdx.z * kp.zstride + (size_t)(it + 1) * kp.rstride,
                                         eL, eR, smem + SM::HB, lane, kp.vstride);
                 if (it + 2 <= je && kp.row0 + it + 2 < kp.ny) {
-                    double *dst = sRow + ((k + 2) % 3) * RL::STRIDE;
+                    double *dst = sRow + ((k + 2) % 3) * RL::SSTRIDE;
                     const double *src = kp.rowtab + (size_t)(kp.row0 + it + 2) * RL::STRIDE;
-                    for (int idx = lane; idx < RL::STRIDE; idx += kLanes) cp_async8(dst + idx, src + idx);
+                    for (int idx = lane; idx < RL::SSTRIDE; idx += kLanes) cp_async8(dst + idx, src + idx);
                 }
                 cp_commit();
             }
@@ -866,7 +923,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             // bottom traces (staged in the face's output slot by the var warps)
             if (it + 1 <= last_fetch && (!pre || below)) {
                 const int dst = (int)((pre ? fb : fa) - smem);
-                const double *above = sRow + ((k + 1) % 3) * RL::STRIDE;
+                const double *above = sRow + ((k + 1) % 3) * RL::SSTRIDE;
                 face_flux_call<P>(SM::TT, kLanes, lane, dst, kLanes, lane, dst, kLanes, lane,
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
                                            kp.alpha_mode, 1, above[RL::CRB], above[RL::COSB], alpha_y,
@@ -906,7 +963,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             const int jg = kp.row0 + jl;
             const bool has_top = jg + 1 < kp.ny;
             const bool has_bot = jg > 0;
-            const double *row = sRow + (k % 3) * RL::STRIDE;
+            const double *row = sRow + (k % 3) * RL::SSTRIDE;
             TSTAMP(s);
 
             // warm L2 for this row's u^n and for row jl+2 (copied in after finalize)
@@ -940,10 +997,18 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
                                            kp.alpha_mode, 0, 0.0, 0.0, alpha_x, kp.bdy});
             }
             double vol[N][N];
-            if (v == 0)
-                volume<P, false>(vol, v, ringS + slot * SM::TILE, row, lane, kp);
-            else
-                volume<P, true>(vol, v, ringS + slot * SM::TILE, row, lane, kp);
+            if constexpr (vol_rolled<P>()) {
+                double *sE = smem + SM::E + v * NP * kLanes;
+                if (v == 0)
+                    volume_rolled<P, false>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sE);
+                else
+                    volume_rolled<P, true>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sE);
+            } else {
+                if (v == 0)
+                    volume<P, false>(vol, v, ringS + slot * SM::TILE, row, lane, kp);
+                else
+                    volume<P, true>(vol, v, ringS + slot * SM::TILE, row, lane, kp);
+            }
             TSTAMP(3);
             __syncthreads();                           // barrier 2
             TSTAMP(4);
