@@ -474,14 +474,14 @@ __device__ __forceinline__ void face_flux_call(int in_off, int in_ld, int in_col
 
 // Pointwise flux / source at the N nodes (qi, qj), qj = 0..N-1
 // (models.py:161-252): F = x-flux (its cx/R goes into the xi weights),
-// G = y-flux * cy cos/R, S = source.  MOM = false: the h equation
-// (F = hu, G = hv cos/R, no source).  MOM = true: one branch-free code path
-// for both momentum equations, the variable (is_v: hv) entering only
-// through uniform selects, so the nodes' instructions interleave:
-//   hu: F = hu u + g h^2/2,  G = hu w cos/R,             S = t hv
-//   hv: F = hu w,            G = (hv w + g h^2/2) cos/R, S = -(g h^2/2 sin/R + t hu)
+// G = y-flux * cy cos/R, S = source, for the equation of KIND:
+//   0 h:  F = hu,              G = hv cos/R,               S = 0
+//   1 hu: F = hu u + g h^2/2,  G = hu w cos/R,             S = t hv
+//   2 hv: F = hu w,            G = (hv w + g h^2/2) cos/R, S = -(g h^2/2 sin/R + t hu)
+//   3:    hu or hv by the uniform flag is_v, one branch-free code path
+//         (the unrolled volume, where a second copy would cost I-cache)
 // with u = hu/hf, w = hv/hf, t = u sin/R + 2 Omega sin cos.
-template <int P, bool MOM>
+template <int P, int KIND>
 __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU, const double *row, int lane,
                                              const StageParams &kp, double (&F)[P + 1],
                                              double (&G)[P + 1], double (&S)[P + 1])
@@ -495,7 +495,7 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
         const double hu = sU[(1 * NP + q) * kLanes + lane];
         const double hv = sU[(2 * NP + q) * kLanes + lane];
         const double crc = row[RL::CRC + qj];
-        if constexpr (!MOM) {
+        if constexpr (KIND == 0) {
             F[qj] = hu;
             G[qj] = hv * crc;
             S[qj] = 0.0;
@@ -511,9 +511,19 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
             const double u = hu * r, w = hv * r;
             const double srs = row[RL::SRS + qj];
             const double t = fma(u, srs, row[RL::FCS + qj]);
-            F[qj] = fma(hu, is_v ? w : u, is_v ? 0.0 : gh2);
-            G[qj] = fma(is_v ? hv : hu, w, is_v ? gh2 : 0.0) * crc;
-            S[qj] = fma(is_v ? -gh2 : 0.0, srs, t * (is_v ? -hu : hv));
+            if constexpr (KIND == 1) {
+                F[qj] = fma(hu, u, gh2);
+                G[qj] = (hu * w) * crc;
+                S[qj] = t * hv;
+            } else if constexpr (KIND == 2) {
+                F[qj] = hu * w;
+                G[qj] = fma(hv, w, gh2) * crc;
+                S[qj] = fma(-gh2, srs, -(t * hu));
+            } else {
+                F[qj] = fma(hu, is_v ? w : u, is_v ? 0.0 : gh2);
+                G[qj] = fma(is_v ? hv : hu, w, is_v ? gh2 : 0.0) * crc;
+                S[qj] = fma(is_v ? -gh2 : 0.0, srs, t * (is_v ? -hu : hv));
+            }
         }
     }
 }
@@ -533,7 +543,7 @@ __device__ __forceinline__ void volume(double (&acc)[P + 1][P + 1], int v, const
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         double F[N], G[N], S[N];
-        node_physics<P, MOM>(v == 2, i, sU, row, lane, kp, F, G, S);
+        node_physics<P, MOM ? 3 : 0>(v == 2, i, sU, row, lane, kp, F, G, S);
 #pragma unroll
         for (int j = 0; j < N; ++j) {
             double e = MOM ? S[j] : 0.0;
@@ -554,7 +564,7 @@ __device__ __forceinline__ void volume(double (&acc)[P + 1][P + 1], int v, const
 // code): the row-local G/S terms of row i go to shared memory sE (this
 // warp's [NP][32] block) and are added in finalize; F still scatters into
 // the register tile through the i-th column of Dx.
-template <int P, bool MOM>
+template <int P, int KIND>
 __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v, const double *sU,
                                               const double *row, int lane, const StageParams &kp, double *sE)
 {
@@ -566,10 +576,10 @@ __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v
 #pragma unroll 1
     for (int i = 0; i < N; ++i) {
         double F[N], G[N], S[N];
-        node_physics<P, MOM>(v == 2, i, sU, row, lane, kp, F, G, S);
+        node_physics<P, KIND>(false, i, sU, row, lane, kp, F, G, S);
 #pragma unroll
         for (int j = 0; j < N; ++j) {
-            double e = MOM ? S[j] : 0.0;
+            double e = KIND ? S[j] : 0.0;
 #pragma unroll
             for (int k = 0; k < N; ++k) e = fma(c_nod[P].dh[j][k], G[k], e);
             sE[(i * N + j) * kLanes + lane] = e;
@@ -1000,9 +1010,11 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             if constexpr (vol_rolled<P>()) {
                 double *sE = smem + SM::E + v * NP * kLanes;
                 if (v == 0)
-                    volume_rolled<P, false>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sE);
+                    volume_rolled<P, 0>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sE);
+                else if (v == 1)
+                    volume_rolled<P, 1>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sE);
                 else
-                    volume_rolled<P, true>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sE);
+                    volume_rolled<P, 2>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sE);
             } else {
                 if (v == 0)
                     volume<P, false>(vol, v, ringS + slot * SM::TILE, row, lane, kp);
