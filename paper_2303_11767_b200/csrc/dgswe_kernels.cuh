@@ -131,6 +131,12 @@ __host__ __device__ inline int row_stride(int p) { return 4 * (p + 1) + 2 + (p +
 #endif
 template <int P>
 __host__ __device__ constexpr bool vol_rolled() { return DG_VROLL < 0 ? P >= 3 : DG_VROLL != 0; }
+#ifndef DG_FCHECK
+#define DG_FCHECK 0  // 1: the face warp checks the interior h nodes (the h warp only the traces)
+#endif
+#ifndef DG_HSPLIT
+#define DG_HSPLIT 2  // 1 / 2: the hu / hv warp also computes the h equation's row-local volume term (2: +0.4% at C3)
+#endif
 #ifndef DG_MINB
 #define DG_MINB 4   // resident CTAs per SM the p = 3 build is register-capped for (128 registers
                     // with the rolled volume loop; 3 at ~160 measured 1-2% slower)
@@ -365,10 +371,11 @@ __device__ __forceinline__ unsigned traces_row(const double (&u)[P + 1][P + 1], 
     if (check) {
 #pragma unroll
         for (int q = 0; q < N; ++q) bad |= !(l[q] > 0.0) | !(r[q] > 0.0) | !(t[q] > 0.0);
+        if (!DG_FCHECK)
 #pragma unroll
-        for (int i = 0; i < N; ++i)
+            for (int i = 0; i < N; ++i)
 #pragma unroll
-            for (int j = 0; j < N; ++j) bad |= !(u[i][j] > 0.0);
+                for (int j = 0; j < N; ++j) bad |= !(u[i][j] > 0.0);
     }
     return bad;
 }
@@ -577,18 +584,39 @@ __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v
     for (int i = 0; i < N; ++i) {
         double F[N], G[N], S[N];
         node_physics<P, KIND>(false, i, sU, row, lane, kp, F, G, S);
+        if (KIND != 0 || DG_HSPLIT == 0) {
 #pragma unroll
-        for (int j = 0; j < N; ++j) {
-            double e = KIND ? S[j] : 0.0;
+            for (int j = 0; j < N; ++j) {
+                double e = KIND ? S[j] : 0.0;
 #pragma unroll
-            for (int k = 0; k < N; ++k) e = fma(c_nod[P].dh[j][k], G[k], e);
-            sE[(i * N + j) * kLanes + lane] = e;
+                for (int k = 0; k < N; ++k) e = fma(c_nod[P].dh[j][k], G[k], e);
+                sE[(i * N + j) * kLanes + lane] = e;
+            }
         }
+        if constexpr (DG_HSPLIT != 0 && KIND == DG_HSPLIT) {
+            // the h equation's row-local term (G = hv cos/R) for the h warp,
+            // whose face work leaves it the longest volume phase
+            constexpr int NP = N * N;
+            using RL = RowLayout<P>;
+            double gh[N];
 #pragma unroll
-        for (int ii = 0; ii < N; ++ii) {
-            const double d = kp.dx[ii][i];
+            for (int k = 0; k < N; ++k) gh[k] = sU[(2 * NP + i * N + k) * kLanes + lane] * row[RL::CRC + k];
+            double *sEh = sE - KIND * NP * kLanes;
 #pragma unroll
-            for (int j = 0; j < N; ++j) acc[ii][j] = fma(d, F[j], acc[ii][j]);
+            for (int j = 0; j < N; ++j) {
+                double e = c_nod[P].dh[j][0] * gh[0];
+#pragma unroll
+                for (int k = 1; k < N; ++k) e = fma(c_nod[P].dh[j][k], gh[k], e);
+                sEh[(i * N + j) * kLanes + lane] = e;
+            }
+        }
+        if constexpr (KIND != 0 || DG_HSPLIT == 0 || true) {
+#pragma unroll
+            for (int ii = 0; ii < N; ++ii) {
+                const double d = kp.dx[ii][i];
+#pragma unroll
+                for (int j = 0; j < N; ++j) acc[ii][j] = fma(d, F[j], acc[ii][j]);
+            }
         }
     }
 }
@@ -841,17 +869,13 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
     const int r_last = min(kp.nrows - 1, kp.ny - 1 - kp.row0);
     const int last_fetch = min(je, r_last);        // rows jb..last_fetch stream through the ring
 
+    // programmatic dependent launch: the next stage's CTAs may become
+    // resident as ours retire; they run the state-independent prologue
+    // (barriers, row tables) and wait for this grid before touching states
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x == 0) {
         for (int k = 0; k < 6; ++k) mbar_init(mbar + k, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    // prologue: the var warps' elected lanes start streaming rows jb, jb+1
-    if (!face_warp && lane == 0) {
-        tma_row(ring0, Xz + (size_t)jb * kp.rstride, kTileBytes, mbar + v);
-        if (jb + 1 <= last_fetch)
-            tma_row(ring0 + SM::TILE, Xz + (size_t)(jb + 1) * kp.rstride, kTileBytes, mbar + 3 + v);
     }
 
     // row-table ring: slot (r - jb) % 3 holds local row r (rows jb, jb+1 now,
@@ -863,6 +887,15 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             const int r = idx / RL::SSTRIDE;
             sRow[idx] = kp.rowtab[(size_t)(gfirst + r) * RL::STRIDE + (idx - r * RL::SSTRIDE)];
         }
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // the previous stage's outputs are visible
+    __syncthreads();
+
+    // prologue: the var warps' elected lanes start streaming rows jb, jb+1
+    if (!face_warp && lane == 0) {
+        tma_row(ring0, Xz + (size_t)jb * kp.rstride, kTileBytes, mbar + v);
+        if (jb + 1 <= last_fetch)
+            tma_row(ring0 + SM::TILE, Xz + (size_t)(jb + 1) * kp.rstride, kTileBytes, mbar + 3 + v);
     }
 
     double alpha_x = kp.alpha, alpha_y = kp.alpha;
@@ -950,6 +983,10 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             cp_wait_all();                             // gathers of this row's phase B (and row tables)
             __syncwarp();
             if (it + 1 < je) {
+                if (DG_FCHECK) {   // positivity of row it+1's interior h nodes (off the h warp's path)
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) bad |= owned & !(next_tile[q * kLanes + lane] > 0.0);
+                }
                 border_traces<P>(smem + SM::HB, next_tile, smem + SM::HL, smem + SM::E0, smem + SM::HR, lane);
                 // every lane computes the same face (uniform control flow, identical stores)
                 face_flux_call<P>(SM::HL, 1, 0, SM::E0, 1, 0, SM::F0 + ((k + 1) & 1) * 3 * N, 1, 0,
