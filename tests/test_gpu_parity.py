@@ -501,3 +501,61 @@ def test_c4_shape_conservation(P):
     assert abs(P.mass_integral(st, op) - m0) <= 1e-13 * abs(m0)
     mh0 = P.mass_integral(st, op, "hu")
     assert np.isfinite(mh0)
+
+
+@pytest.mark.parametrize("p", [0, 1, 3, 4, 6])
+def test_nodal_basis_conversion(P, p):
+    """dgswe_convert: modal -> nodal gives the modal expansion at the Gauss
+    nodes (basis.py:118-133 evaluation), and back recovers the
+    coefficients; padding lanes stay zero."""
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=37, ny=8, p=p, nz=2))
+    op = P.SpatialOperator(setup.mesh, p, setup.model, nz=2)
+    st = op.project_state(setup.ic)
+    st.data[1] *= 1.0001
+    c0 = st.data.clone()
+    n = p + 1
+    leg = np.asarray(op.vander.phi).reshape(n, n, n, n)   # [qi][qj][a][b] = P_a(x_qi) P_b(x_qj)
+    op._ctx.convert(st.data, True, 0, 8)
+    got = st.data.cpu().numpy()
+    want = np.einsum("ijab,zrvsabl->zrvsijl", leg, c0.cpu().numpy().reshape(got.shape[:4] + (n, n, 32)))
+    want = want.reshape(got.shape)
+    assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max()
+    op._ctx.convert(st.data, False, 0, 8)
+    back = st.data.cpu().numpy()
+    ref = c0.cpu().numpy()
+    assert np.abs(back - ref).max() <= 1e-13 * np.abs(ref).max()
+    pad = st.data.view(got.shape[:4] + (n * n, 32))[..., 37 % 32:][:, :, :, -1]
+    assert float(pad.abs().max()) == 0.0
+
+
+def test_nodal_basis_entry_points(P):
+    """dgswe_set_basis(1): the stage and rk entry points take nodal states
+    unchanged; converting around them reproduces the modal-basis calls
+    (bit for bit for the step batch, to rounding for a single stage)."""
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=64, ny=20, p=3))
+    op = P.SpatialOperator(setup.mesh, 3, setup.model)
+    st = op.project_state(setup.ic)
+    a = st.copy()
+    op.ssprk3_steps(a, 20.0, 3)                   # modal basis: converts around the batch
+    b = st.copy()
+    ctx = op._ctx
+    ctx.convert(b.data, True, 0, 20)
+    ctx.set_basis(True)
+    try:
+        op.ssprk3_steps(b, 20.0, 3)
+        y = op.zero_state()
+        x = b.copy()
+        op.stage(0.0, None, 1.0, x, 20.0, y)      # nodal in, nodal out
+    finally:
+        ctx.set_basis(False)
+    ctx.convert(b.data, False, 0, 20)
+    assert torch.equal(a.data, b.data)
+    ctx.convert(y.data, False, 0, 20)
+    ym = op.zero_state()
+    xm = b.copy()
+    ctx.convert(x.data, False, 0, 20)
+    op.stage(0.0, None, 1.0, x, 20.0, ym)         # modal in, modal out
+    d = (y.data - ym.data).abs().max().item()
+    assert d <= 1e-13 * ym.data.abs().max().item()
+    assert op.status()[0] == 0
+    del xm
