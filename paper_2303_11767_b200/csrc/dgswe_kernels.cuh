@@ -131,6 +131,9 @@ __host__ __device__ inline int row_stride(int p) { return 4 * (p + 1) + 2 + (p +
 #endif
 template <int P>
 __host__ __device__ constexpr bool vol_rolled() { return DG_VROLL < 0 ? P >= 3 : DG_VROLL != 0; }
+#ifndef DG_ROWHOIST
+#define DG_ROWHOIST 1  // the rolled volume loop keeps the row's physics factors in registers (+1%)
+#endif
 #ifndef DG_FCHECK
 #define DG_FCHECK 0  // 1: the face warp checks the interior h nodes (the h warp only the traces)
 #endif
@@ -479,6 +482,32 @@ __device__ __forceinline__ void face_flux_call(int in_off, int in_ld, int in_col
 }
 
 
+// per-row factors of the physics, read from the staged row table or held
+// in registers across a row's node loop (DG_ROWHOIST)
+template <int P>
+struct RowRef {
+    const double *p;
+    __device__ __forceinline__ double crc(int q) const { return p[RowLayout<P>::CRC + q]; }
+    __device__ __forceinline__ double srs(int q) const { return p[RowLayout<P>::SRS + q]; }
+    __device__ __forceinline__ double fcs(int q) const { return p[RowLayout<P>::FCS + q]; }
+};
+template <int P>
+struct RowRegs {
+    double c[P + 1], s[P + 1], f[P + 1];
+    __device__ __forceinline__ RowRegs(const double *p)
+    {
+#pragma unroll
+        for (int q = 0; q < P + 1; ++q) {
+            c[q] = p[RowLayout<P>::CRC + q];
+            s[q] = p[RowLayout<P>::SRS + q];
+            f[q] = p[RowLayout<P>::FCS + q];
+        }
+    }
+    __device__ __forceinline__ double crc(int q) const { return c[q]; }
+    __device__ __forceinline__ double srs(int q) const { return s[q]; }
+    __device__ __forceinline__ double fcs(int q) const { return f[q]; }
+};
+
 // Pointwise flux / source at the N nodes (qi, qj), qj = 0..N-1
 // (models.py:161-252): F = x-flux (its cx/R goes into the xi weights),
 // G = y-flux * cy cos/R, S = source, for the equation of KIND:
@@ -488,8 +517,8 @@ __device__ __forceinline__ void face_flux_call(int in_off, int in_ld, int in_col
 //   3:    hu or hv by the uniform flag is_v, one branch-free code path
 //         (the unrolled volume, where a second copy would cost I-cache)
 // with u = hu/hf, w = hv/hf, t = u sin/R + 2 Omega sin cos.
-template <int P, int KIND>
-__device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU, const double *row, int lane,
+template <int P, int KIND, typename RT>
+__device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU, const RT &row, int lane,
                                              const StageParams &kp, double (&F)[P + 1],
                                              double (&G)[P + 1], double (&S)[P + 1])
 {
@@ -501,7 +530,7 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
         const int q = qi * N + qj;
         const double hu = sU[(1 * NP + q) * kLanes + lane];
         const double hv = sU[(2 * NP + q) * kLanes + lane];
-        const double crc = row[RL::CRC + qj];
+        const double crc = row.crc(qj);
         if constexpr (KIND == 0) {
             F[qj] = hu;
             G[qj] = hv * crc;
@@ -516,8 +545,8 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
 #endif
             const double gh2 = h * h * kp.half_g;
             const double u = hu * r, w = hv * r;
-            const double srs = row[RL::SRS + qj];
-            const double t = fma(u, srs, row[RL::FCS + qj]);
+            const double srs = row.srs(qj);
+            const double t = fma(u, srs, row.fcs(qj));
             if constexpr (KIND == 1) {
                 F[qj] = fma(hu, u, gh2);
                 G[qj] = (hu * w) * crc;
@@ -550,7 +579,7 @@ __device__ __forceinline__ void volume(double (&acc)[P + 1][P + 1], int v, const
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         double F[N], G[N], S[N];
-        node_physics<P, MOM ? 3 : 0>(v == 2, i, sU, row, lane, kp, F, G, S);
+        node_physics<P, MOM ? 3 : 0>(v == 2, i, sU, RowRef<P>{row}, lane, kp, F, G, S);
 #pragma unroll
         for (int j = 0; j < N; ++j) {
             double e = MOM ? S[j] : 0.0;
@@ -580,10 +609,15 @@ __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v
     for (int ii = 0; ii < N; ++ii)
 #pragma unroll
         for (int j = 0; j < N; ++j) acc[ii][j] = 0.0;
+#if DG_ROWHOIST
+    const RowRegs<P> rr(row);
+#else
+    const RowRef<P> rr{row};
+#endif
 #pragma unroll 1
     for (int i = 0; i < N; ++i) {
         double F[N], G[N], S[N];
-        node_physics<P, KIND>(false, i, sU, row, lane, kp, F, G, S);
+        node_physics<P, KIND>(false, i, sU, rr, lane, kp, F, G, S);
         if (KIND != 0 || DG_HSPLIT == 0) {
 #pragma unroll
             for (int j = 0; j < N; ++j) {
@@ -600,7 +634,7 @@ __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v
             using RL = RowLayout<P>;
             double gh[N];
 #pragma unroll
-            for (int k = 0; k < N; ++k) gh[k] = sU[(2 * NP + i * N + k) * kLanes + lane] * row[RL::CRC + k];
+            for (int k = 0; k < N; ++k) gh[k] = sU[(2 * NP + i * N + k) * kLanes + lane] * rr.crc(k);
             double *sEh = sE - KIND * NP * kLanes;
 #pragma unroll
             for (int j = 0; j < N; ++j) {
@@ -673,7 +707,6 @@ __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const 
         }
     }
     const double *rj = row + RL::RJ;
-    int fexp = 0;                     // max exponent field of the outputs (integer pipe)
 #pragma unroll
     for (int j = 0; j < N; ++j) {
         const double gr = kp.g * rj[j];
@@ -686,7 +719,6 @@ __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const 
             if (owned) Yv[(i * N + j) * kLanes] = y;
             if (owned && Ypeer) Ypeer[(i * N + j) * kLanes] = y;   // fused halo exchange (NVLink store)
             if (owned && Ypeer2) Ypeer2[(i * N + j) * kLanes] = y;
-            fexp = max(fexp, __double2hiint(y) & 0x7ff00000);
             if constexpr (HAS_Y2) {
                 const double y2 = fma(g2r, k, an[i][j]);
                 if (owned) Y2v[(i * N + j) * kLanes] = y2;
@@ -696,7 +728,14 @@ __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const 
     }
     unsigned bad = 0;
     if (owned) {
-        bad |= (kp.check_finite && fexp == 0x7ff00000) ? 2u : 0u;   // Inf or NaN
+        if (kp.check_finite) {   // Inf or NaN: max exponent field of the outputs (integer pipe)
+            int fexp = 0;
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+#pragma unroll
+                for (int j = 0; j < N; ++j) fexp = max(fexp, __double2hiint(acc[i][j]) & 0x7ff00000);
+            bad |= fexp == 0x7ff00000 ? 2u : 0u;
+        }
         if (v == 0 && kp.check_mean) {   // cell mean = modal c_00 = sum w_i w_j u_ij / 4
             double m = 0.0;
 #pragma unroll
