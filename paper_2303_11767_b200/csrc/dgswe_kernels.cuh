@@ -121,9 +121,6 @@ __host__ __device__ inline int row_stride(int p) { return 4 * (p + 1) + 2 + (p +
 #ifndef DG_SELFLOOR
 #define DG_SELFLOOR 1   // 1/max(h, floor) as rcp(h) + select: the reciprocal starts at once
 #endif
-#ifndef DG_VOL_UNROLL
-#define DG_VOL_UNROLL 0
-#endif
 #ifndef DG_VROLL
 #define DG_VROLL -1  // volume loop over node rows kept rolled (row-local terms through shared memory):
                      // -1 = for p >= 3 (a quarter of the unrolled code: measured +1% at p=3, +6% at
@@ -133,9 +130,6 @@ template <int P>
 __host__ __device__ constexpr bool vol_rolled() { return DG_VROLL < 0 ? P >= 3 : DG_VROLL != 0; }
 #ifndef DG_ROWHOIST
 #define DG_ROWHOIST 1  // the rolled volume loop keeps the row's physics factors in registers (+1%)
-#endif
-#ifndef DG_FCHECK
-#define DG_FCHECK 0  // 1: the face warp checks the interior h nodes (the h warp only the traces)
 #endif
 #ifndef DG_HSPLIT
 #define DG_HSPLIT 2  // 1 / 2: the hu / hv warp also computes the h equation's row-local volume term (2: +0.4% at C3)
@@ -374,11 +368,10 @@ __device__ __forceinline__ unsigned traces_row(const double (&u)[P + 1][P + 1], 
     if (check) {
 #pragma unroll
         for (int q = 0; q < N; ++q) bad |= !(l[q] > 0.0) | !(r[q] > 0.0) | !(t[q] > 0.0);
-        if (!DG_FCHECK)
 #pragma unroll
-            for (int i = 0; i < N; ++i)
+        for (int i = 0; i < N; ++i)
 #pragma unroll
-                for (int j = 0; j < N; ++j) bad |= !(u[i][j] > 0.0);
+            for (int j = 0; j < N; ++j) bad |= !(u[i][j] > 0.0);
     }
     return bad;
 }
@@ -837,20 +830,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
     // fixed roles: warp w runs on sub-partition w of its SM, so every
     // sub-partition executes a single code path (better I-cache locality
     // than rotating roles, measured)
-#if DG_ROLEMIX
-    // experiment: rotate the role map by the CTA's warp-slot group so the
-    // resident CTAs spread each role over the sub-partitions
-    __shared__ int s_rot;
-    if (threadIdx.x == 0) {
-        unsigned wid;
-        asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
-        s_rot = (int)((wid >> 2) & 3u);
-    }
-    __syncthreads();
-    const int role = ((int)(threadIdx.x >> 5) + s_rot) & 3;
-#else
     const int role = threadIdx.x >> 5;
-#endif
     const int v = role < kVarWarps ? role : 0;     // face warp borrows var 0's addressing
     const bool face_warp = role == kVarWarps;
     const int lane = threadIdx.x & 31;
@@ -1022,10 +1002,6 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             cp_wait_all();                             // gathers of this row's phase B (and row tables)
             __syncwarp();
             if (it + 1 < je) {
-                if (DG_FCHECK) {   // positivity of row it+1's interior h nodes (off the h warp's path)
-#pragma unroll
-                    for (int q = 0; q < NP; ++q) bad |= owned & !(next_tile[q * kLanes + lane] > 0.0);
-                }
                 border_traces<P>(smem + SM::HB, next_tile, smem + SM::HL, smem + SM::E0, smem + SM::HR, lane);
                 // every lane computes the same face (uniform control flow, identical stores)
                 face_flux_call<P>(SM::HL, 1, 0, SM::E0, 1, 0, SM::F0 + ((k + 1) & 1) * 3 * N, 1, 0,
