@@ -123,11 +123,11 @@ __host__ __device__ inline int row_stride(int p) { return 4 * (p + 1) + 2 + (p +
 #endif
 #ifndef DG_VROLL
 #define DG_VROLL -1  // volume loop over node rows kept rolled (row-local terms through shared memory):
-                     // -1 = for p >= 3 (a quarter of the unrolled code: measured +1% at p=3, +6% at
-                     // p=4, -2% at p=2), 0 = never, 1 = always
+                     // -1 = for p >= 2 (a quarter of the unrolled code; with the per-equation
+                     // physics +0.2% at p=2, p=3/4 see DESIGN.md; -3.5% at p=1), 0 = never, 1 = always
 #endif
 template <int P>
-__host__ __device__ constexpr bool vol_rolled() { return DG_VROLL < 0 ? P >= 3 : DG_VROLL != 0; }
+__host__ __device__ constexpr bool vol_rolled() { return DG_VROLL < 0 ? P >= 2 : DG_VROLL != 0; }
 #ifndef DG_ROWHOIST
 #define DG_ROWHOIST 1  // the rolled volume loop keeps the row's physics factors in registers (+1%)
 #endif
