@@ -197,9 +197,9 @@ class BandOperator:
             raise ValueError("transport 'fused' supports local / pinned alpha only")
         # the fused transport still exchanges u's halos once per step batch
         # (begin), over NCCL -- or the host when the group is gloo
-        hx = transport
-        if transport == "fused":
-            hx = "host" if dist.is_initialized() and dist.get_backend(group) == "gloo" else "p2p"
+        hx = "p2p" if transport == "fused" else transport
+        if hx == "p2p" and dist.is_initialized() and dist.get_backend(group) == "gloo":
+            hx = "host"                # gloo moves host memory only
         self.halo = HaloExchange(layout, hx, group)
         self._owned_mem = []       # (ptr, keep-alive) of library allocations
         self._opened = []          # peer mappings to close
