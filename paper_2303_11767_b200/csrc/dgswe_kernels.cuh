@@ -7,24 +7,23 @@
 // nphi * 256 bytes: it moves with ONE TMA bulk copy (cp.async.bulk +
 // mbarrier), its L2 prefetch is one bulk-prefetch instruction, and every
 // per-lane load/store inside it is an immediate offset from one base.
+// Inside a step the slot of mode (a, b) holds the value at Gauss node
+// (i, j) instead (convert_kernel; DESIGN.md section 3 "Nodal form").
 //
 // One CTA = 4 warps x 32 lanes on one strip: warp v < 3 owns variable v in
-// {h, hu, hv}; warp 0 (lightest physics) also evaluates the row's x-faces
-// 1..32 and warp 3 (the face warp) the y-face above the row, the strip's
-// two halo traces and its left border face 0.  Lane l owns element
-// 32*strip + l.  The CTA marches north through a chunk of latitude rows.
+// {h, hu, hv}; warp 0 also evaluates the row's x-faces 1..32 and warp 3
+// (the face warp) the y-face above the row, the strip's two halo traces and
+// its left border face 0.  Lane l owns element 32*strip + l.  The CTA
+// marches north through a chunk of latitude rows.
 //
-// Per row, per variable and lane (n = p+1, all tensor contractions
-// sum-factorised with the even/odd split; constant tables in __constant__):
-//   1. modal -> nodal: t[a][qj] = sum_b c[a][b] P_b(x_qj),
-//      U[qi][qj] = sum_a P_a(x_qi) t[a][qj]; traces L/R from t, T/B from
-//      sum_b c[a][b](+-1)^b                          (dg.py:348-357)
-//   2. nodal values exchanged through shared memory; pointwise flux /
-//      source physics for this warp's variable      (models.py:161-252)
-//   3. Rusanov fluxes with local alpha               (dg.py:92-119,385-453)
-//   4. volume + source projection streamed over xi node pairs, boundary
-//      lifts, per-row inverse mass (Kronecker block form), fused RK stage
-//      update (dg.py:455-502, timestep.py:132-167)
+// Per row, per variable and lane (n = p+1; constant tables in __constant__):
+//   1. traces L/R/T (and B of the next row) of the nodal tile: one n-point
+//      dot product each                               (dg.py:348-357)
+//   2. pointwise flux / source physics at the nodes    (models.py:161-252)
+//   3. Rusanov fluxes with local alpha                 (dg.py:92-119,385-453)
+//   4. weak derivatives of the fluxes (W^-1 D^T W per direction), source,
+//      face lifts, the diagonal nodal mass and the fused RK stage update
+//      (dg.py:455-502, timestep.py:132-167)
 //
 // Floating point: FMA contraction, refined MUFU reciprocals and a different
 // summation order than the reference; results agree with the reference's
@@ -113,11 +112,8 @@ __host__ __device__ inline int row_stride(int p) { return 4 * (p + 1) + 2 + (p +
 #define WP(a, q) c_tab[P][2][a][q]
 #define WD(a, q) c_tab[P][3][a][q]
 
-// Gauss nodes are exactly antisymmetric (numpy's leggauss symmetrises them)
-// and the Legendre recurrences are odd/even in x, so the tables satisfy
-//   T(a, N-1-q) = (-1)^(a + PAR) T(a, q)   exactly,
-// PAR = 0 for P and wP, 1 for P' and wP'.  Every 1-D contraction below
-// uses this even/odd split: N adds + N*ceil(N/2) FMA instead of N*N.
+// (the Legendre tables serve the basis conversions; the stage kernel uses
+// the nodal tables c_nod below)
 #ifndef DG_SELFLOOR
 #define DG_SELFLOOR 1   // 1/max(h, floor) as rcp(h) + select: the reciprocal starts at once
 #endif
