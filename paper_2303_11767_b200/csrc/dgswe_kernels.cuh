@@ -110,7 +110,6 @@ __host__ __device__ inline int row_stride(int p) { return 4 * (p + 1) + 2 + (p +
 
 #define LEG(a, q) c_tab[P][0][a][q]
 #define WP(a, q) c_tab[P][2][a][q]
-#define WD(a, q) c_tab[P][3][a][q]
 
 // (the Legendre tables serve the basis conversions; the stage kernel uses
 // the nodal tables c_nod below)
@@ -653,8 +652,8 @@ template <int P, bool HAS_U, bool HAS_Y2>
 __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const double *cur,
                                              const double *Uv, const double *Av, double *Y2v, int v,
                                              const double *sFX, const double *sF0,
-                                             const double *sFtop, const double *sFbot, bool has_top,
-                                             bool has_bot, const double *row, int lane, bool owned,
+                                             const double *sFtop, const double *sFbot,
+                                             const double *row, int lane, bool owned,
                                              double *Yv, const StageParams &kp, double *Ypeer = nullptr,
                                              double *Ypeer2 = nullptr)
 {
@@ -686,8 +685,8 @@ __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const 
     for (int q = 0; q < N; ++q) {
         const double l = lane == 0 ? sF0[v * N + q] : sFX[o + q * kLanes + ((lane + kLanes - 1) & (kLanes - 1))];
         const double r = sFX[o + q * kLanes + lane];
-        const double t = has_top ? sFtop[o + q * kLanes + lane] : 0.0;   // pole faces carry
-        const double bo = has_bot ? sFbot[o + q * kLanes + lane] : 0.0;  // no flux (dg.py:483-495)
+        const double t = sFtop[o + q * kLanes + lane];     // zero at a pole (the face warp)
+        const double bo = sFbot[o + q * kLanes + lane];
 #pragma unroll
         for (int k = 0; k < N; ++k) {
             // x faces at eta node q lift along xi (column q); y faces at xi node q along eta (row q)
@@ -986,6 +985,11 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
                                            kp.alpha_mode, 1, above[RL::CRB], above[RL::COSB], alpha_y,
                                            kp.bdx});
+            } else {
+                // a pole: no face, no flux (dg.py:483-495) -- the lift reads zeros
+                double *dst = pre ? fb : fa;
+#pragma unroll
+                for (int q = 0; q < 3 * N; ++q) dst[q * kLanes + lane] = 0.0;
             }
             TSTAMP(c);
             __syncthreads();                           // barrier 2 of row it (prologue barrier B)
@@ -1018,9 +1022,6 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             const int k = jl - jb;
             const int slot = k & 1;
             double *const cur = ring0 + slot * SM::TILE;
-            const int jg = kp.row0 + jl;
-            const bool has_top = jg + 1 < kp.ny;
-            const bool has_bot = jg > 0;
             const double *row = sRow + (k % 3) * RL::SSTRIDE;
             TSTAMP(s);
 
@@ -1085,7 +1086,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             }
             bad |= finalize<P, HAS_U, HAS_Y2>(vol, cur, HAS_U ? Uz + roff : nullptr,
                                               HAS_Y2 ? Az + roff : nullptr, HAS_Y2 ? Y2z + roff : nullptr, v, sFX,
-                                      smem + SM::F0 + slot * 3 * N, sFa, sFb, has_top, has_bot, row, lane,
+                                      smem + SM::F0 + slot * 3 * N, sFa, sFb, row, lane,
                                       owned, Yz + roff, kp, Ypeer, Ypeer2);
             // X(jl) is consumed: stream row jl+2 into its slot (L2-warm by now)
             __syncwarp();
@@ -1182,6 +1183,5 @@ __global__ void __launch_bounds__(96) convert_kernel(const double *in, double *o
 
 #undef LEG
 #undef WP
-#undef WD
 
 }  // namespace dgswe
