@@ -179,6 +179,15 @@ int dgswe_ipc_close(void *p);
 int dgswe_stage_rows2(dgswe_ctx *ctx, double a, const double *U, double b, const double *X,
                       double g, double *Y, int tag, int r0, int r1, int r2, int r3, void *stream);
 
+/* Nodal basis only: Y = a*U + b*X + g*RHS(X) on local rows [r0, r1) with the
+ * status checks of a step's last stage (non-finite output, optional cell
+ * mean) -- the row-pipelined host-state step of the Python API
+ * (SpatialOperator.ssprk3_step_host: host<->device copies overlapped with
+ * the stages of row chunks). */
+int dgswe_stage_rows_checked(dgswe_ctx *ctx, double a, const double *U, double b, const double *X,
+                             double g, double *Y, int tag, int r0, int r1, int check_finite,
+                             int check_mean, void *stream);
+
 /* Y = a*U + b*X + g*RHS(X) and Y2 = A + g2*RHS(X) in one launch, on local
  * rows [r0, r1): the stage of classical RK4 whose second output is the
  * running accumulator u + sum_i dt b_i k_i (timestep.py:71-81, 163-164).

@@ -56,6 +56,7 @@ SIGNATURES = {
     "dgswe_stage": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _VP]),
     "dgswe_stage_rows": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _I, _I, _VP]),
     "dgswe_stage_rows2": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _I, _I, _I, _I, _VP]),
+    "dgswe_stage_rows_checked": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _I, _I, _I, _I, _VP]),
     "dgswe_set_exchange": (_I, [_VP, ctypes.c_longlong, _VP, ctypes.c_longlong, _VP, _VP, _VP]),
     "dgswe_stage_edge": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _VP, _VP, _VP]),
     "dgswe_dev_alloc": (_I, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),

@@ -731,6 +731,16 @@ int dgswe_stage_rows2(dgswe_ctx *ctx, double a, const double *U, double b, const
     return api_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, r0, r1, (cudaStream_t)stream, r2, r3);
 }
 
+int dgswe_stage_rows_checked(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g,
+                             double *Y, int tag, int r0, int r1, int check_finite, int check_mean,
+                             void *stream)
+{
+    if (!ctx) return fail(DGSWE_EINVAL, "null context");
+    if (!ctx->basis) return fail(DGSWE_EINVAL, "checked row stages take nodal states (dgswe_set_basis)");
+    return launch_stage(ctx, a, U, b, X, g, Y, nullptr, 0.0, nullptr, tag, r0, r1, check_finite ? 1 : 0,
+                        check_mean ? 1 : 0, (cudaStream_t)stream);
+}
+
 int dgswe_stage2(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g,
                  double *Y, const double *A, double g2, double *Y2, int tag, int r0, int r1, void *stream)
 {

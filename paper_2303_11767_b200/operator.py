@@ -365,7 +365,8 @@ class SpatialOperator:
         if ws is None:
             # zeroed once: the strip padding past nx is read but never written
             ws = tuple(torch.zeros_like(state.data) for _ in range(3))
-            self._scratch = {key: ws}
+            self._scratch = {k: v for k, v in self._scratch.items() if not isinstance(k, int)}
+            self._scratch[key] = ws
         c = self._ctx
         _lib.check(c.lib.dgswe_rk_steps(c.h, int(order), _ptr(state.data), _ptr(ws[0]), _ptr(ws[1]),
                                         _ptr(ws[2]), float(dt), int(nsteps), int(check_mean), c.stream()),
@@ -374,6 +375,100 @@ class SpatialOperator:
     def ssprk3_steps(self, state: State, dt: float, nsteps: int, check_mean: bool = False):
         """nsteps fused Shu-Osher SSPRK3 steps in place (one CUDA graph)."""
         self.rk_steps(state, dt, nsteps, 3, check_mean)
+
+    def ssprk3_step_host(self, host: torch.Tensor, dt: float, tag: int = 0, check_mean: bool = False,
+                         chunks: int | None = None, graph: bool = True):
+        """One SSPRK3 step of a host-resident (pinned) modal state, in place:
+        the reference's ``rk_step`` contract on a host array
+        (timestep.py:149-167), row-pipelined.  The state moves in latitude
+        chunks; chunk c's host->device copy, chunk c-1's stage 1, c-2's
+        stage 2, c-3's stage 3 and the device->host copy of finished chunks
+        overlap (two copy streams: PCIe is full duplex).  Bitwise equal to
+        ``ssprk3_steps(state, dt, 1)`` on the device copy.  Enqueued on the
+        current stream (which waits for the last copy); ``status()`` syncs.
+        With ``graph`` the ~10 launches per chunk are captured once per
+        (host buffer, dt, tag, check_mean) and replayed as one CUDA graph."""
+        if graph:
+            gkey = ("hostgraph", host.data_ptr(), float(dt), int(tag), bool(check_mean), chunks)
+            g = self._scratch.get(gkey)
+            if g is None:
+                if sum(1 for k in self._scratch if isinstance(k, tuple) and k[0] == "hostgraph") >= 8:
+                    for k in [k for k in self._scratch if isinstance(k, tuple) and k[0] == "hostgraph"]:
+                        del self._scratch[k]
+                self.ssprk3_step_host(host, dt, tag, check_mean, chunks, graph=False)   # warm-up step
+                torch.cuda.current_stream().synchronize()
+                g = torch.cuda.CUDAGraph()             # captured, not run: this call's step was the eager one
+                with torch.cuda.graph(g):
+                    self.ssprk3_step_host(host, dt, tag, check_mean, chunks, graph=False)
+                self._scratch[gkey] = g
+                return
+            g.replay()
+            return
+        mesh = self.mesh
+        ny, nz = mesh.ny, self.nz
+        if tuple(host.shape) != tuple(self.state_shape) or host.dtype != torch.float64:
+            raise ValueError(f"host state must be float64 {tuple(self.state_shape)}")
+        if self.rusanov.mode == "global" and self.rusanov.alpha is None:
+            raise ValueError("global-alpha mode needs the whole state before a stage: use ssprk3_steps")
+        nch = chunks if chunks is not None else max(1, min(16, ny // 4))
+        bounds = [ny * c // nch for c in range(nch + 1)]
+        key = ("host", tuple(host.shape))
+        ws = self._scratch.get(key)
+        if ws is None:
+            ws = tuple(torch.zeros(self.state_shape, dtype=torch.float64, device=self.device) for _ in range(3))
+            ws = ws + (torch.cuda.Stream(), torch.cuda.Stream())
+            self._scratch[key] = ws
+        u, w1, w2, s_in, s_out = ws
+        c = self._ctx
+        cur = torch.cuda.current_stream()
+        s_in.wait_stream(cur)
+        s_out.wait_stream(cur)
+        ev_in = [torch.cuda.Event() for _ in range(nch)]
+
+        def rows(k):
+            return bounds[k], bounds[k + 1]
+
+        def launch(fn, a, U, b, X, g, Y, k, last=False):
+            r0, r1 = rows(k)
+            if last:
+                _lib.check(c.lib.dgswe_stage_rows_checked(
+                    c.h, float(a), _ptr(U), float(b), _ptr(X), float(g), _ptr(Y), int(tag), r0, r1, 1,
+                    int(check_mean), c.stream()), "dgswe_stage_rows_checked")
+            else:
+                _lib.check(c.lib.dgswe_stage_rows(
+                    c.h, float(a), _ptr(U), float(b), _ptr(X), float(g), _ptr(Y), int(tag), r0, r1,
+                    c.stream()), "dgswe_stage_rows")
+
+        c.set_basis(True)
+        try:
+            for it in range(nch + 3):
+                if it < nch:
+                    r0, r1 = rows(it)
+                    with torch.cuda.stream(s_in):
+                        for z in range(nz):
+                            u[z, r0:r1].copy_(host[z, r0:r1], non_blocking=True)
+                        ev_in[it].record(s_in)
+                    cur.wait_event(ev_in[it])
+                    c.convert(u, True, r0, r1)
+                if 0 <= it - 1 < nch:
+                    launch(None, 0.0, None, 1.0, u, dt, w1, it - 1)
+                if 0 <= it - 2 < nch:
+                    launch(None, 0.75, u, 0.25, w1, 0.25 * dt, w2, it - 2)
+                k3 = it - 3
+                if 0 <= k3 < nch:
+                    launch(None, 1.0 / 3.0, u, 2.0 / 3.0, w2, (2.0 / 3.0) * dt, u, k3, last=True)
+                    r0, r1 = rows(k3)
+                    c.convert(u, False, r0, r1)
+                    ev = torch.cuda.Event()
+                    ev.record(cur)
+                    s_out.wait_event(ev)
+                    with torch.cuda.stream(s_out):
+                        for z in range(nz):
+                            host[z, r0:r1].copy_(u[z, r0:r1], non_blocking=True)
+        finally:
+            c.set_basis(False)
+        cur.wait_stream(s_out)
+        cur.wait_stream(s_in)
 
     def stage2(self, a: float, U: State | None, b: float, X: State, g: float, Y: State, A: State,
                g2: float, Y2: State, tag: int = 0):

@@ -559,3 +559,28 @@ def test_nodal_basis_entry_points(P):
     assert d <= 1e-13 * ym.data.abs().max().item()
     assert op.status()[0] == 0
     del xm
+
+
+@pytest.mark.parametrize("case,nx,ny,p,nz,chunks", [("williamson_tc6", 64, 40, 3, 1, None),
+                                                    ("williamson_tc6", 70, 21, 2, 2, 5),
+                                                    ("williamson_tc2", 40, 20, 4, 1, 3)])
+def test_host_state_step_pipelined(P, case, nx, ny, p, nz, chunks):
+    """ssprk3_step_host (row chunks: copies overlapped with the stages) is
+    bitwise the device step of the same state, and raises on positivity."""
+    setup = P.build_case(P.default_config(case).override(nx=nx, ny=ny, p=p, nz=nz))
+    op = P.SpatialOperator(setup.mesh, p, setup.model, nz=nz)
+    st = op.project_state(setup.ic)
+    if nz > 1:
+        st.data[1:] *= 1.0001
+    host = st.data.cpu().pin_memory()
+    dt = 5.0                                      # 5 steps well inside the polar-row CFL limit
+    for k in range(2):
+        op.ssprk3_step_host(host, dt, tag=k, chunks=chunks, graph=False)
+    for _ in range(3):                            # eager step + capture, then two replays
+        op.ssprk3_step_host(host, dt, chunks=chunks)
+    assert op.status()[0] == 0
+    op.ssprk3_steps(st, dt, 1)
+    op.ssprk3_steps(st, dt, 1)
+    for _ in range(3):
+        op.ssprk3_steps(st, dt, 1)
+    assert torch.equal(host, st.data.cpu())
