@@ -402,24 +402,28 @@ __device__ __forceinline__ void face_flux_body(int in_off, int in_ld, int in_col
 {
     constexpr int N = P + 1;
     extern __shared__ double smem[];
-    double in[3][N], out[3][N];
+    // variables by role: h, the normal momentum (hu across an x-face, hv
+    // across a y-face) and the tangential one, addressed through the
+    // runtime direction instead of per-node selects
+    const int vn = 1 + fa.dir, vt = 2 - fa.dir;
+    double hI[N], nI[N], tI[N], hO[N], nO[N], tO[N];
 #pragma unroll
-    for (int v = 0; v < 3; ++v)
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-            in[v][k] = smem[in_off + (v * N + k) * in_ld + in_col];
-            out[v][k] = smem[out_off + (v * N + k) * out_ld + out_col];
-        }
-    double rin[N], rout[N], mi[N], mo[N];
+    for (int k = 0; k < N; ++k) {
+        hI[k] = smem[in_off + k * in_ld + in_col];
+        nI[k] = smem[in_off + (vn * N + k) * in_ld + in_col];
+        tI[k] = smem[in_off + (vt * N + k) * in_ld + in_col];
+        hO[k] = smem[out_off + k * out_ld + out_col];
+        nO[k] = smem[out_off + (vn * N + k) * out_ld + out_col];
+        tO[k] = smem[out_off + (vt * N + k) * out_ld + out_col];
+    }
+    double rin[N], rout[N];
     double am[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         double ci, co;
-        inv_and_celerity(in[0][k], fa.h_floor, fa.inv_floor, fa.sqrt_g, rin[k], ci);
-        inv_and_celerity(out[0][k], fa.h_floor, fa.inv_floor, fa.sqrt_g, rout[k], co);
-        mi[k] = fa.dir == 0 ? in[1][k] : in[2][k];     // normal momentum
-        mo[k] = fa.dir == 0 ? out[1][k] : out[2][k];
-        am[k] = max_nn(fabs(mi[k] * rin[k]) + ci, fabs(mo[k] * rout[k]) + co);
+        inv_and_celerity(hI[k], fa.h_floor, fa.inv_floor, fa.sqrt_g, rin[k], ci);
+        inv_and_celerity(hO[k], fa.h_floor, fa.inv_floor, fa.sqrt_g, rout[k], co);
+        am[k] = max_nn(fabs(nI[k] * rin[k]) + ci, fabs(nO[k] * rout[k]) + co);
     }
 #pragma unroll
     for (int w = 1; w < N; w *= 2)
@@ -430,24 +434,16 @@ __device__ __forceinline__ void face_flux_body(int in_off, int in_ld, int in_col
     if (fa.alpha_mode != 0) alpha = fa.alpha_glob;
     const double ha = (0.5 * fa.scale) * alpha;
     const double hs = (0.5 * fa.scale) * (fa.dir == 0 ? fa.inv_r : fa.cr_e);
-    const double sx = fa.dir == 0 ? 1.0 : 0.0, sy = 1.0 - sx;
-    double fs[3][N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-        const double hi = in[0][k], ui = in[1][k], vi = in[2][k];
-        const double ho = out[0][k], uo = out[1][k], vo = out[2][k];
-        const double gi = hi * hi * fa.half_g, go = ho * ho * fa.half_g;
-        const double wi = mi[k] * rin[k], wo = mo[k] * rout[k];
-        const double fi1 = fma(ui, wi, sx * gi), fo1 = fma(uo, wo, sx * go);
-        const double fi2 = fma(vi, wi, sy * gi), fo2 = fma(vo, wo, sy * go);
-        fs[0][k] = fma(hs, mi[k] + mo[k], -ha * (ho - hi));
-        fs[1][k] = fma(hs, fi1 + fo1, -ha * (uo - ui));
-        fs[2][k] = fma(hs, fi2 + fo2, -ha * (vo - vi));
+        const double gi = hI[k] * hI[k] * fa.half_g, go = hO[k] * hO[k] * fa.half_g;
+        const double wi = nI[k] * rin[k], wo = nO[k] * rout[k];
+        const double fni = fma(nI[k], wi, gi), fno = fma(nO[k], wo, go);   // normal: m w + g h^2/2
+        const double fti = tI[k] * wi, fto = tO[k] * wo;                   // tangential: m_t w
+        smem[dst_off + k * dst_ld + dst_col] = fma(hs, nI[k] + nO[k], -ha * (hO[k] - hI[k]));
+        smem[dst_off + (vn * N + k) * dst_ld + dst_col] = fma(hs, fni + fno, -ha * (nO[k] - nI[k]));
+        smem[dst_off + (vt * N + k) * dst_ld + dst_col] = fma(hs, fti + fto, -ha * (tO[k] - tI[k]));
     }
-#pragma unroll
-    for (int v = 0; v < 3; ++v)
-#pragma unroll
-        for (int k = 0; k < N; ++k) smem[dst_off + (v * N + k) * dst_ld + dst_col] = fs[v][k];
 }
 
 template <int P>
