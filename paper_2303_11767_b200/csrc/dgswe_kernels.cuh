@@ -126,6 +126,9 @@ __host__ __device__ constexpr bool vol_rolled() { return DG_VROLL < 0 ? P >= 2 :
 #ifndef DG_ROWHOIST
 #define DG_ROWHOIST 1  // the rolled volume loop keeps the row's physics factors in registers (+1%)
 #endif
+#ifndef DG_ICMP
+#define DG_ICMP 1    // h-floor / celerity branches compared on the integer pipe
+#endif
 #ifndef DG_HSPLIT
 #define DG_HSPLIT 2  // 1 / 2: the hu / hv warp also computes the h equation's row-local volume term (2: +0.4% at C3)
 #endif
@@ -216,6 +219,15 @@ __device__ __forceinline__ double max_pos(double x, double y)
     return __longlong_as_double(xb > yb ? xb : yb);
 }
 
+// x >= y for y > 0 and x > 0 on the integer pipe (signed 64-bit order of
+// the bit patterns; differs from the fp64 compare only for NaN x, which the
+// positivity checks flag anyway)
+__device__ __forceinline__ bool ge_pos(double x, double y)
+{
+    return __double_as_longlong(x) >= __double_as_longlong(y);
+}
+__device__ __forceinline__ bool gt_zero(double x) { return __double_as_longlong(x) > 0; }
+
 // max of two non-negative values (same integer trick)
 __device__ __forceinline__ double max_nn(double x, double y) { return max_pos(x, y); }
 
@@ -247,8 +259,13 @@ __device__ __forceinline__ void inv_and_celerity(double h, double h_floor, doubl
                                                  double &r, double &c)
 {
     const double y = rsqrt64(max_pos(h, 2.2250738585072014e-308));
+#if DG_ICMP
+    r = ge_pos(h, h_floor) ? y * y : inv_floor;
+    c = gt_zero(h) ? sqrt_g * (h * y) : 0.0;
+#else
     r = h >= h_floor ? y * y : inv_floor;
     c = h > 0.0 ? sqrt_g * (h * y) : 0.0;
+#endif
 }
 
 // --- TMA bulk copies and mbarriers (one elected lane per variable warp) ---
@@ -523,7 +540,11 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
             const double h = sU[(0 * NP + q) * kLanes + lane];
 #if DG_SELFLOOR
             const double r0 = rcp64(h);
+#if DG_ICMP
+            const double r = ge_pos(h, kp.h_floor) ? r0 : kp.inv_floor;
+#else
             const double r = h >= kp.h_floor ? r0 : kp.inv_floor;
+#endif
 #else
             const double r = rcp64(max_pos(h, kp.h_floor));
 #endif
