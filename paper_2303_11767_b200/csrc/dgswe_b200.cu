@@ -259,6 +259,33 @@ int launch_stage_p(dgswe_ctx *c, const dgswe::StageParams &kp, int r0, int r1, c
                 best_chunks = ch;
             }
         }
+        // Second look, by the busiest SM's row work: CTAs share their SM's
+        // issue and FP64 throughput, so a one-wave grid that puts o CTAs on
+        // some SMs and o-1 on the others runs at the pace of the former.
+        // Chunks long enough for at most o-1 CTAs per SM win when that
+        // load is clearly lower (C3: 23 strips x 19 chunks of 19 rows, 3
+        // per SM, instead of 24 chunks of 15, 4 on 108 SMs: +1.4%; C2 +2%).
+        // Measured for p = 3 only: at p = 2 the lighter CTAs want the 4th
+        // CTA's latency hiding (-3%), at p >= 4 o - 1 = 1 CTA per SM.
+        if (P == 3 && o > 1) {
+            auto sm_load = [&](long long ch) {
+                const long long per = (rows + ch - 1) / ch;
+                const long long per_sm = (cols * ch + c->sms - 1) / c->sms;
+                return (double)per_sm * ((double)per + 1.0);
+            };
+            const double cur = sm_load(best_chunks);
+            long long alt = 0;
+            double alt_cost = 1e300;
+            for (long long ch = 1; ch <= rows && cols * ch <= (long long)c->sms * (o - 1); ++ch) {
+                if ((cols * ch + c->sms - 1) / c->sms != o - 1) continue;   // exactly o-1 on the busiest SM
+                const double t = sm_load(ch);
+                if (t < alt_cost - 1e-9) {
+                    alt_cost = t;
+                    alt = ch;
+                }
+            }
+            if (alt > 0 && alt_cost < 0.95 * cur) best_chunks = alt;
+        }
         rc = (int)((rows + best_chunks - 1) / best_chunks);
     }
     dgswe::StageParams kq = kp;
