@@ -25,9 +25,15 @@
  *                                  for tableau(1..4) (timestep.py:57-82), as
  *                                  fused stages, CUDA-graph batched
  *   dgswe_alpha_prepass            global Rusanov alpha (dg.py:389-411)
- *   dgswe_status                   PositivityError (models.py:143-146) and
+ *   dgswe_status / _status_tags    PositivityError (models.py:143-146) and
  *                                  DivergenceError (timestep.py:165-166,
- *                                  220-226) as device status bits
+ *                                  220-226) as device status bits, with the
+ *                                  first failing step per bit
+ *   dgswe_mass / dgswe_l2_sums     diagnostics.mass_integral / l2_error
+ *                                  (diagnostics.py:92-107, 42-80)
+ *   dgswe_project                  basis.project_initial (basis.py:206-233)
+ *   dgswe_stage_edge + exchange    _halo_exchange (dg.py:330-346) across GPUs:
+ *                                  latitude bands, peer-memory stores
  *
  * Layout of every state buffer (fp64), strip-blocked structure of arrays:
  *   [nz][nrows][3][nstrip][nphi][DGSWE_STRIP]
@@ -47,13 +53,23 @@
  * layout): with every integral of the reference on that Gauss rule the
  * nodal form is the same linear operator with a diagonal mass matrix.
  * dgswe_rk_steps converts u in place before and after its steps; the
- * single-stage entry points convert around each launch.  A caller that
+ * single-stage entry points (dgswe_rhs, dgswe_stage*) take modal states in
+ * ONE launch: every row tile is converted to nodal values in shared memory
+ * as it lands and the outputs back to modes in registers.  A caller that
  * keeps its states nodal across many stages (a band driver) calls
  * dgswe_set_basis(ctx, 1) and dgswe_convert itself: then dgswe_rhs,
  * dgswe_stage*, dgswe_alpha_prepass and dgswe_rk_steps take and return
  * nodal states unchanged.  dgswe_stage_edge requires the nodal basis.
  * Diagnostics (dgswe_mass, dgswe_l2_sums) and dgswe_project always use
  * modal states.
+ *
+ * Ownership: the caller owns every state buffer; the
+ * context owns the constant tables, status words, the global-alpha pair, a
+ * fixed-size diagnostics scratch and cached CUDA graphs, all allocated by
+ * dgswe_create -- no other entry point allocates device memory.  State
+ * pointers must be 16-byte aligned (TMA bulk copies; DGSWE_EINVAL else).
+ * A context holds no process-global mutable state: contexts on different
+ * threads / devices are independent (one host thread per context).
  *
  * All calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy
  * default) except dgswe_status, which synchronises it.  Return 0 on success,
@@ -69,13 +85,15 @@
 extern "C" {
 #endif
 
-#define DGSWE_ABI_VERSION 3
+#define DGSWE_ABI_VERSION 4
 #define DGSWE_STRIP 32          /* longitude elements per strip block */
 
 /* status bits (dgswe_status) */
 #define DGSWE_STATUS_POSITIVITY 0x1u  /* h <= 0 (or NaN) at a quadrature node */
 #define DGSWE_STATUS_NONFINITE 0x2u   /* non-finite coefficient after an update */
 #define DGSWE_STATUS_MEAN_NONPOS 0x4u /* cell-mean h <= 0 (check_positivity) */
+#define DGSWE_STATUS_PEER_TIMEOUT 0x8u /* a band neighbour's halo rows never arrived */
+#define DGSWE_STATUS_BITS 4
 
 /* error codes */
 #define DGSWE_OK 0
@@ -114,6 +132,10 @@ typedef struct dgswe_tables {
     const double *cos_r_edge; /* (ny+1): cos/R at edge latitude y_edges[e] (dg.py:276-282) */
     const double *cos_edge;   /* (ny+1): cos(y_edges[e]) for the y-direction alpha (models.py:280) */
     const double *minv;       /* (ny, nphi, nphi): per-row inverse mass (basis.py:159-190) */
+    const double *orog;       /* NULL, or (ny, nx, (p+1)^2): bottom height b at the Gauss nodes
+                                 (q = qi*(p+1)+qj, qi along lambda); adds the momentum sources
+                                 -(g h/R) db/dlambda, -(g h cos/R) db/dtheta (Williamson TC5;
+                                 not in the reference) */
 } dgswe_tables;
 
 typedef struct dgswe_ctx dgswe_ctx;
@@ -228,6 +250,14 @@ int dgswe_set_external_alpha(dgswe_ctx *ctx, int external);
 /* Reads (and optionally clears) the status word; synchronises `stream`.
  * first_tag receives the smallest tag that raised a flag (INT32_MAX if none). */
 int dgswe_status(dgswe_ctx *ctx, uint32_t *flags, int32_t *first_tag, int reset, void *stream);
+/* Same with the smallest tag per status bit: tags[DGSWE_STATUS_BITS], bit b
+ * (POSITIVITY, NONFINITE, MEAN_NONPOS, PEER_TIMEOUT) in tags[b]. */
+int dgswe_status_tags(dgswe_ctx *ctx, uint32_t *flags, int32_t *tags, int reset, void *stream);
+
+/* Bound (ns, default 2 s) on an edge launch's wait for a neighbour's halo
+ * rows; on expiry the launch raises DGSWE_STATUS_PEER_TIMEOUT instead of
+ * hanging the GPU (the stage's result is then invalid). */
+int dgswe_set_peer_timeout(dgswe_ctx *ctx, unsigned long long timeout_ns);
 
 /* ---- device diagnostics (single-band contexts; synchronise `stream`) ----
  * dgswe_mass: *out = sum over elements of sum_m m0_rows[j][m] c_m of variable

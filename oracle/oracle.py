@@ -252,11 +252,63 @@ def ic_tc6():
             "hv": lambda lam, th: height(lam, th) * winds(lam, th)[1]}
 
 
-H_REF = {"williamson_tc2": TC2_GH0 / GRAVITY, "williamson_tc6": TC6_H0}
+# Williamson TC5 (zonal flow over an isolated mountain, Williamson et al. 1992
+# section 3.5).  EXTENSION: the reference has no orography, so
+# this case is "parity unpinned" -- the oracle restates the same source the
+# CUDA path adds, -g h grad b, with grad b the derivative of b's degree-p
+# nodal interpolant (see orography_factors).
+TC5_U0 = 20.0
+TC5_H0 = 5960.0
+TC5_HS0 = 2000.0
+TC5_RM = math.pi / 9.0
+TC5_LC = 1.5 * math.pi
+TC5_TC = math.pi / 6.0
+
+
+def tc5_bottom(lam, th):
+    r = np.minimum(TC5_RM, np.sqrt((lam - TC5_LC) ** 2 + (th - TC5_TC) ** 2))
+    return TC5_HS0 * (1.0 - r / TC5_RM)
+
+
+def ic_tc5():
+    coef = RADIUS * OMEGA * TC5_U0 + 0.5 * TC5_U0 * TC5_U0
+
+    def depth(lam, th):
+        return (GRAVITY * TC5_H0 - coef * np.sin(th) ** 2) / GRAVITY - tc5_bottom(lam, th)
+
+    return {"h": depth,
+            "hu": lambda lam, th: depth(lam, th) * TC5_U0 * np.cos(th),
+            "hv": lambda lam, th: np.zeros(np.broadcast(lam, th).shape)}
+
+
+H_REF = {"williamson_tc2": TC2_GH0 / GRAVITY, "williamson_tc6": TC6_H0, "williamson_tc5": TC5_H0}
 
 
 def ic_funcs(case):
+    if case == "williamson_tc5":
+        return ic_tc5()
     return ic_tc2()[0] if case == "williamson_tc2" else ic_tc6()
+
+
+def orography_factors(t, bottom):
+    """(nx, ny, nq) factors -(g/R) db/dlambda and -(g cos/R) db/dtheta at the
+    interior nodes, grad b from the nodal interpolant of b:
+    db/dxi(x_i, x_j) = sum_k l_k'(x_i) b(x_k, x_j), l_k' from the Legendre
+    expansion l_k(x) = sum_a (2a+1)/2 w_k P_a(x_k) P_a(x)."""
+    n = t.p + 1
+    x, y = node_coords(t, t.nodes)
+    b = np.broadcast_to(bottom(x[:, None, :, None], y[None, :, None, :]), (t.nx, t.ny, n, n))
+    P = np.stack([legendre(a, t.nodes) for a in range(n)])          # [a][k]
+    dP = np.stack([legendre_d(a, t.nodes) for a in range(n)])       # [a][i]
+    scale = np.array([(2 * a + 1) / 2.0 for a in range(n)])
+    D = np.einsum("a,ai,ak,k->ik", scale, dP, P, t.weights)           # D[i][k] = l_k'(x_i)
+    dxi = np.einsum("ik,xykj->xyij", D, b)
+    deta = np.einsum("jk,xyik->xyij", D, b)
+    cos_n = np.cos(y)                                               # (ny, n) node latitudes
+    ox = -(GRAVITY / RADIUS) * dxi * (2.0 / t.dx)
+    oy = -(GRAVITY / RADIUS) * cos_n[None, :, None, :] * deta * (2.0 / t.dy)
+    return (np.ascontiguousarray(ox.reshape(t.nx, t.ny, n * n)),
+            np.ascontiguousarray(oy.reshape(t.nx, t.ny, n * n)))
 
 
 def node_coords(t: Tables, nodes):
@@ -342,6 +394,7 @@ class _Cfg(ctypes.Structure):
         ("phi", _P), ("edge", _P * 4), ("volx", _P), ("voly", _P), ("src", _P),
         ("bnd", _P * 4), ("minv", _P), ("cr_int", _P), ("sr_int", _P), ("fc_int", _P),
         ("cr_yb", _P), ("cr_yt", _P), ("cos_yb", _P), ("cos_yt", _P),
+        ("orog_x", _P), ("orog_y", _P),
     ]
 
 
@@ -378,7 +431,7 @@ class Oracle:
     POSITIVITY = 1
     NONFINITE = 2
 
-    def __init__(self, t: Tables):
+    def __init__(self, t: Tables, bottom=None):
         self.t = t
         ny = t.ny
         c = lambda a: np.ascontiguousarray(a, dtype=np.float64)
@@ -393,7 +446,8 @@ class Oracle:
         }
         edges = [c(e) for e in t.edge]
         bnds = [c(b) for b in t.bnd]
-        self._keep = (keep, edges, bnds)
+        orog = orography_factors(t, bottom) if bottom is not None else None
+        self._keep = (keep, edges, bnds, orog)
         cfg = _Cfg()
         cfg.nx, cfg.ny, cfg.nz, cfg.p = t.nx, t.ny, t.nz, t.p
         cfg.radius = RADIUS
@@ -408,6 +462,8 @@ class Oracle:
         for e in range(4):
             cfg.edge[e] = _ptr(edges[e])
             cfg.bnd[e] = _ptr(bnds[e])
+        if orog is not None:
+            cfg.orog_x, cfg.orog_y = _ptr(orog[0]), _ptr(orog[1])
         self.cfg = cfg
 
     def rhs(self, X, nthreads=0):
@@ -455,6 +511,7 @@ def sha16(X):
 
 
 def build_case(case, nx, ny, p, nz=1, alpha_mode="local", alpha=None):
-    """(Tables, Oracle, initial state) for a Williamson case."""
+    """(Tables, Oracle, initial state) for a Williamson case (TC5: with its
+    orography, an extension of the reference)."""
     t = make_tables(nx, ny, p, H_REF[case], nz=nz, alpha_mode=alpha_mode, alpha=alpha)
-    return t, Oracle(t), initial_state(t, case)
+    return t, Oracle(t, tc5_bottom if case == "williamson_tc5" else None), initial_state(t, case)

@@ -14,11 +14,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdgswe_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "dgswe_b200.h")
 
-ABI_VERSION = 3            # DGSWE_ABI_VERSION
+ABI_VERSION = 4            # DGSWE_ABI_VERSION
 STRIP = 32                 # DGSWE_STRIP: longitude elements per strip block
 STATUS_POSITIVITY = 0x1
 STATUS_NONFINITE = 0x2
 STATUS_MEAN_NONPOS = 0x4
+STATUS_PEER_TIMEOUT = 0x8
+STATUS_BITS = 4
 
 ALPHA_LOCAL, ALPHA_GLOBAL_PINNED, ALPHA_GLOBAL = 0, 1, 2
 
@@ -40,7 +42,7 @@ class Cfg(ctypes.Structure):
 class Tables(ctypes.Structure):
     _fields_ = [(name, _PD) for name in (
         "leg", "dleg", "weights", "cos_r_int", "sin_r_int", "fcos_int",
-        "cos_r_edge", "cos_edge", "minv")]
+        "cos_r_edge", "cos_edge", "minv", "orog")]
 
 
 # name -> (restype, argtypes); the single source for the symbol-export test
@@ -76,6 +78,9 @@ SIGNATURES = {
     "dgswe_set_external_alpha": (_I, [_VP, _I]),
     "dgswe_status": (_I, [_VP, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int32),
                           _I, _VP]),
+    "dgswe_status_tags": (_I, [_VP, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int32),
+                               _I, _VP]),
+    "dgswe_set_peer_timeout": (_I, [_VP, ctypes.c_ulonglong]),
     "dgswe_launch_count": (ctypes.c_int64, [_VP]),
 }
 

@@ -189,7 +189,8 @@ class BandOperator:
         self.shape = device_shape(op_host.nz, layout.nrows, op_host.nphi, mesh.nx)
         self.ctx = _Context(mesh, op_host.p, op_host.model, op_host.rusanov, op_host.nz,
                             op_host.quad, op_host.vander, op_host.Minv_rows, row0=layout.row0,
-                            nrows=layout.nrows, jlo=layout.jlo, jhi=layout.jhi, row_chunk=row_chunk)
+                            nrows=layout.nrows, jlo=layout.jlo, jhi=layout.jhi, row_chunk=row_chunk,
+                            bottom=op_host.bottom_nodal)
         self.global_alpha = op_host.rusanov.mode == "global" and op_host.rusanov.alpha is None
         if self.global_alpha:
             _lib.check(self.ctx.lib.dgswe_set_external_alpha(self.ctx.h, 1), "set_external_alpha")

@@ -1,0 +1,220 @@
+// dgswe_degree.cuh -- host launchers of the kernels of ONE degree P.  Each
+// deg_pP.cu includes this file and instantiates DGSWE_DEGREE_UNIT(P): the
+// seven degrees compile in parallel, and each unit owns its copy of the
+// __constant__ nodal tables (uploaded by ops->upload in dgswe_create).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstring>
+
+#include "dgswe_ctx.h"
+#include "dgswe_kernels.cuh"
+
+namespace dgswe_deg {
+
+using dgswe::StageParams;
+
+template <int P>
+int upload(const dgswe::NodTab &nt)
+{
+    CUDA_TRY(cudaMemcpyToSymbol(dgswe::c_nod, &nt, sizeof nt, sizeof nt * P));
+    return DGSWE_OK;
+}
+
+template <int P, int F>
+size_t stage_smem(const dgswe_ctx *c)
+{
+    using SM = dgswe::Smem<P>;
+    return (size_t)((F & dgswe::kOrog) ? SM::TOTAL_OROG : SM::TOTAL) * sizeof(double) + (size_t)c->smem_pad;
+}
+
+// resident CTAs per SM of variant F (queried once per context: the context
+// is bound to one device)
+template <int P, int F>
+int occupancy(dgswe_ctx *c)
+{
+    if (!c->occ[F]) {
+        const size_t smem = stage_smem<P, F>(c);
+        CUDA_TRY(cudaFuncSetAttribute(dgswe::stage_kernel<P, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        int o = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, dgswe::stage_kernel<P, F>, dgswe::kThreads,
+                                                               smem));
+        c->occ[F] = o > 0 ? o : 1;
+    }
+    return c->occ[F];
+}
+
+// Row chunking: every (strip, level) column of rows is split into
+// contiguous chunks, one CTA each.  The chunk count minimises the modelled
+// makespan  waves * (rows per chunk + kChunkOverhead), where waves =
+// ceil(CTAs / resident slots) and the overhead (prologue and first-row
+// work, measured ~1.4 rows) favours long chunks.  Narrow grids get one full
+// wave; wide grids, whose strips alone outnumber the slots, get several
+// waves of short chunks instead of one under-filled wave of very long ones.
+template <int P>
+int chunk_rows(const dgswe_ctx *c, int rows, int o)
+{
+    constexpr double kChunkOverhead = 1.5;
+    const long long slots = (long long)c->sms * o;
+    const long long cols = (long long)c->nstrip * c->cfg.nz;
+    double best = 1e300;
+    long long best_chunks = 1;
+    const long long max_chunks = rows < 4 * slots ? rows : 4 * slots;
+    for (long long ch = 1; ch <= max_chunks; ++ch) {
+        const long long per = (rows + ch - 1) / ch;
+        if (ch > 1 && (rows + ch - 2) / (ch - 1) == per) continue;   // same chunk length
+        const long long waves = (cols * ch + slots - 1) / slots;
+        const double t = (double)waves * ((double)per + kChunkOverhead);
+        if (t < best - 1e-9) {
+            best = t;
+            best_chunks = ch;
+        }
+    }
+    // Second look, by the busiest SM's row work: CTAs share their SM's issue
+    // and FP64 throughput, so a one-wave grid that puts o CTAs on some SMs
+    // and o-1 on the others runs at the pace of the former.  Chunks long
+    // enough for at most o-1 CTAs per SM win when that load is clearly lower
+    // (C3: 23 strips x 19 chunks of 19 rows, 3 per SM, instead of 24 chunks
+    // of 15, 4 on 108 SMs: +1.4%; C2 +2%).  Measured for p = 3 only: at
+    // p = 2 the lighter CTAs want the 4th CTA's latency hiding (-3%), at
+    // p >= 4 o - 1 = 1 CTA per SM.
+    if (P == 3 && o > 1) {
+        auto sm_load = [&](long long ch) {
+            const long long per = (rows + ch - 1) / ch;
+            const long long per_sm = (cols * ch + c->sms - 1) / c->sms;
+            return (double)per_sm * ((double)per + 1.0);
+        };
+        const double cur = sm_load(best_chunks);
+        long long alt = 0;
+        double alt_cost = 1e300;
+        for (long long ch = 1; ch <= rows && cols * ch <= (long long)c->sms * (o - 1); ++ch) {
+            if ((cols * ch + c->sms - 1) / c->sms != o - 1) continue;   // exactly o-1 on the busiest SM
+            const double t = sm_load(ch);
+            if (t < alt_cost - 1e-9) {
+                alt_cost = t;
+                alt = ch;
+            }
+        }
+        if (alt > 0 && alt_cost < 0.95 * cur) best_chunks = alt;
+    }
+    return (int)((rows + best_chunks - 1) / best_chunks);
+}
+
+template <int P, int F>
+int launch_variant(dgswe_ctx *c, const StageParams &kp0, cudaStream_t s)
+{
+    const int o = occupancy<P, F>(c);
+    if (o < 0) return o;
+    StageParams kp = kp0;
+    const int rows1 = kp.j_end - kp.j_begin, rows2 = kp.j_end2 - kp.j_begin2;
+    const int rows = rows1 > rows2 ? rows1 : rows2;
+    if (rows <= 0) return DGSWE_OK;
+    int rc = (F & dgswe::kEdge) ? 1 : kp.rc;
+    if (rc <= 0) rc = chunk_rows<P>(c, rows, o);
+    kp.rc = rc;
+    int nchunks = (rows1 + rc - 1) / rc;
+    if (rows2 > 0) {   // a second row range in the same launch
+        kp.nchunk1 = nchunks;
+        nchunks += (rows2 + rc - 1) / rc;
+    }
+    const dim3 grid(c->nstrip, nchunks, c->cfg.nz);
+    dgswe::stage_kernel<P, F><<<grid, dgswe::kThreads, stage_smem<P, F>(c), s>>>(kp);
+    CUDA_TRY(cudaGetLastError());
+    c->launches += 1;
+    return DGSWE_OK;
+}
+
+// the 20 instantiated variants: every combination of U, Y2, MODAL, OROG,
+// and the edge launches (nodal, one output) with or without U / OROG
+#define DGSWE_VARIANTS(X)                                                                   \
+    X(0) X(1) X(2) X(3) X(8) X(9) X(10) X(11) X(16) X(17) X(18) X(19) X(24) X(25) X(26) X(27) \
+    X(4) X(5) X(20) X(21)
+
+template <int P>
+int stage(dgswe_ctx *c, const StageParams &kp, cudaStream_t s)
+{
+    const int F = (kp.U ? dgswe::kHasU : 0) | (kp.Y2 ? dgswe::kHasY2 : 0) | (kp.edge ? dgswe::kEdge : 0) |
+                  (kp.modal ? dgswe::kModal : 0) | (kp.orog ? dgswe::kOrog : 0);
+    switch (F) {
+#define DGSWE_CASE(f) \
+    case f: return launch_variant<P, f>(c, kp, s);
+        DGSWE_VARIANTS(DGSWE_CASE)
+#undef DGSWE_CASE
+    default: return dgswe_fail(DGSWE_EUNSUPPORTED, "stage variant %d not built (edge launches are nodal, one output)", F);
+    }
+}
+
+template <int P>
+int convert(dgswe_ctx *c, const double *in, double *out, bool to_nodal, int r0, int r1, cudaStream_t s)
+{
+    if (r1 <= r0) return DGSWE_OK;
+    const dim3 grid(c->nstrip, r1 - r0, c->cfg.nz);
+    if (to_nodal)
+        dgswe::convert_kernel<P, true><<<grid, 96, 0, s>>>(in, out, c->zstride, c->rstride, c->vstride, r0);
+    else
+        dgswe::convert_kernel<P, false><<<grid, 96, 0, s>>>(in, out, c->zstride, c->rstride, c->vstride, r0);
+    CUDA_TRY(cudaGetLastError());
+    c->launches += 1;
+    return DGSWE_OK;
+}
+
+template <int P>
+int alpha(dgswe_ctx *c, const double *X, bool modal, cudaStream_t s)
+{
+    CUDA_TRY(cudaMemsetAsync(c->alpha, 0, 2 * sizeof(double), s));
+    const int rows = c->cfg.jhi - c->cfg.jlo;
+    const dim3 grid((c->cfg.nx + 127) / 128, rows, c->cfg.nz);
+    if (modal)
+        dgswe::alpha_prepass_kernel<P, true><<<grid, 128, 0, s>>>(
+            X, c->zstride, c->rstride, c->vstride, c->cfg.nx, c->cfg.row0, c->cfg.jlo, c->cfg.jhi, c->cos_edge,
+            c->inv_r, c->cfg.gravity, c->cfg.h_floor, c->alpha);
+    else
+        dgswe::alpha_prepass_kernel<P, false><<<grid, 128, 0, s>>>(
+            X, c->zstride, c->rstride, c->vstride, c->cfg.nx, c->cfg.row0, c->cfg.jlo, c->cfg.jhi, c->cos_edge,
+            c->inv_r, c->cfg.gravity, c->cfg.h_floor, c->alpha);
+    CUDA_TRY(cudaGetLastError());
+    c->launches += 1;
+    return DGSWE_OK;
+}
+
+template <int P>
+int project(dgswe_ctx *c, const double *f, const double *cosn, double determ, double *Y, cudaStream_t s)
+{
+    const dim3 grid((c->cfg.nx + 127) / 128, c->cfg.ny, 3);
+    const dgswe::DiagLayout L{c->zstride, c->rstride, c->vstride, c->cfg.nx, c->cfg.ny, c->nphi};
+    dgswe::project_kernel<P><<<grid, 128, 0, s>>>(f, cosn, c->rowtab, dgswe::row_stride(P),
+                                                  dgswe::RowLayout<P>::T, L, c->cfg.nz, determ, Y);
+    CUDA_TRY(cudaGetLastError());
+    c->launches += 1;
+    return DGSWE_OK;
+}
+
+}  // namespace dgswe_deg
+
+#ifdef DG_TIMING
+// experiment builds only: per-role phase cycle sums of degree P since the last call
+#define DGSWE_TIMING_HOOK(P)                                                                     \
+    extern "C" int dgswe_debug_timing_p##P(unsigned long long *out28)                             \
+    {                                                                                            \
+        CUDA_TRY(cudaDeviceSynchronize());                                                       \
+        CUDA_TRY(cudaMemcpyFromSymbol(out28, dgswe::g_timing, sizeof(unsigned long long) * 28)); \
+        static const unsigned long long zero[28] = {};                                           \
+        CUDA_TRY(cudaMemcpyToSymbol(dgswe::g_timing, zero, sizeof zero));                        \
+        return DGSWE_OK;                                                                         \
+    }
+#else
+#define DGSWE_TIMING_HOOK(P)
+#endif
+
+#define DGSWE_DEGREE_UNIT(P)                                                                     \
+    DGSWE_TIMING_HOOK(P)                                                                         \
+    const DegreeOps *dgswe_degree_ops_##P()                                                      \
+    {                                                                                            \
+        static const DegreeOps ops = {dgswe_deg::upload<P>, dgswe_deg::stage<P>,                 \
+                                      dgswe_deg::convert<P>, dgswe_deg::alpha<P>,                \
+                                      dgswe_deg::project<P>};                                    \
+        return &ops;                                                                             \
+    }

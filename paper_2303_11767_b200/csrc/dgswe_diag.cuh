@@ -7,8 +7,6 @@
 //   l2_rows_kernel     per-row partial sums of the L2 error with a p+2 rule
 //                      and the cos(theta) metric      (diagnostics.py:42-80)
 //   rows_total_kernel  fixed-order sum of the row partials
-//   project_kernel     cos-weighted L2 projection of nodal values onto the
-//                      modal basis                    (basis.py:206-233)
 //
 // Reductions are deterministic (fixed per-thread order, fixed shuffle tree,
 // fixed row order) and carried in double-double (TwoSum), so the result is
@@ -18,6 +16,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include "dgswe_params.h"
 
 namespace dgswe {
 
@@ -71,10 +71,6 @@ __device__ __forceinline__ void block_reduce(DD (&v)[K], DD (*sm)[8])
     }
 }
 
-struct DiagLayout {
-    long long zstride, rstride, vstride;
-    int nx, ny, nphi;
-};
 
 __device__ __forceinline__ const double *elem_ptr(const double *X, const DiagLayout &L, int z, int j, int v,
                                                   int i)
@@ -155,59 +151,6 @@ __global__ void rows_total_kernel(const double *__restrict__ part, int ny, int z
     if (threadIdx.x == 0)
 #pragma unroll
         for (int k = 0; k < K; ++k) out[k] = __dadd_rn(acc[k].hi, acc[k].lo);
-}
-
-// grid (ceil(nx/128), ny, 3), block 128: one thread per element and
-// variable.  f: nodal values [3][ny][nx][n*n] at the (p+1)^2 Gauss nodes
-// (q = qi*n + qj, qi along lambda); moments = determ sum_q w_qi w_qj
-// cos(theta_qj) phi_m(q) f_q (sum-factorised), then the Kronecker inverse
-// mass c[a][b] = (2a+1) sum_bb T_j[b][bb] moments[a][bb] (T_j: the a = 0
-// block of the row's M^-1, from the row table); written to every level.
-template <int P>
-__global__ void project_kernel(const double *__restrict__ f, const double *__restrict__ cos_nodes,
-                               const double *__restrict__ rowtab, int row_stride, int t_off, DiagLayout L,
-                               int nz, double determ, double *Y)
-{
-    constexpr int N = P + 1;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y, v = blockIdx.z;
-    if (i >= L.nx) return;
-    const double *fv = f + (((size_t)v * L.ny + j) * L.nx + i) * (N * N);
-    const double *cj = cos_nodes + (size_t)j * N;
-    double g[N][N];   // g[qi][b] = sum_qj wP_b(qj) cos_qj f(qi, qj)
-#pragma unroll
-    for (int qi = 0; qi < N; ++qi)
-#pragma unroll
-        for (int b = 0; b < N; ++b) {
-            double acc = 0.0;
-#pragma unroll
-            for (int qj = 0; qj < N; ++qj) acc = fma(c_tab[P][2][b][qj] * cj[qj], fv[qi * N + qj], acc);
-            g[qi][b] = acc;
-        }
-    double mom[N][N];
-#pragma unroll
-    for (int a = 0; a < N; ++a)
-#pragma unroll
-        for (int b = 0; b < N; ++b) {
-            double acc = 0.0;
-#pragma unroll
-            for (int qi = 0; qi < N; ++qi) acc = fma(c_tab[P][2][a][qi], g[qi][b], acc);
-            mom[a][b] = determ * acc;
-        }
-    const double *T = rowtab + (size_t)j * row_stride + t_off;
-    for (int z = 0; z < nz; ++z) {
-        double *y = Y + (size_t)z * L.zstride + (size_t)j * L.rstride + (size_t)v * L.vstride +
-                    (size_t)(i >> 5) * L.nphi * 32 + (i & 31);
-#pragma unroll
-        for (int a = 0; a < N; ++a)
-#pragma unroll
-            for (int b = 0; b < N; ++b) {
-                double acc = 0.0;
-#pragma unroll
-                for (int bb = 0; bb < N; ++bb) acc = fma(T[b * N + bb], mom[a][bb], acc);
-                y[(a * N + b) * 32] = (double)(2 * a + 1) * acc;
-            }
-    }
 }
 
 }  // namespace dgswe

@@ -25,6 +25,14 @@
 //      face lifts, the diagonal nodal mass and the fused RK stage update
 //      (dg.py:455-502, timestep.py:132-167)
 //
+// Kernel variants (template bitmask F, see kHasU ... kOrog): the stage
+// combination's u^n term, classical RK4's second output, the band edge rows
+// of the fused halo exchange, modal in/out states (the reference's own
+// coefficients: every tile is converted to the Gauss nodes in shared memory
+// as it lands and the output back to modes in registers -- the single-launch
+// form of assemble_rhs / rk_step) and the orography source of Williamson
+// TC5 (-g h grad b, not in the reference: SPEC.md:157).
+//
 // Floating point: FMA contraction, refined MUFU reciprocals and a different
 // summation order than the reference; results agree with the reference's
 // exact-order oracle to ~1e-15 relative per step (tests/test_gpu_parity.py).
@@ -33,56 +41,16 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "dgswe_params.h"
+
 namespace dgswe {
 
-constexpr int kMaxP = 6;
-constexpr int kLanes = 32;   // elements per strip (== DGSWE_STRIP)
-constexpr int kVarWarps = 3; // one per conserved variable
-constexpr int kWarps = 4;    // + one face warp (Rusanov fluxes)
-constexpr int kThreads = kWarps * kLanes;
-
-// [p][table][a][q]: 0 P_a(x_q), 1 P'_a(x_q), 2 w_q P_a(x_q), 3 w_q P'_a(x_q)
-__constant__ double c_tab[kMaxP + 1][4][kMaxP + 1][kMaxP + 1];
-
-struct StageParams {
-    const double *X;      // stage input (level 0, buffer row 0)
-    const double *U;      // u^n for the combination (may be null when a == 0)
-    double *Y;            // output
-    const double *A;      // second output's addend (HAS_Y2 kernels; may alias Y2)
-    double *Y2;           // second output Y2 = A + g2 RHS(X) (classical RK4's accumulator)
-    double g2;
-    long long zstride;    // doubles per level
-    long long rstride;    // doubles per buffer row (3 * vstride)
-    long long vstride;    // doubles per variable row (nstrip * nphi * 32)
-    int nx, nstrip, ny, row0, nrows;
-    int j_begin, j_end, rc;   // local rows [j_begin, j_end), rc rows per CTA
-    int nchunk1;              // chunks of the first range; later chunks cover [j_begin2, j_end2)
-    int j_begin2, j_end2;
-    double a, b, g;       // Y = a U + b X + g RHS(X)
-    double dx[kMaxP + 1][kMaxP + 1];   // (1/R)(determ/bd_det_x) dh: the xi derivative of F
-    const double *rowtab; // per global row, see RowLayout
-    double inv_r;         // 1/R
-    double inv_r_cx;      // (1/R) * determ/bd_det_x
-    double gravity, half_g, h_floor, inv_floor, sqrt_g;
-    double bdx, bdy;      // bd_det_x, bd_det_y
-    int alpha_mode;       // 0 local, 1 pinned, 2 global (from alpha_dev)
-    double alpha;
-    const double *alpha_dev;
-    unsigned *status;
-    int *first_tag;
-    int tag;
-    int check_finite;
-    int check_mean;
-    // fused halo exchange over peer memory (edge launches of a latitude
-    // band, bands.py transport "fused"): [0] south, [1] north neighbour
-    int edge;                           // 1: this launch computes the band's edge rows
-    int band_lo, band_hi;               // the band's computed rows [band_lo, band_hi)
-    double *peer_row[2];                // neighbour's halo row (level 0) our edge row is copied to
-    long long peer_zstride[2];
-    unsigned long long *peer_count[2];  // neighbour's receive counter for that halo
-    const unsigned long long *recv_count;   // own receive counters [2] (system-scope atomics)
-    unsigned long long *stage_ctr;      // own [0] completed edge launches, [1] CTA completions
-};
+__device__ __forceinline__ unsigned long long globaltimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p)
 {
@@ -91,56 +59,20 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     return v;
 }
 
-// per-row table layout (doubles): crc[n] srs[n] fcs[n] cr_b cos_b rj[n] T[n][n]
+// Resident CTAs per SM the stage kernels are register-capped for: p <= 3
+// at 128 registers (4 CTAs), p >= 4 at 2 CTAs; a rolled volume loop (row-
+// local terms through shared memory) for p >= 2.
 template <int P>
-struct RowLayout {
-    static constexpr int N = P + 1;
-    static constexpr int CRC = 0;
-    static constexpr int SRS = N;
-    static constexpr int FCS = 2 * N;
-    static constexpr int CRB = 3 * N;
-    static constexpr int COSB = 3 * N + 1;
-    static constexpr int RJ = 3 * N + 2;     // 1 / (determ cos_j): the nodal mass
-    static constexpr int SSTRIDE = RJ + N;   // the part staged in shared memory
-    static constexpr int T = SSTRIDE;        // theta block of M^-1 (modal; device IC projection only)
-    static constexpr int STRIDE = T + N * N;
-};
-
-__host__ __device__ inline int row_stride(int p) { return 4 * (p + 1) + 2 + (p + 1) * (p + 1); }
-
-#define LEG(a, q) c_tab[P][0][a][q]
-#define WP(a, q) c_tab[P][2][a][q]
-
-// (the Legendre tables serve the basis conversions; the stage kernel uses
-// the nodal tables c_nod below)
-#ifndef DG_SELFLOOR
-#define DG_SELFLOOR 1   // 1/max(h, floor) as rcp(h) + select: the reciprocal starts at once
-#endif
-#ifndef DG_VROLL
-#define DG_VROLL -1  // volume loop over node rows kept rolled (row-local terms through shared memory):
-                     // -1 = for p >= 2 (a quarter of the unrolled code; with the per-equation
-                     // physics +0.2% at p=2, p=3/4 see DESIGN.md; -3.5% at p=1), 0 = never, 1 = always
-#endif
+__host__ __device__ constexpr int min_blocks() { return P <= 3 ? 4 : 2; }
 template <int P>
-__host__ __device__ constexpr bool vol_rolled() { return DG_VROLL < 0 ? P >= 2 : DG_VROLL != 0; }
-#ifndef DG_ROWHOIST
-#define DG_ROWHOIST 1  // the rolled volume loop keeps the row's physics factors in registers (+1%)
-#endif
-#ifndef DG_ICMP
-#define DG_ICMP 1    // h-floor / celerity branches compared on the integer pipe
-#endif
-#ifndef DG_HSPLIT
-#define DG_HSPLIT 2  // 1 / 2: the hu / hv warp also computes the h equation's row-local volume term (2: +0.4% at C3)
-#endif
-#ifndef DG_MINB
-#define DG_MINB 4   // resident CTAs per SM the p = 3 build is register-capped for (128 registers
-                    // with the rolled volume loop; 3 at ~160 measured 1-2% slower)
-#endif
+__host__ __device__ constexpr bool vol_rolled() { return P >= 2; }
 
 // DG_TIMING builds record per-role phase durations (clock cycles) of every
 // row: [role][A work, barrier-1 wait, B work, barrier-2 wait, C work, rows]
 #ifdef DG_TIMING
+namespace {
 __device__ unsigned long long g_timing[4][7];
+}
 #define TSTAMP(k)                                                                  \
     unsigned tk##k;                                                                \
     asm volatile("mov.u32 %0, %%clock;" : "=r"(tk##k)::"memory")
@@ -150,25 +82,68 @@ __device__ unsigned long long g_timing[4][7];
 #define TACC(i, d)
 #endif
 
-// Nodal (Gauss-Lagrange) tables of degree P, built on the host from the
-// Legendre tables (dgswe_b200.cu, dgswe_create): with l_i the Lagrange
-// polynomial of Gauss node x_i,
-//   lm[i]    = l_i(-1)                (l_i(+1) = l_{N-1-i}(-1))
-//   mu[i]    = l_i(-1) / w_i          (boundary lift of a face value)
-//   dh[i][k] = w_k l_i'(x_k) / w_i    (weak derivative, W^-1 D^T W)
-//   w[i]     = w_i
-// The state is carried at the (p+1)^2 Gauss nodes inside a step: the
-// reference's modal scheme with every integral on the same (p+1)-point Gauss
-// rule (dg.py:186-213, basis.py:159-177) is, in the Lagrange basis of those
-// nodes, the same linear operator with a diagonal mass matrix
-// determ w_i w_j cos_j (exact algebra; only the rounding differs).
-struct NodTab {
-    double lm[kMaxP + 1];
-    double mu[kMaxP + 1];
-    double dh[kMaxP + 1][kMaxP + 1];
-    double w[kMaxP + 1];
-};
+// internal linkage: every degree's translation unit (deg_p*.cu) owns its
+// copy, uploaded by that unit's dgswe_create path
+namespace {
 __constant__ NodTab c_nod[kMaxP + 1];
+}
+
+#define LEG(a, q) c_nod[P].leg[a][q]
+#define WP(a, q) c_nod[P].wp[a][q]
+
+// Modal <-> nodal change of basis of one element tile in registers, in the
+// operation order of convert_kernel (so both give identical bits):
+//   nodal u[i][j] = sum_a P_a(x_i) sum_b P_b(x_j) c[a][b]
+//   modal c[a][b] = (2a+1)(2b+1)/4 sum_i w_i P_a(x_i) sum_j w_j P_b(x_j) u[i][j]
+template <int P>
+__device__ __forceinline__ void to_nodal(double (&x)[P + 1][P + 1])
+{
+    constexpr int N = P + 1;
+    double t[N][N];
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            double s = 0.0;
+#pragma unroll
+            for (int b = 0; b < N; ++b) s = fma(LEG(b, q), x[a][b], s);
+            t[a][q] = s;
+        }
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < N; ++a) s = fma(LEG(a, q), t[a][r], s);
+            x[q][r] = s;
+        }
+}
+
+template <int P>
+__device__ __forceinline__ void to_modal(double (&x)[P + 1][P + 1])
+{
+    constexpr int N = P + 1;
+    double t[N][N];
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            double s = 0.0;
+#pragma unroll
+            for (int b = 0; b < N; ++b) s = fma(WP(q, b), x[a][b], s);
+            t[a][q] = s;
+        }
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < N; ++a) s = fma(WP(q, a), t[a][r], s);
+            x[q][r] = s * (0.25 * (double)((2 * q + 1) * (2 * r + 1)));
+        }
+}
 
 // value at xi = -1 (LO) or +1 of the nodal line x
 template <int P, bool LO>
@@ -207,6 +182,8 @@ struct Smem {
     static constexpr int ROW = HB + 6 * NP;              // row-table ring, 3 rows
     static constexpr int MBAR = ROW + 3 * RowLayout<P>::SSTRIDE;  // 6 mbarriers [slot][var]
     static constexpr int TOTAL = MBAR + 6;
+    static constexpr int OB = (TOTAL + 1) & ~1;          // orography tiles [slot][hu, hv][NP][32] (kOrog)
+    static constexpr int TOTAL_OROG = OB + 4 * NP * kLanes;
 };
 
 // max(x, y) for y > 0 on the integer pipe: the signed 64-bit order of the
@@ -259,13 +236,8 @@ __device__ __forceinline__ void inv_and_celerity(double h, double h_floor, doubl
                                                  double &r, double &c)
 {
     const double y = rsqrt64(max_pos(h, 2.2250738585072014e-308));
-#if DG_ICMP
-    r = ge_pos(h, h_floor) ? y * y : inv_floor;
+    r = ge_pos(h, h_floor) ? y * y : inv_floor;   // branches compared on the integer pipe
     c = gt_zero(h) ? sqrt_g * (h * y) : 0.0;
-#else
-    r = h >= h_floor ? y * y : inv_floor;
-    c = h > 0.0 ? sqrt_g * (h * y) : 0.0;
-#endif
 }
 
 // --- TMA bulk copies and mbarriers (one elected lane per variable warp) ---
@@ -484,7 +456,7 @@ __device__ __forceinline__ void face_flux_call(int in_off, int in_ld, int in_col
 
 
 // per-row factors of the physics, read from the staged row table or held
-// in registers across a row's node loop (DG_ROWHOIST)
+// in registers across a row's node loop
 template <int P>
 struct RowRef {
     const double *p;
@@ -517,15 +489,17 @@ struct RowRegs {
 //   2 hv: F = hu w,            G = (hv w + g h^2/2) cos/R, S = -(g h^2/2 sin/R + t hu)
 //   3:    hu or hv by the uniform flag is_v, one branch-free code path
 //         (the unrolled volume, where a second copy would cost I-cache)
-// with u = hu/hf, w = hv/hf, t = u sin/R + 2 Omega sin cos.
-template <int P, int KIND, typename RT>
+// with u = hu/hf, w = hv/hf, t = u sin/R + 2 Omega sin cos.  With OROG the
+// momentum sources gain h * B (B = this equation's orography factor at the
+// node, the warp's staged tile sB: -(g/R) db/dlambda resp. -(g cos/R)
+// db/dtheta, determ folded in).
+template <int P, int KIND, bool OROG, typename RT>
 __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU, const RT &row, int lane,
-                                             const StageParams &kp, double (&F)[P + 1],
+                                             const StageParams &kp, const double *sB, double (&F)[P + 1],
                                              double (&G)[P + 1], double (&S)[P + 1])
 {
     constexpr int N = P + 1;
     constexpr int NP = N * N;
-    using RL = RowLayout<P>;
 #pragma unroll
     for (int qj = 0; qj < N; ++qj) {
         const int q = qi * N + qj;
@@ -538,16 +512,8 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
             S[qj] = 0.0;
         } else {
             const double h = sU[(0 * NP + q) * kLanes + lane];
-#if DG_SELFLOOR
-            const double r0 = rcp64(h);
-#if DG_ICMP
-            const double r = ge_pos(h, kp.h_floor) ? r0 : kp.inv_floor;
-#else
-            const double r = h >= kp.h_floor ? r0 : kp.inv_floor;
-#endif
-#else
-            const double r = rcp64(max_pos(h, kp.h_floor));
-#endif
+            // 1/max(h, floor) as rcp(h) + select: the reciprocal starts at once
+            const double r = ge_pos(h, kp.h_floor) ? rcp64(h) : kp.inv_floor;
             const double gh2 = h * h * kp.half_g;
             const double u = hu * r, w = hv * r;
             const double srs = row.srs(qj);
@@ -565,6 +531,7 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
                 G[qj] = fma(is_v ? hv : hu, w, is_v ? gh2 : 0.0) * crc;
                 S[qj] = fma(is_v ? -gh2 : 0.0, srs, t * (is_v ? -hu : hv));
             }
+            if constexpr (OROG) S[qj] = fma(h, sB[q * kLanes + lane], S[qj]);
         }
     }
 }
@@ -576,15 +543,15 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
 // common 1/(determ cos_j) is applied in finalize.  Node row i (fixed xi
 // node) is evaluated at once: its G/S terms land in acc[i][.], its F
 // scatters into every acc[.][j].
-template <int P, bool MOM>
+template <int P, bool MOM, bool OROG>
 __device__ __forceinline__ void volume(double (&acc)[P + 1][P + 1], int v, const double *sU,
-                                       const double *row, int lane, const StageParams &kp)
+                                       const double *row, int lane, const StageParams &kp, const double *sB)
 {
     constexpr int N = P + 1;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         double F[N], G[N], S[N];
-        node_physics<P, MOM ? 3 : 0>(v == 2, i, sU, RowRef<P>{row}, lane, kp, F, G, S);
+        node_physics<P, MOM ? 3 : 0, OROG>(v == 2, i, sU, RowRef<P>{row}, lane, kp, sB, F, G, S);
 #pragma unroll
         for (int j = 0; j < N; ++j) {
             double e = MOM ? S[j] : 0.0;
@@ -604,39 +571,35 @@ __device__ __forceinline__ void volume(double (&acc)[P + 1][P + 1], int v, const
 // Same terms with the loop over node rows kept rolled (a quarter of the
 // code): the row-local G/S terms of row i go to shared memory sE (this
 // warp's [NP][32] block) and are added in finalize; F still scatters into
-// the register tile through the i-th column of Dx.
-template <int P, int KIND>
+// the register tile through the i-th column of Dx.  The h equation's
+// row-local term (G = hv cos/R) is formed by the hv warp (KIND 2): the h
+// warp's x-face work leaves it the longest volume phase otherwise.
+template <int P, int KIND, bool OROG>
 __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v, const double *sU,
-                                              const double *row, int lane, const StageParams &kp, double *sE)
+                                              const double *row, int lane, const StageParams &kp, double *sE,
+                                              const double *sB)
 {
     constexpr int N = P + 1;
 #pragma unroll
     for (int ii = 0; ii < N; ++ii)
 #pragma unroll
         for (int j = 0; j < N; ++j) acc[ii][j] = 0.0;
-#if DG_ROWHOIST
-    const RowRegs<P> rr(row);
-#else
-    const RowRef<P> rr{row};
-#endif
+    const RowRegs<P> rr(row);   // the row's physics factors in registers across the loop
 #pragma unroll 1
     for (int i = 0; i < N; ++i) {
         double F[N], G[N], S[N];
-        node_physics<P, KIND>(false, i, sU, rr, lane, kp, F, G, S);
-        if (KIND != 0 || DG_HSPLIT == 0) {
+        node_physics<P, KIND, OROG>(false, i, sU, rr, lane, kp, sB, F, G, S);
+        if constexpr (KIND != 0) {
 #pragma unroll
             for (int j = 0; j < N; ++j) {
-                double e = KIND ? S[j] : 0.0;
+                double e = S[j];
 #pragma unroll
                 for (int k = 0; k < N; ++k) e = fma(c_nod[P].dh[j][k], G[k], e);
                 sE[(i * N + j) * kLanes + lane] = e;
             }
         }
-        if constexpr (DG_HSPLIT != 0 && KIND == DG_HSPLIT) {
-            // the h equation's row-local term (G = hv cos/R) for the h warp,
-            // whose face work leaves it the longest volume phase
+        if constexpr (KIND == 2) {
             constexpr int NP = N * N;
-            using RL = RowLayout<P>;
             double gh[N];
 #pragma unroll
             for (int k = 0; k < N; ++k) gh[k] = sU[(2 * NP + i * N + k) * kLanes + lane] * rr.crc(k);
@@ -649,13 +612,11 @@ __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v
                 sEh[(i * N + j) * kLanes + lane] = e;
             }
         }
-        if constexpr (KIND != 0 || DG_HSPLIT == 0 || true) {
 #pragma unroll
-            for (int ii = 0; ii < N; ++ii) {
-                const double d = kp.dx[ii][i];
+        for (int ii = 0; ii < N; ++ii) {
+            const double d = kp.dx[ii][i];
 #pragma unroll
-                for (int j = 0; j < N; ++j) acc[ii][j] = fma(d, F[j], acc[ii][j]);
-            }
+            for (int j = 0; j < N; ++j) acc[ii][j] = fma(d, F[j], acc[ii][j]);
         }
     }
 }
@@ -664,8 +625,10 @@ __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v
 // Face values are scale * f* at the face's nodes (bd_det folded in by the
 // face warps); x lifts run along xi with mu, y lifts along eta.
 // Uv / Yv point at this lane's element of the variable's strip block
-// (node stride 32 doubles: immediate offsets).
-template <int P, bool HAS_U, bool HAS_Y2>
+// (node stride 32 doubles: immediate offsets).  MODAL: U, A, Y, Y2 hold
+// modal coefficients; the nodal parts b X + g K and g2 K are converted to
+// modes in registers before the u^n / accumulator terms are added.
+template <int P, bool HAS_U, bool HAS_Y2, bool MODAL>
 __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const double *cur,
                                              const double *Uv, const double *Av, double *Y2v, int v,
                                              const double *sFX, const double *sF0,
@@ -712,23 +675,59 @@ __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const 
         }
     }
     const double *rj = row + RL::RJ;
+    if constexpr (MODAL) {
+        // K = diag(rj) acc at the nodes; Y2 = A + g2 K and Y = a U + (b X + g K),
+        // with the nodal parts converted to modes
 #pragma unroll
-    for (int j = 0; j < N; ++j) {
-        const double gr = kp.g * rj[j];
-        const double g2r = HAS_Y2 ? kp.g2 * rj[j] : 0.0;
+        for (int j = 0; j < N; ++j)
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-            const double k = acc[i][j];
-            double y = fma(kp.b, cur[(i * N + j) * kLanes + lane], gr * k);
-            if (HAS_U) y = fma(kp.a, un[i][j], y);
-            if (owned) Yv[(i * N + j) * kLanes] = y;
-            if (owned && Ypeer) Ypeer[(i * N + j) * kLanes] = y;   // fused halo exchange (NVLink store)
-            if (owned && Ypeer2) Ypeer2[(i * N + j) * kLanes] = y;
-            if constexpr (HAS_Y2) {
-                const double y2 = fma(g2r, k, an[i][j]);
-                if (owned) Y2v[(i * N + j) * kLanes] = y2;
+            for (int i = 0; i < N; ++i) acc[i][j] *= rj[j];
+        if constexpr (HAS_Y2) {
+            double k2[N][N];
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+#pragma unroll
+                for (int j = 0; j < N; ++j) k2[i][j] = kp.g2 * acc[i][j];
+            to_modal<P>(k2);
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+#pragma unroll
+                for (int j = 0; j < N; ++j)
+                    if (owned) Y2v[(i * N + j) * kLanes] = an[i][j] + k2[i][j];
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+            for (int j = 0; j < N; ++j) acc[i][j] = fma(kp.b, cur[(i * N + j) * kLanes + lane], kp.g * acc[i][j]);
+        to_modal<P>(acc);
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                double y = acc[i][j];
+                if (HAS_U) y = fma(kp.a, un[i][j], y);
+                if (owned) Yv[(i * N + j) * kLanes] = y;
+                acc[i][j] = y;
             }
-            acc[i][j] = y;
+    } else {
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double gr = kp.g * rj[j];
+            const double g2r = HAS_Y2 ? kp.g2 * rj[j] : 0.0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                const double k = acc[i][j];
+                double y = fma(kp.b, cur[(i * N + j) * kLanes + lane], gr * k);
+                if (HAS_U) y = fma(kp.a, un[i][j], y);
+                if (owned) Yv[(i * N + j) * kLanes] = y;
+                if (owned && Ypeer) Ypeer[(i * N + j) * kLanes] = y;   // fused halo exchange (NVLink store)
+                if (owned && Ypeer2) Ypeer2[(i * N + j) * kLanes] = y;
+                if constexpr (HAS_Y2) {
+                    const double y2 = fma(g2r, k, an[i][j]);
+                    if (owned) Y2v[(i * N + j) * kLanes] = y2;
+                }
+                acc[i][j] = y;
+            }
         }
     }
     unsigned bad = 0;
@@ -741,16 +740,20 @@ __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const 
                 for (int j = 0; j < N; ++j) fexp = max(fexp, __double2hiint(acc[i][j]) & 0x7ff00000);
             bad |= fexp == 0x7ff00000 ? 2u : 0u;
         }
-        if (v == 0 && kp.check_mean) {   // cell mean = modal c_00 = sum w_i w_j u_ij / 4
-            double m = 0.0;
+        if (v == 0 && kp.check_mean) {
+            if constexpr (MODAL) {   // the reference's check: mode 0 (timestep.py:220-226)
+                bad |= !(acc[0][0] > 0.0) ? 4u : 0u;
+            } else {                 // cell mean = modal c_00 = sum w_i w_j u_ij / 4
+                double m = 0.0;
 #pragma unroll
-            for (int i = 0; i < N; ++i) {
-                double s = 0.0;
+                for (int i = 0; i < N; ++i) {
+                    double s = 0.0;
 #pragma unroll
-                for (int j = 0; j < N; ++j) s = fma(c_nod[P].w[j], acc[i][j], s);
-                m = fma(c_nod[P].w[i], s, m);
+                    for (int j = 0; j < N; ++j) s = fma(c_nod[P].w[j], acc[i][j], s);
+                    m = fma(c_nod[P].w[i], s, m);
+                }
+                bad |= !(m > 0.0) ? 4u : 0u;
             }
-            bad |= !(m > 0.0) ? 4u : 0u;
         }
     }
     return bad;
@@ -775,10 +778,11 @@ __device__ __forceinline__ void fetch_neighbours(const double *Xrow, int eL, int
 
 // Face warp: the traces of the strip's left border face for one row.
 // Lanes 0..5 each build one trace: (side 0) R trace of the left neighbour
-// element, from its gathered nodal values; (side 1) L trace of the strip's
-// element 0, from the ring.  Also the L trace of the right
-// neighbour (lanes 6..8), which the h warp needs for the last lane's right face.
-template <int P>
+// element, from its gathered values; (side 1) L trace of the strip's
+// element 0, from the (nodal) ring.  Also the L trace of the right
+// neighbour (lanes 6..8), which the h warp needs for the last lane's right
+// face.  MODAL: the gathered neighbours hold modes, converted here.
+template <int P, bool MODAL>
 __device__ __forceinline__ void border_traces(const double *sHB, const double *ring_slot, double *sHL,
                                               double *sE0, double *sHR, int lane)
 {
@@ -799,6 +803,7 @@ __device__ __forceinline__ void border_traces(const double *sHB, const double *r
             for (int a = 0; a < N; ++a)
 #pragma unroll
                 for (int b = 0; b < N; ++b) c[a][b] = src[a * N + b];
+            if constexpr (MODAL) to_nodal<P>(c);
         }
         double tr[N];
         if (side == 0)
@@ -830,9 +835,64 @@ __device__ __forceinline__ unsigned stage_bottom(const double *tile, double *dst
     return bad;
 }
 
-template <int P, bool HAS_U, bool HAS_Y2, bool EDGE>
-__global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2)) stage_kernel(StageParams kp)
+// MODAL: a landed ring tile (this lane's element of one variable) -> nodal
+// values in place; every later reader of the slot sees the nodal tile
+template <int P>
+__device__ __forceinline__ void tile_to_nodal(double *tile, int lane)
 {
+    constexpr int N = P + 1;
+    double c[N][N];
+    tile_read<P>(c, tile, lane);
+    to_nodal<P>(c);
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int b = 0; b < N; ++b) tile[(a * N + b) * kLanes + lane] = c[a][b];
+    __syncwarp();
+}
+
+// one variable's row tile (and, with orography, the matching tile of the
+// warp's orography factor) into a ring slot, completing on one mbarrier
+__device__ __forceinline__ void tma_row2(double *dst, const double *src, double *dst2, const double *src2,
+                                         unsigned bytes, unsigned long long *mb)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(2 * bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(mb))
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst2)),
+        "l"(src2), "r"(bytes), "r"(smem_u32(mb))
+        : "memory");
+}
+
+// Wait (thread 0) until a system-scope counter reaches `need`, at most
+// timeout_ns; false on timeout (a neighbour that died or stalled)
+__device__ __forceinline__ bool wait_counter(const unsigned long long *ctr, unsigned long long need,
+                                             unsigned long long timeout_ns)
+{
+    if (ld_acquire_sys(ctr) >= need) return true;
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(ctr) < need) {
+        __nanosleep(64);
+        if (globaltimer() - t0 > timeout_ns) return false;
+    }
+    return true;
+}
+
+template <int P, int F>
+__global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageParams kp)
+{
+    constexpr bool HAS_U = (F & kHasU) != 0;
+    constexpr bool HAS_Y2 = (F & kHasY2) != 0;
+    constexpr bool EDGE = (F & kEdge) != 0;
+    constexpr bool MODAL = (F & kModal) != 0;
+    constexpr bool OROG = (F & kOrog) != 0;
+    static_assert(!(EDGE && (MODAL || HAS_Y2)), "edge launches take nodal states and have one output");
     constexpr int N = P + 1;
     constexpr int NP = N * N;
     constexpr unsigned kTileBytes = NP * kLanes * sizeof(double);   // one variable's row tile
@@ -854,18 +914,22 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
     const int jb = second ? kp.j_begin2 + ((int)blockIdx.y - kp.nchunk1) * kp.rc : kp.j_begin + blockIdx.y * kp.rc;
     const int je = min(jb + kp.rc, second ? kp.j_end2 : kp.j_end);
     if (jb >= je) return;
+    unsigned bad = 0;
     // fused halo exchange: an edge row first waits until the neighbour has
     // delivered this stage's halo row (its previous stage's edge row):
-    // nstrip deliveries per completed stage, counted in our memory
+    // nstrip deliveries per completed stage, counted in our memory.  The
+    // wait is bounded: a neighbour that never delivers raises PEER_TIMEOUT
+    // (the row is then computed from a stale halo and must be discarded).
     if constexpr (EDGE) {
         if (threadIdx.x == 0) {
             const unsigned long long need =
                 ld_acquire_sys(kp.stage_ctr) * (unsigned long long)kp.nstrip * gridDim.z;
             const int g = kp.row0 + jb;
-            if (jb == kp.band_lo && g > 0)
-                while (ld_acquire_sys(kp.recv_count) < need) __nanosleep(64);
+            bool ok = true;
+            if (jb == kp.band_lo && g > 0) ok &= wait_counter(kp.recv_count, need, kp.peer_timeout_ns);
             if (jb == kp.band_hi - 1 && g + 1 < kp.ny)
-                while (ld_acquire_sys(kp.recv_count + 1) < need) __nanosleep(64);
+                ok &= wait_counter(kp.recv_count + 1, need, kp.peer_timeout_ns);
+            if (!ok) bad |= kPeerTimeout;
             asm volatile("fence.proxy.async.global;" ::: "memory");   // peer stores -> TMA reads
         }
         __syncthreads();
@@ -881,6 +945,9 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
     double *sFb = smem + SM::FY1;
     double *sRow = smem + SM::ROW;
     unsigned long long *mbar = reinterpret_cast<unsigned long long *>(smem + SM::MBAR);   // [slot][var]
+    // orography tiles of the momentum warps: [slot][hu, hv][mode][lane]
+    double *const sOB = smem + SM::OB + (v > 0 ? (v - 1) * NP * kLanes : 0);
+    const double *Oz = OROG && v > 0 ? kp.orog + (size_t)(v - 1) * kp.vstride + (size_t)strip * NP * kLanes : nullptr;
 
     // this strip's block of variable v (row 0); per-lane element pointers
     const double *Xb = kp.X + (size_t)blockIdx.z * kp.zstride + (size_t)strip * NP * kLanes;
@@ -894,16 +961,24 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
     const double *Az = HAS_Y2 ? kp.A + lane_off : nullptr;
     double *Y2z = HAS_Y2 ? kp.Y2 + lane_off : nullptr;
     const bool chk = (v == 0) && !face_warp;
-    unsigned bad = 0;
+
+    // the row tile (and orography tile) of local row r into ring slot `slot`
+    auto issue_row = [&](int slot, int r) {
+        double *dst = ring0 + slot * SM::TILE;
+        if constexpr (OROG) {
+            if (v > 0) {
+                tma_row2(dst, Xz + (size_t)r * kp.rstride, sOB + slot * 2 * NP * kLanes,
+                         Oz + (size_t)r * kp.orog_rstride, kTileBytes, mbar + slot * 3 + v);
+                return;
+            }
+        }
+        tma_row(dst, Xz + (size_t)r * kp.rstride, kTileBytes, mbar + slot * 3 + v);
+    };
 
     // rows whose coefficients exist: local r with global row0+r in [0, ny)
     const int r_last = min(kp.nrows - 1, kp.ny - 1 - kp.row0);
     const int last_fetch = min(je, r_last);        // rows jb..last_fetch stream through the ring
 
-    // programmatic dependent launch: the next stage's CTAs may become
-    // resident as ours retire; they run the state-independent prologue
-    // (barriers, row tables) and wait for this grid before touching states
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x == 0) {
         for (int k = 0; k < 6; ++k) mbar_init(mbar + k, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -919,14 +994,12 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             sRow[idx] = kp.rowtab[(size_t)(gfirst + r) * RL::STRIDE + (idx - r * RL::SSTRIDE)];
         }
     }
-    asm volatile("griddepcontrol.wait;" ::: "memory");   // the previous stage's outputs are visible
     __syncthreads();
 
     // prologue: the var warps' elected lanes start streaming rows jb, jb+1
     if (!face_warp && lane == 0) {
-        tma_row(ring0, Xz + (size_t)jb * kp.rstride, kTileBytes, mbar + v);
-        if (jb + 1 <= last_fetch)
-            tma_row(ring0 + SM::TILE, Xz + (size_t)(jb + 1) * kp.rstride, kTileBytes, mbar + 3 + v);
+        issue_row(0, jb);
+        if (jb + 1 <= last_fetch) issue_row(1, jb + 1);
     }
 
     double alpha_x = kp.alpha, alpha_y = kp.alpha;
@@ -944,6 +1017,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
         for (int a = 0; a < N; ++a)
 #pragma unroll
             for (int b = 0; b < N; ++b) c[a][b] = __ldg(src + (a * N + b) * kLanes);
+        if constexpr (MODAL) to_nodal<P>(c);
         double tt[N];
         ytrace<P, false>(c, tt);
 #pragma unroll
@@ -951,6 +1025,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
     }
     if (!face_warp) {
         mbar_wait(mbar + v, 0);                    // row jb landed (this variable)
+        if constexpr (MODAL) tile_to_nodal<P>(ring0, lane);
         // its bottom traces: the face below row jb (the face warp's pre-iteration)
         bad |= owned & stage_bottom<P>(ring0, sFb + v * N * kLanes, lane, chk);
     }
@@ -1019,7 +1094,8 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             cp_wait_all();                             // gathers of this row's phase B (and row tables)
             __syncwarp();
             if (it + 1 < je) {
-                border_traces<P>(smem + SM::HB, next_tile, smem + SM::HL, smem + SM::E0, smem + SM::HR, lane);
+                border_traces<P, MODAL>(smem + SM::HB, next_tile, smem + SM::HL, smem + SM::E0, smem + SM::HR,
+                                        lane);
                 // every lane computes the same face (uniform control flow, identical stores)
                 face_flux_call<P>(SM::HL, 1, 0, SM::E0, 1, 0, SM::F0 + ((k + 1) & 1) * 3 * N, 1, 0,
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
@@ -1056,6 +1132,7 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
             TSTAMP(0);
             if (jl + 1 <= last_fetch) {
                 mbar_wait(mbar + (slot ^ 1) * 3 + v, ((k + 1) >> 1) & 1);   // X(jl+1)
+                if constexpr (MODAL) tile_to_nodal<P>(ring0 + (slot ^ 1) * SM::TILE, lane);
                 // its bottom traces for the face warp's y-face above row jl
                 bad |= owned & stage_bottom<P>(ring0 + (slot ^ 1) * SM::TILE, sFa + v * N * kLanes, lane, chk);
             }
@@ -1073,19 +1150,20 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
                                            kp.alpha_mode, 0, 0.0, 0.0, alpha_x, kp.bdy});
             }
             double vol[N][N];
+            const double *sB = OROG ? sOB + slot * 2 * NP * kLanes : nullptr;
             if constexpr (vol_rolled<P>()) {
                 double *sE = smem + SM::E + v * NP * kLanes;
                 if (v == 0)
-                    volume_rolled<P, 0>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sE);
+                    volume_rolled<P, 0, false>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sE, sB);
                 else if (v == 1)
-                    volume_rolled<P, 1>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sE);
+                    volume_rolled<P, 1, OROG>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sE, sB);
                 else
-                    volume_rolled<P, 2>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sE);
+                    volume_rolled<P, 2, OROG>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sE, sB);
             } else {
                 if (v == 0)
-                    volume<P, false>(vol, v, ringS + slot * SM::TILE, row, lane, kp);
+                    volume<P, false, false>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sB);
                 else
-                    volume<P, true>(vol, v, ringS + slot * SM::TILE, row, lane, kp);
+                    volume<P, true, OROG>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sB);
             }
             TSTAMP(3);
             __syncthreads();                           // barrier 2
@@ -1101,15 +1179,15 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
                 if (jl == kp.band_hi - 1 && kp.peer_row[1])
                     Ypeer2 = kp.peer_row[1] + (size_t)blockIdx.z * kp.peer_zstride[1] + off;
             }
-            bad |= finalize<P, HAS_U, HAS_Y2>(vol, cur, HAS_U ? Uz + roff : nullptr,
-                                              HAS_Y2 ? Az + roff : nullptr, HAS_Y2 ? Y2z + roff : nullptr, v, sFX,
-                                      smem + SM::F0 + slot * 3 * N, sFa, sFb, row, lane,
-                                      owned, Yz + roff, kp, Ypeer, Ypeer2);
+            bad |= finalize<P, HAS_U, HAS_Y2, MODAL>(vol, cur, HAS_U ? Uz + roff : nullptr,
+                                                     HAS_Y2 ? Az + roff : nullptr, HAS_Y2 ? Y2z + roff : nullptr,
+                                                     v, sFX, smem + SM::F0 + slot * 3 * N, sFa, sFb, row, lane,
+                                                     owned, Yz + roff, kp, Ypeer, Ypeer2);
             // X(jl) is consumed: stream row jl+2 into its slot (L2-warm by now)
             __syncwarp();
             if (lane == 0 && jl + 2 <= last_fetch) {
                 fence_proxy_async();
-                tma_row(cur, Xz + (size_t)(jl + 2) * kp.rstride, kTileBytes, mbar + slot * 3 + v);
+                issue_row(slot, jl + 2);
             }
             TSTAMP(5);
             TACC(0, tk0 - tks);   // phase A work (eval)
@@ -1133,7 +1211,8 @@ __global__ void __launch_bounds__(kThreads, (P <= 2 ? 4 : P == 3 ? DG_MINB : 2))
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && lane == 0) {
         atomicOr(kp.status, bad);
-        atomicMin(kp.first_tag, kp.tag);
+        for (int b = 0; b < kStatusBits; ++b)
+            if (bad & (1u << b)) atomicMin(kp.first_tag + b, kp.tag);
     }
     if constexpr (EDGE) {
         // publish the edge rows stored into the neighbours' halos, then count
@@ -1196,6 +1275,114 @@ __global__ void __launch_bounds__(96) convert_kernel(const double *in, double *o
             if (!TO_NODAL) s *= 0.25 * (double)((2 * q + 1) * (2 * r + 1));
             out[off + (q * N + r) * kLanes] = s;
         }
+}
+
+// Global-mode alpha (dg.py:389-411, models.py:271-280): max over all
+// traces of the rows [jlo, jhi) into out[0] (x faces) and out[1] (y faces,
+// with cos of the edge latitude); MODAL converts each tile first.
+template <int P, bool MODAL>
+__global__ void alpha_prepass_kernel(const double *__restrict__ X, long long zstride, long long rstride,
+                                     long long vstride, int nx, int row0, int jlo, int jhi,
+                                     const double *__restrict__ cos_edge, double inv_r, double gravity,
+                                     double h_floor, double *out)
+{
+    constexpr int N = P + 1;
+    constexpr int NP = N * N;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int jl = jlo + blockIdx.y;
+    if (i >= nx || jl >= jhi) return;
+    const double *base = X + (size_t)blockIdx.z * zstride + (size_t)jl * rstride;
+    const int jg = row0 + jl;
+    double tr[4][3][N];   // L R B T, from the nodal tile u[i][j]
+    for (int v = 0; v < 3; ++v) {
+        double u[N][N];
+        for (int a = 0; a < N; ++a)
+            for (int b = 0; b < N; ++b)
+                u[a][b] = base[(size_t)v * vstride + (size_t)(i >> 5) * NP * 32 + (a * N + b) * 32 + (i & 31)];
+        if constexpr (MODAL) to_nodal<P>(u);
+        for (int q = 0; q < N; ++q) {
+            double l = 0, r = 0, bo = 0, t = 0;
+            for (int k = 0; k < N; ++k) {
+                const double lo = c_nod[P].lm[k], hi = c_nod[P].lm[N - 1 - k];
+                l = fma(lo, u[k][q], l);
+                r = fma(hi, u[k][q], r);
+                bo = fma(lo, u[q][k], bo);
+                t = fma(hi, u[q][k], t);
+            }
+            tr[0][v][q] = l;
+            tr[1][v][q] = r;
+            tr[2][v][q] = bo;
+            tr[3][v][q] = t;
+        }
+    }
+    double ax = 0.0, ay = 0.0;
+    for (int e = 0; e < 4; ++e)
+        for (int q = 0; q < N; ++q) {
+            const double h = tr[e][0][q];
+            const double m = tr[e][e < 2 ? 1 : 2][q];
+            const double a = (fabs(m / fmax(h, h_floor)) + sqrt(gravity * fmax(h, 0.0))) * inv_r;
+            if (e < 2)
+                ax = fmax(ax, a);
+            else
+                ay = fmax(ay, a * cos_edge[jg + (e == 3 ? 1 : 0)]);
+        }
+    atomicMax(reinterpret_cast<unsigned long long *>(out), (unsigned long long)__double_as_longlong(ax));
+    atomicMax(reinterpret_cast<unsigned long long *>(out + 1), (unsigned long long)__double_as_longlong(ay));
+}
+
+// Initial-condition projection (basis.py:206-233) of nodal values onto the
+// modal basis.
+// grid (ceil(nx/128), ny, 3), block 128: one thread per element and
+// variable.  f: nodal values [3][ny][nx][n*n] at the (p+1)^2 Gauss nodes
+// (q = qi*n + qj, qi along lambda); moments = determ sum_q w_qi w_qj
+// cos(theta_qj) phi_m(q) f_q (sum-factorised), then the Kronecker inverse
+// mass c[a][b] = (2a+1) sum_bb T_j[b][bb] moments[a][bb] (T_j: the a = 0
+// block of the row's M^-1, from the row table); written to every level.
+template <int P>
+__global__ void project_kernel(const double *__restrict__ f, const double *__restrict__ cos_nodes,
+                               const double *__restrict__ rowtab, int row_stride, int t_off, DiagLayout L,
+                               int nz, double determ, double *Y)
+{
+    constexpr int N = P + 1;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, v = blockIdx.z;
+    if (i >= L.nx) return;
+    const double *fv = f + (((size_t)v * L.ny + j) * L.nx + i) * (N * N);
+    const double *cj = cos_nodes + (size_t)j * N;
+    double g[N][N];   // g[qi][b] = sum_qj wP_b(qj) cos_qj f(qi, qj)
+#pragma unroll
+    for (int qi = 0; qi < N; ++qi)
+#pragma unroll
+        for (int b = 0; b < N; ++b) {
+            double acc = 0.0;
+#pragma unroll
+            for (int qj = 0; qj < N; ++qj) acc = fma(c_nod[P].wp[b][qj] * cj[qj], fv[qi * N + qj], acc);
+            g[qi][b] = acc;
+        }
+    double mom[N][N];
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int b = 0; b < N; ++b) {
+            double acc = 0.0;
+#pragma unroll
+            for (int qi = 0; qi < N; ++qi) acc = fma(c_nod[P].wp[a][qi], g[qi][b], acc);
+            mom[a][b] = determ * acc;
+        }
+    const double *T = rowtab + (size_t)j * row_stride + t_off;
+    for (int z = 0; z < nz; ++z) {
+        double *y = Y + (size_t)z * L.zstride + (size_t)j * L.rstride + (size_t)v * L.vstride +
+                    (size_t)(i >> 5) * L.nphi * 32 + (i & 31);
+#pragma unroll
+        for (int a = 0; a < N; ++a)
+#pragma unroll
+            for (int b = 0; b < N; ++b) {
+                double acc = 0.0;
+#pragma unroll
+                for (int bb = 0; bb < N; ++bb) acc = fma(T[b * N + bb], mom[a][bb], acc);
+                y[(a * N + b) * 32] = (double)(2 * a + 1) * acc;
+            }
+    }
 }
 
 #undef LEG

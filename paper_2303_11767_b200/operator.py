@@ -110,6 +110,8 @@ class State:
         if tuple(data.shape) != device_shape(nz, ny, nphi, nx) or not data.is_contiguous():
             raise ValueError(f"State data must be contiguous {device_shape(nz, ny, nphi, nx)} "
                              f"(nz, ny, 3, nstrip, nphi, {STRIP}), got {tuple(data.shape)}")
+        if data.data_ptr() % 16:
+            raise ValueError("State data must be 16-byte aligned (the kernels move row tiles by TMA)")
         self.data = data
         self.names = VAR_NAMES
         self.nx, self.ny, self.nz, self.nphi = nx, ny, nz, nphi
@@ -150,7 +152,7 @@ class _Context:
     """Owns one dgswe_ctx (C ABI) for a band of latitude rows."""
 
     def __init__(self, mesh: Mesh, p: int, model: SphereSWEModel, rusanov: RusanovParams, nz: int,
-                 quad, vander, Minv, row0=0, nrows=None, jlo=None, jhi=None, row_chunk=0):
+                 quad, vander, Minv, row0=0, nrows=None, jlo=None, jhi=None, row_chunk=0, bottom=None):
         lib = _lib.load()
         ny = mesh.ny
         nrows = ny if nrows is None else nrows
@@ -166,6 +168,8 @@ class _Context:
             "cos_r_edge": np.cos(mesh.y_edges) / R, "cos_edge": np.cos(mesh.y_edges),
             "minv": Minv,
         }
+        if bottom is not None:
+            arrs["orog"] = bottom                             # (ny, nx, n*n) b at the Gauss nodes
         keep = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in arrs.items()}
         tabs = _lib.Tables(**{k: v.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
                               for k, v in keep.items()})
@@ -200,11 +204,18 @@ class _Context:
         return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
     def status(self, reset=True):
+        """(flags, smallest tag over the raised bits)."""
+        flags, tags = self.status_tags(reset)
+        return flags, min(tags)
+
+    def status_tags(self, reset=True):
+        """(flags, [smallest tag per status bit]) -- POSITIVITY, NONFINITE,
+        MEAN_NONPOS, PEER_TIMEOUT (INT32_MAX where the bit is clear)."""
         flags = ctypes.c_uint32(0)
-        tag = ctypes.c_int32(0)
-        _lib.check(self.lib.dgswe_status(self.h, ctypes.byref(flags), ctypes.byref(tag),
-                                         int(reset), self.stream()), "dgswe_status")
-        return flags.value, tag.value
+        tags = (ctypes.c_int32 * _lib.STATUS_BITS)()
+        _lib.check(self.lib.dgswe_status_tags(self.h, ctypes.byref(flags), tags, int(reset),
+                                              self.stream()), "dgswe_status_tags")
+        return flags.value, list(tags)
 
     def launches(self) -> int:
         return int(self.lib.dgswe_launch_count(self.h))
@@ -257,11 +268,25 @@ class SpatialOperator:
         self.halo_shape = (mesh.nx + 2, mesh.ny + 2, self.nz)
         self.M_rows, self.Minv_rows = sphere_row_mass_matrices(self.p, mesh, self.quad)
         self.M_planar = None
+        self.bottom_nodal = self._bottom_at_nodes()
         with torch.cuda.device(self.device):
             self._ctx = _Context(mesh, self.p, model, self.rusanov, self.nz, self.quad, self.vander,
-                                 self.Minv_rows, row_chunk=row_chunk)
+                                 self.Minv_rows, row_chunk=row_chunk, bottom=self.bottom_nodal)
         self._phi_dev = None
         self._scratch = {}
+
+    def _bottom_at_nodes(self):
+        """(ny, nx, n*n) orography b at every element's Gauss nodes (q = qi n + qj,
+        qi along lambda), or None without orography (the reference's model)."""
+        b = getattr(self.model, "bottom", None)
+        if b is None:
+            return None
+        from .geometry import element_node_coords
+        lam, th = element_node_coords(self.mesh, self.quad.nodes)      # (nx, n), (ny, n)
+        n = self.p + 1
+        vals = np.asarray(b(lam[None, :, :, None], th[:, None, None, :]), dtype=np.float64)
+        vals = np.broadcast_to(vals, (self.mesh.ny, self.mesh.nx, n, n))
+        return np.ascontiguousarray(vals.reshape(self.mesh.ny, self.mesh.nx, n * n))
 
     # -- state construction -------------------------------------------------
 
@@ -325,6 +350,8 @@ class SpatialOperator:
     def raise_on_status(self, flags: int):
         if flags & _lib.STATUS_POSITIVITY:
             raise PositivityError("non-positive water height at a quadrature node")
+        if flags & _lib.STATUS_PEER_TIMEOUT:
+            raise RuntimeError("a latitude-band neighbour's halo rows never arrived")
 
     def assemble_rhs(self, state: State, out: State | None = None, check: bool = True) -> State:
         """Full right-hand side M^-1 (volume - boundary + source); raises
@@ -388,6 +415,18 @@ class SpatialOperator:
         current stream (which waits for the last copy); ``status()`` syncs.
         With ``graph`` the ~10 launches per chunk are captured once per
         (host buffer, dt, tag, check_mean) and replayed as one CUDA graph."""
+        mesh = self.mesh
+        ny, nz = mesh.ny, self.nz
+        # argument checks before any graph lookup: a replay must never run on
+        # a buffer the capture was not made for
+        if tuple(host.shape) != tuple(self.state_shape) or host.dtype != torch.float64:
+            raise ValueError(f"host state must be float64 {tuple(self.state_shape)}")
+        if host.device.type != "cpu" or not host.is_pinned() or not host.is_contiguous():
+            raise ValueError("host state must be a contiguous pinned CPU tensor")
+        if chunks is not None and not 1 <= int(chunks) <= ny:
+            raise ValueError(f"chunks must be in [1, ny={ny}], got {chunks}")
+        if self.rusanov.mode == "global" and self.rusanov.alpha is None:
+            raise ValueError("global-alpha mode needs the whole state before a stage: use ssprk3_steps")
         if graph:
             gkey = ("hostgraph", host.data_ptr(), float(dt), int(tag), bool(check_mean), chunks)
             g = self._scratch.get(gkey)
@@ -404,12 +443,6 @@ class SpatialOperator:
                 return
             g.replay()
             return
-        mesh = self.mesh
-        ny, nz = mesh.ny, self.nz
-        if tuple(host.shape) != tuple(self.state_shape) or host.dtype != torch.float64:
-            raise ValueError(f"host state must be float64 {tuple(self.state_shape)}")
-        if self.rusanov.mode == "global" and self.rusanov.alpha is None:
-            raise ValueError("global-alpha mode needs the whole state before a stage: use ssprk3_steps")
         nch = chunks if chunks is not None else max(1, min(16, ny // 4))
         bounds = [ny * c // nch for c in range(nch + 1)]
         key = ("host", tuple(host.shape))
@@ -470,6 +503,50 @@ class SpatialOperator:
         cur.wait_stream(s_out)
         cur.wait_stream(s_in)
 
+    def rk_step_fused(self, state: State, dt: float, order: int, bufs, tag: int = 0) -> State:
+        """One step of tableau(order) (1..4) in fused stage form on modal
+        states: ``order`` single-launch stage kernels (each converts its
+        tiles to nodal values in shared memory and its outputs back to modes;
+        no other kernel, no allocation), the last one writing the new state
+        into ``bufs[order-1]`` with the non-finite check.  Returns that buffer;
+        ``state`` is left untouched (the caller swaps on success, so a
+        PositivityError leaves u^n in place like the reference)."""
+        c = self._ctx
+        st = c.stream()
+        u = state.data
+
+        def stage(a, U, b, X, g, Y, check=False):
+            _lib.check(c.lib.dgswe_stage_rows_checked(
+                c.h, float(a), _ptr(U), float(b), _ptr(X), float(g), _ptr(Y), int(tag), 0, self.mesh.ny,
+                int(check), 0, st), "dgswe_stage_rows_checked")
+
+        def stage2(a, U, b, X, g, Y, A, g2, Y2):
+            _lib.check(c.lib.dgswe_stage2(c.h, float(a), _ptr(U), float(b), _ptr(X), float(g), _ptr(Y),
+                                          _ptr(A), float(g2), _ptr(Y2), int(tag), 0, self.mesh.ny, st),
+                       "dgswe_stage2")
+
+        b = [x.data if isinstance(x, State) else x for x in bufs]
+        if order == 1:
+            stage(0.0, None, 1.0, u, dt, b[0], check=True)
+            return b[0]
+        if order == 2:
+            stage(0.0, None, 1.0, u, dt, b[0])
+            stage(0.5, u, 0.5, b[0], 0.5 * dt, b[1], check=True)
+            return b[1]
+        if order == 3:
+            stage(0.0, None, 1.0, u, dt, b[0])
+            stage(0.75, u, 0.25, b[0], 0.25 * dt, b[1])
+            stage(1.0 / 3.0, u, 2.0 / 3.0, b[1], (2.0 / 3.0) * dt, b[2], check=True)
+            return b[2]
+        if order == 4:
+            w1, w2, acc, out = b[0], b[1], b[2], b[3]
+            stage2(0.0, None, 1.0, u, 0.5 * dt, w1, u, dt / 6.0, acc)
+            stage2(1.0, u, 0.0, w1, 0.5 * dt, w2, acc, dt / 3.0, acc)
+            stage2(1.0, u, 0.0, w2, dt, w1, acc, dt / 3.0, acc)
+            stage(1.0, acc, 0.0, w1, dt / 6.0, out, check=True)
+            return out
+        raise ValueError(f"unsupported RK order {order}; choose 1..4")
+
     def stage2(self, a: float, U: State | None, b: float, X: State, g: float, Y: State, A: State,
                g2: float, Y2: State, tag: int = 0):
         """Y = a U + b X + g RHS(X) and Y2 = A + g2 RHS(X) in one launch (no sync)."""
@@ -482,6 +559,9 @@ class SpatialOperator:
     def status(self, reset: bool = True):
         return self._ctx.status(reset)
 
+    def status_tags(self, reset: bool = True):
+        return self._ctx.status_tags(reset)
+
     def launch_count(self) -> int:
         return self._ctx.launches()
 
@@ -493,9 +573,6 @@ class SpatialOperator:
             self._phi_dev = torch.from_numpy(self.vander.phi).to(self.device)
         U = torch.einsum("qm,zjvmi->vijzq", self._phi_dev, lon_major(state.data, self.mesh.nx))
         return {n: U[v].cpu().numpy() for v, n in enumerate(VAR_NAMES)}
-
-    def interior_theta(self):
-        return None
 
     def max_physical_speed(self, state: State) -> float:
         """max over interior nodes of max(|u|,|v|) + sqrt(g h) (models.py:282-285)."""

@@ -11,6 +11,12 @@ Flux-form SWE in lat-lon coordinates, conserved (h, hu, hv):
     F = (1/R) (hu, hu u + g h^2/2, hu v)
     G = (cos/R) (hv, hu v, hv v + g h^2/2)
     S = (0, t hv, -(g h^2/2) sin/R - t hu),  t = u sin/R + 2 Omega sin cos
+
+Extension (not in the reference, whose SPEC.md:157 lists orography as a
+non-goal): an optional bottom topography b(lambda, theta) adds the momentum
+sources -(g h / R) db/dlambda and -(g h cos / R) db/dtheta -- the
+cos-weighted form of -g h grad b -- for Williamson test case 5.  h is the
+fluid depth; the free surface is h + b.
 """
 
 from __future__ import annotations
@@ -32,12 +38,13 @@ class SphereSWEModel:
     has_source = True
     is_spherical = True
 
-    def __init__(self, constants: PhysicalConstants, h_ref: float = 1.0):
+    def __init__(self, constants: PhysicalConstants, h_ref: float = 1.0, bottom=None):
         if constants.gravity <= 0:
             raise ValueError("gravity must be positive")
         self.constants = constants
         self.gravity = float(constants.gravity)
         self.h_floor = 1e-8 * float(h_ref)
+        self.bottom = bottom          # None, or b(lambda, theta) in metres (numpy)
 
     def _floor_and_celerity(self, U):
         h = U["h"]
@@ -69,5 +76,6 @@ class SphereSWEModel:
         return float(np.max(vel + c))
 
 
-def swe_sphere_model(constants: PhysicalConstants, h_ref: float = 1.0) -> SphereSWEModel:
-    return SphereSWEModel(constants, h_ref)
+def swe_sphere_model(constants: PhysicalConstants, h_ref: float = 1.0, bottom=None) -> SphereSWEModel:
+    """models.py:293-295; ``bottom`` (extension) is the orography b(lambda, theta)."""
+    return SphereSWEModel(constants, h_ref, bottom)

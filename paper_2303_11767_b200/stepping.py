@@ -4,9 +4,11 @@ Same API as /root/reference/pkg/src/dgswe/timestep.py (``ButcherTableau``,
 ``tableau``, ``TimeControls``, ``DivergenceError``, ``StepLog``,
 ``rk_step``, ``integrate``).  Two device paths:
 
-* ``rk_step`` -- Butcher form for any tableau: per stage a device copy,
-  fused axpy launches (two roundings, like ``_axpy`` timestep.py:132-141)
-  and one fused RHS launch; one status read per step.
+* ``rk_step`` -- with ``tableau(1..4)`` one single-launch stage kernel per
+  stage on the modal state (Shu-Osher / RK4-accumulator forms); any other
+  tableau (or ``fused=False``) in Butcher form: per stage a device copy,
+  axpy launches (two roundings, like ``_axpy`` timestep.py:132-141) and one
+  RHS launch.  One status read per step.
 * ``integrate`` with ``tableau(1..4)`` -- the tableaux of timestep.py:57-82
   evaluated as fused stages (RHS + stage combination in one kernel):
   Euler; Heun and SSPRK3 in Shu-Osher form (SSPRK3: three launches per step,
@@ -140,16 +142,37 @@ def _fused_order(tab: ButcherTableau):
     return None
 
 
-def rk_step(state, rhs_fn, dt: float, tab: ButcherTableau, workspace: _RKWorkspace | None = None):
-    """One explicit RK step in Butcher form, updating ``state`` in place.
+def rk_step(state, rhs_fn, dt: float, tab: ButcherTableau, workspace: _RKWorkspace | None = None,
+            fused: bool = True):
+    """One explicit RK step, updating ``state`` in place (timestep.py:149-167).
 
-    Raises PositivityError (from the RHS) or DivergenceError when the
-    updated state is non-finite, like timestep.py:149-167.
+    With our operator's ``assemble_rhs`` and ``tableau(1..4)`` (``fused``):
+    one single-launch stage kernel per stage on the modal state (the stage
+    combination fused into the RHS kernel: SSPRK3 moves 21.3 B/DOF instead
+    of the Butcher form's copies and axpys), the new state written into a
+    workspace buffer that is swapped into ``state`` on success.  Otherwise
+    (or ``fused=False``) the Butcher form of the reference: per stage a
+    copy, axpys with two roundings and one RHS launch.  Both read the status
+    once per step: PositivityError (from any stage's RHS) leaves ``state``
+    at u^n like the reference; DivergenceError (non-finite update) is raised
+    after the update, as the reference's finite check does.
     """
     ws = workspace or _RKWorkspace(state, tab.s)
     op = _device_operator(rhs_fn)
     if op is None:
         return _rk_step_generic(state, rhs_fn, dt, tab, ws)
+    order = _fused_order(tab) if fused else None
+    if order is not None:
+        bufs = [ws.stage_input] + list(ws.k)
+        new = op.rk_step_fused(state, dt, order, bufs)
+        flags, _ = op.status(reset=True)
+        op.raise_on_status(flags)                   # PositivityError: state still u^n
+        # the new state becomes ``state``; its old buffer joins the workspace
+        slot = next(b for b in bufs if b.data is new)
+        state.data, slot.data = new, state.data
+        if flags & _lib.STATUS_NONFINITE:
+            raise DivergenceError("non-finite state after RK update", -1, float("nan"))
+        return state
     for i in range(tab.s):
         ws.stage_input.data.copy_(state.data)      # u * 1.0 is exact
         for j in range(i):
@@ -157,13 +180,14 @@ def rk_step(state, rhs_fn, dt: float, tab: ButcherTableau, workspace: _RKWorkspa
             if coef != 0.0:
                 op.axpy(coef, ws.k[j], ws.stage_input)
         op.assemble_rhs(ws.stage_input, out=ws.k[i], check=False)
+    flags, _ = op.status(reset=True)               # before the update: u^n stays on error
+    op.raise_on_status(flags)
     last = max((i for i in range(tab.s) if dt * tab.b[i] != 0.0), default=-1)
     for i in range(tab.s):
         coef = dt * tab.b[i]
         if coef != 0.0:
             op.axpy(coef, ws.k[i], state, check_finite=(i == last))
     flags, _ = op.status(reset=True)
-    op.raise_on_status(flags)
     if flags & _lib.STATUS_NONFINITE or last < 0 and not math.isfinite(state.max_abs()):
         raise DivergenceError("non-finite state after RK update", -1, float("nan"))
     return state
@@ -208,7 +232,12 @@ def integrate(state, operator, controls: TimeControls, tab: ButcherTableau, call
     With our SpatialOperator and ``tableau(1..4)`` the steps run as fused
     CUDA-graph batches of up to ``batch`` steps between callback
     cadences; errors are detected per batch and reported with the exact
-    failing step and time, as the reference does per step.
+    failing step and time, as the reference does per step, and ``state``
+    is left where the reference leaves it: a batch starts from a snapshot,
+    and on failure the state is restored and re-advanced to the step before
+    the failing one (non-positive / non-finite) or through it (cell mean,
+    which the reference checks after the update).  ``fused=False`` steps
+    with the Butcher-form ``rk_step`` (the reference's operation order).
     """
     log = StepLog()
     log.diameter = min_effective_diameter(operator.mesh)
@@ -233,7 +262,7 @@ def integrate(state, operator, controls: TimeControls, tab: ButcherTableau, call
         ws = _RKWorkspace(state, tab.s)
         for step, (h, t0, t1) in enumerate(steps, start=1):
             try:
-                rk_step(state, operator.assemble_rhs, h, tab, ws)
+                rk_step(state, operator.assemble_rhs, h, tab, ws, fused=False)
             except (PositivityError, DivergenceError) as exc:
                 log.steps, log.t = step - 1, t0
                 log.wall_seconds = time.perf_counter() - started
@@ -253,6 +282,8 @@ def integrate(state, operator, controls: TimeControls, tab: ButcherTableau, call
     cadences = [c for c, _ in callbacks]
     step = 0
     operator.status(reset=True)
+    snapshot = state.data.clone()
+    check_mean = check_positivity == "h"
     while step < n_steps:
         h = steps[step][0]
         k = 1
@@ -260,19 +291,30 @@ def integrate(state, operator, controls: TimeControls, tab: ButcherTableau, call
             if any((step + k) % c == 0 for c in cadences):
                 break
             k += 1
-        operator.rk_steps(state, h, k, order, check_mean=check_positivity == "h")
-        flags, tag = operator.status(reset=True)
+        snapshot.copy_(state.data)
+        operator.rk_steps(state, h, k, order, check_mean=check_mean)
+        flags, tags = operator.status_tags(reset=True)
         if flags:
+            # the earliest failing step decides; at equal steps the RHS
+            # positivity check precedes the finite check, which precedes the
+            # cell-mean check (timestep.py:162-166, 220-226)
+            tag, bit = min((tags[b], b) for b in range(_lib.STATUS_BITS) if flags & (1 << b))
             bad = step + tag + 1
             t0, t1 = steps[bad - 1][1], steps[bad - 1][2]
+            mean = (1 << bit) == _lib.STATUS_MEAN_NONPOS
+            state.data.copy_(snapshot)
+            redo = bad - step if mean else bad - 1 - step
+            if redo > 0:
+                operator.rk_steps(state, h, redo, order)
+                operator.status(reset=True)
             log.wall_seconds = time.perf_counter() - started
-            if flags & (_lib.STATUS_POSITIVITY | _lib.STATUS_NONFINITE):
-                log.steps, log.t = bad - 1, t0
-                what = ("non-positive water height at a quadrature node"
-                        if flags & _lib.STATUS_POSITIVITY else "non-finite state after RK update")
-                raise DivergenceError(what, bad, t0)
-            log.steps, log.t = bad, t1
-            raise DivergenceError("cell-mean h lost positivity", bad, t1)
+            if mean:
+                log.steps, log.t = bad, t1
+                raise DivergenceError("cell-mean h lost positivity", bad, t1)
+            log.steps, log.t = bad - 1, t0
+            what = ("non-positive water height at a quadrature node"
+                    if (1 << bit) == _lib.STATUS_POSITIVITY else "non-finite state after RK update")
+            raise DivergenceError(what, bad, t0)
         step += k
         for cadence, fn in callbacks:
             if step % cadence == 0 or step == n_steps:

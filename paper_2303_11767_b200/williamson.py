@@ -6,6 +6,10 @@ API of /root/reference/pkg/src/dgswe/cases.py (``CaseConfig``,
 Williamson et al. (1992) equations: TC2 (90)-(95) with alpha = 0,
 TC6 (142)-(149).  The planar cases (advection, geostrophic adjustment) are
 outside the spherical hot path and raise NotImplementedError.
+Williamson TC5 (flow over an isolated mountain) is an extension: the
+reference has no orography; its bottom topography enters the
+model's momentum sources (physics.py) and the oracle restates the same
+discretisation (parity unpinned against the reference).
 """
 
 from __future__ import annotations
@@ -25,6 +29,14 @@ TC6_OMEGA = 7.848e-6
 TC6_K = 7.848e-6
 TC6_H0 = 8.0e3
 TC6_R = 4
+# test case 5 (zonal flow over an isolated mountain), Williamson et al. (1992)
+# section 3.5 -- EXTENSION: the reference has no orography
+TC5_U0 = 20.0
+TC5_H0 = 5960.0
+TC5_HS0 = 2000.0
+TC5_RM = math.pi / 9.0
+TC5_LC = 1.5 * math.pi        # lambda_c = -pi/2 on [0, 2 pi)
+TC5_TC = math.pi / 6.0
 
 def _xp(*arrays):
     """numpy, or torch when the coordinates are torch tensors (the device
@@ -43,8 +55,9 @@ def _zeros(lam, th):
     return xp.zeros(xp.broadcast_shapes(lam.shape, th.shape), dtype=xp.float64, device=lam.device)
 
 
-CASE_IDS = ("advection_sine", "geostrophic_adjustment", "williamson_tc2", "williamson_tc6")
-SPHERE_CASES = ("williamson_tc2", "williamson_tc6")
+CASE_IDS = ("advection_sine", "geostrophic_adjustment", "williamson_tc2", "williamson_tc6",
+            "williamson_tc5")
+SPHERE_CASES = ("williamson_tc2", "williamson_tc6", "williamson_tc5")
 
 
 @dataclass(frozen=True)
@@ -70,6 +83,7 @@ _DEFAULTS = {
     "geostrophic_adjustment": dict(nx=50, ny=50, p=3, rk=4, t_final=36000.0, dt=100.0),
     "williamson_tc2": dict(nx=20, ny=20, p=3, rk=4, t_final=2.0 * DAY, courant=0.2),
     "williamson_tc6": dict(nx=40, ny=20, p=3, rk=4, t_final=8.0 * DAY, dt=4.0),
+    "williamson_tc5": dict(nx=40, ny=20, p=4, rk=3, t_final=15.0 * DAY, dt=2.0),
 }
 
 
@@ -120,6 +134,29 @@ def tc6_fields(constants: PhysicalConstants = EARTH):
     return height, winds
 
 
+def tc5_bottom(lam, th):
+    """Isolated conical mountain: b = hs0 (1 - r/R_m), r = min(R_m, dist to
+    (lambda_c, theta_c)) in the (lambda, theta) plane (Williamson eq. 134)."""
+    xp = _xp(lam, th)
+    d = xp.sqrt((lam - TC5_LC) ** 2 + (th - TC5_TC) ** 2)
+    r = xp.minimum(d, xp.full_like(d, TC5_RM) if xp is not np else TC5_RM)
+    return TC5_HS0 * (1.0 - r / TC5_RM)
+
+
+def ic_williamson_tc5(constants: PhysicalConstants = EARTH):
+    """TC2-like balanced zonal flow (u0 = 20 m/s, h0 = 5960 m) over the
+    mountain: depth h = h0 - (R Omega u0 + u0^2/2) sin^2(theta)/g - b."""
+    g = constants.gravity
+    k = constants.radius * constants.omega * TC5_U0 + 0.5 * TC5_U0 * TC5_U0
+
+    def depth(lam, th):
+        return (g * TC5_H0 - k * _xp(th).sin(th) ** 2) / g - tc5_bottom(lam, th)
+
+    return {"h": depth,
+            "hu": lambda lam, th: depth(lam, th) * TC5_U0 * _xp(th).cos(th),
+            "hv": _zeros}
+
+
 def ic_williamson_tc6(constants: PhysicalConstants = EARTH):
     height, winds = tc6_fields(constants)
     return {"h": height,
@@ -150,6 +187,10 @@ def build_case(config: CaseConfig, constants: PhysicalConstants = EARTH) -> RunS
         return RunSetup(config, build_latlon_mesh(config.nx, config.ny, constants.radius),
                         swe_sphere_model(constants, h_ref=TC6_H0), ic_williamson_tc6(constants),
                         None, constants)
+    if case == "williamson_tc5":
+        model = swe_sphere_model(constants, h_ref=TC5_H0, bottom=tc5_bottom)
+        return RunSetup(config, build_latlon_mesh(config.nx, config.ny, constants.radius), model,
+                        ic_williamson_tc5(constants), None, constants)
     if case in CASE_IDS:
         raise NotImplementedError(f"{case!r} is a planar case, outside the spherical hot path")
     raise ValueError(f"unknown case {case!r}; choose from {CASE_IDS}")

@@ -70,6 +70,11 @@ CASES = [
     ("tc6_nz2", "williamson_tc6", 12, 6, 2, 2, 3, 20.0, 5, ("local", None), True),
     ("tc6_wide", "williamson_tc6", 70, 8, 3, 1, 3, 2.0, 5, ("local", None), True),
     ("tc2_c2_shape", "williamson_tc2", 360, 180, 3, 1, 3, 0.05, 3, ("local", None), False),
+    # BASELINE.json configs at full size (SHA / mass / L2 pins only; `--only` regenerates these
+    # without rerunning the small cases): C2 100 steps, C3 20 steps, C4 shape 3 steps
+    ("c2_full", "williamson_tc2", 360, 180, 3, 1, 3, 0.05, 100, ("local", None), False),
+    ("c3_full", "williamson_tc6", 720, 360, 3, 1, 3, 5e-3, 20, ("local", None), False),
+    ("c4_full", "williamson_tc6", 1440, 720, 4, 1, 3, 5e-4, 3, ("local", None), False),
 ]
 
 TABLE_SHAPES = [(6, 4, 0), (8, 5, 1), (10, 6, 2), (12, 6, 3), (8, 4, 4), (6, 4, 5), (20, 10, 3)]
@@ -95,15 +100,21 @@ def initial_state(setup, op, nz, name):
 
 
 def main():
+    only = None
+    if "--only" in sys.argv:
+        only = set(sys.argv[sys.argv.index("--only") + 1].split(","))
     arrays = {}
     meta = {"reference": REF, "numpy": np.__version__, "cases": {}, "tables": []}
+    if only is not None:
+        # merge into the existing fixtures: the npz is left untouched (no full arrays)
+        meta = json.load(open(os.path.join(HERE, "golden.json")))
     try:
         import numba
         meta["numba"] = numba.__version__
     except ImportError:  # pragma: no cover
         meta["numba"] = None
 
-    for (nx, ny, p) in TABLE_SHAPES:
+    for (nx, ny, p) in (TABLE_SHAPES if only is None else ()):
         setup, op = build("williamson_tc6", nx, ny, p, 1, ("local", None))
         tag = f"tab_{nx}x{ny}_p{p}"
         meta["tables"].append(tag)
@@ -127,6 +138,10 @@ def main():
                 arrays[f"{tag}/{cname}.{fld}"] = getattr(c, fld).data[0, :, 0]
 
     for (name, case, nx, ny, p, nz, rk, dt, nsteps, rus, full) in CASES:
+        if only is not None and name not in only:
+            continue
+        if only is not None and full:
+            raise SystemExit(f"{name} stores full arrays: regenerate everything instead")
         t0 = time.time()
         setup, op = build(case, nx, ny, p, nz, rus)
         st = initial_state(setup, op, nz, name)
@@ -159,7 +174,8 @@ def main():
         print(name, entry["sha_ic"], entry["sha_rhs"], entry["sha_final"], entry["seconds"], "s",
               flush=True)
 
-    np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
+    if only is None:
+        np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)
 
