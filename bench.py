@@ -33,8 +33,11 @@ CONFIGS = {
     # name: (case, nx, ny, p, dt, label)
     "c3": ("williamson_tc6", 720, 360, 3, 5e-3, "C3: Williamson TC6, order 4 (p=3), 720x360, SSPRK3"),
     "c2": ("williamson_tc2", 360, 180, 3, 0.05, "C2: Williamson TC2, order 4 (p=3), 360x180, SSPRK3"),
-    "c4": ("williamson_tc6", 1440, 720, 4, 5e-4,
-           "C4 shape: order 5 (p=4), 1440x720, SSPRK3, TC6 IC (no orography in the reference)"),
+    "c4": ("williamson_tc5", 1440, 720, 4, 5e-4,
+           "C4: Williamson TC5 (flow over an isolated mountain; orography is an extension of the "
+           "reference), order 5 (p=4), 1440x720, SSPRK3"),
+    "c4tc6": ("williamson_tc6", 1440, 720, 4, 5e-4,
+              "C4 shape with the TC6 IC (no orography): order 5 (p=4), 1440x720, SSPRK3"),
 }
 # C5: order sweep 1..6 (p = 0..5) at ~1e9 DOF (SURVEY 8d grids, nx = 2 ny); one
 # GPU holds the three ~8 GB states; the initial condition is projected on
@@ -135,6 +138,64 @@ def cpu_oracle_rate(case, nx, ny, p, dt, budget_s=12.0, max_steps=None):
     return dofs * 3 * steps / el, steps, el, threads
 
 
+def host_cpu():
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count()}
+
+
+REF_PY = r"""
+import json, sys, time
+from dgswe import cases, dg, timestep
+case, nx, ny, p, dt, steps = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), float(sys.argv[5]), int(sys.argv[6])
+setup = cases.build_case(cases.default_config(case).override(nx=nx, ny=ny, p=p))
+op = dg.SpatialOperator(setup.mesh, p, setup.model)
+st = op.project_state(setup.ic)
+tab = timestep.tableau(3)
+ws = timestep._RKWorkspace(st, tab.s)
+timestep.rk_step(st, op.assemble_rhs, dt, tab, ws)          # warm-up (numba JIT)
+t0 = time.perf_counter()
+for _ in range(steps):
+    timestep.rk_step(st, op.assemble_rhs, dt, tab, ws)
+el = time.perf_counter() - t0
+print(json.dumps({"seconds": el, "steps": steps}))
+"""
+
+
+def reference_python_rate(case, nx, ny, p, dt, steps):
+    """The UNMODIFIED reference (pip-installed into baseline/_ref, pure
+    Python + numba, single-threaded by construction) on one pinned core:
+    rk_step(state, op.assemble_rhs, dt, tableau(3)) (timestep.py:149-167)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if case not in ("williamson_tc2", "williamson_tc6"):
+        return {"unavailable": f"{case} is not a case of the reference (no orography)"}
+    if not os.path.isdir(os.path.join(ref, "dgswe")):
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref)"}
+    env = dict(os.environ, PYTHONPATH=ref, NUMBA_CACHE_DIR="/tmp/dgswe_numba_cache",
+               OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
+               NUMBA_NUM_THREADS="1")
+    cmd = [sys.executable, "-c", REF_PY, case, str(nx), str(ny), str(p), repr(dt), str(steps)]
+    if os.path.exists("/usr/bin/taskset"):
+        cmd = ["taskset", "-c", "0"] + cmd
+    try:
+        res = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900)
+        out = json.loads(res.stdout.strip().splitlines()[-1])
+    except Exception as exc:                          # noqa: BLE001
+        return {"unavailable": f"reference run failed: {exc}"}
+    dofs = nx * ny * (p + 1) ** 2 * 3
+    return {"value": dofs * 3 * out["steps"] / out["seconds"], "unit": UNIT, "cores": 1,
+            "kind": "reference",
+            "sample": f"{out['steps']} rk_step(tableau(3)) steps of the same grid after 1 warm-up step, "
+                      "unmodified reference package (baseline/_ref), pinned to one core",
+            "host": host_cpu()}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -164,7 +225,10 @@ def run_reference(args):
                                    f"grid after {args.warmup} warm-up steps; oracle/dgswe_oracle.c "
                                    "(bit-exact C port of the reference RHS/RK, OpenMP)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "host": host_cpu(),
     }
+    if not args.no_ref_python:
+        line["reference_python"] = reference_python_rate(case, nx, ny, p, dt, args.ref_steps)
     print(json.dumps(line), flush=True)
 
 
@@ -342,6 +406,34 @@ def run_gpu(args):
         roofline["per_stage_gbs"] = {
             k: local_dofs * (16.0 if k == 1 else 24.0) / (v * 1e-3) / 1e9 for k, v in per_stage.items()}
 
+    # the reference's own entry point on a device state: rk_step(state,
+    # op.assemble_rhs, dt, tableau(3)) -- three single-launch modal stage
+    # kernels per step (in-kernel modal<->nodal conversion) and the per-step
+    # status read the reference's exceptions need (timestep.py:149-167)
+    api = None
+    if world == 1 and not args.no_api and not big:
+        tab = P.tableau(3)
+        st_api = P.State(state.data.clone(), nx, ny, 1, op.nphi)
+        ws = P.stepping._RKWorkspace(st_api, tab.s)
+        for _ in range(3):
+            P.rk_step(st_api, op.assemble_rhs, dt, tab, ws)
+        torch.cuda.synchronize()
+        k3 = max(3, min(args.steps, 50))
+        n_api = op.launch_count()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(k3):
+            P.rk_step(st_api, op.assemble_rhs, dt, tab, ws)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ms_api = a0.elapsed_time(a1) / k3
+        ach = dofs * B_ALG / (ms_api / 3 * 1e-3) / 1e9
+        api = {"path": "rk_step(state, op.assemble_rhs, dt, tableau(3)): 3 modal single-launch stage "
+                       "kernels + 1 status read per step", "value": dofs * 3 / (ms_api * 1e-3), "unit": UNIT,
+               "ms_per_step": ms_api, "steps": k3, "gpu_launches": op.launch_count() - n_api,
+               "achieved_gbs": ach, "frac": ach / measured_peaks().get("hbm_gbs", 6650.0)}
+        del st_api, ws
+
     # end to end through the public API with host buffers: every step copies
     # the state from pinned host memory, runs one fused SSPRK3 step and reads
     # the result back (the reference's rk_step contract on a host state)
@@ -395,7 +487,10 @@ def run_gpu(args):
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{n} full SSPRK3 steps of the same {args.config.upper()} grid "
                          f"({el:.1f} s) with the bit-exact C port of the reference path "
-                         "(oracle/dgswe_oracle.c, OpenMP)"}
+                         "(oracle/dgswe_oracle.c, OpenMP)",
+               "host": host_cpu()}
+        if not args.no_ref_python:
+            cpu["reference_python"] = reference_python_rate(case, nx, ny, p, dt, args.ref_steps)
 
     if rank == 0:
         line = {
@@ -410,7 +505,7 @@ def run_gpu(args):
                        "l2": f"no flush; per-stage working set {3 * dofs * 8 / 1e6:.0f} MB "
                              f"(3 states) > 126 MB L2" if args.config != "c2" else
                              "C2 states (25 MB each) fit in L2; roofline inflated"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "api_rk_step": api,
             "clocks": clk.summary(), "gpu_launches": int(launches),
             "dofs_per_gpu": local_dofs, "per_gpu_value": value / world,
         }
@@ -429,6 +524,10 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ref-python", action="store_true",
+                    help="skip timing the unmodified Python reference (baseline/_ref)")
+    ap.add_argument("--ref-steps", type=int, default=2, help="timed steps of the Python reference")
+    ap.add_argument("--no-api", action="store_true", help="skip the rk_step (reference API) timing")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -32,7 +32,7 @@
  *   dgswe_mass / dgswe_l2_sums     diagnostics.mass_integral / l2_error
  *                                  (diagnostics.py:92-107, 42-80)
  *   dgswe_project                  basis.project_initial (basis.py:206-233)
- *   dgswe_stage_edge + exchange    _halo_exchange (dg.py:330-346) across GPUs:
+ *   dgswe_stage_band + exchange    _halo_exchange (dg.py:330-346) across GPUs:
  *                                  latitude bands, peer-memory stores
  *
  * Layout of every state buffer (fp64), strip-blocked structure of arrays:
@@ -59,7 +59,7 @@
  * keeps its states nodal across many stages (a band driver) calls
  * dgswe_set_basis(ctx, 1) and dgswe_convert itself: then dgswe_rhs,
  * dgswe_stage*, dgswe_alpha_prepass and dgswe_rk_steps take and return
- * nodal states unchanged.  dgswe_stage_edge requires the nodal basis.
+ * nodal states unchanged.  dgswe_stage_band requires the nodal basis.
  * Diagnostics (dgswe_mass, dgswe_l2_sums) and dgswe_project always use
  * modal states.
  *
@@ -170,24 +170,26 @@ int dgswe_stage_rows(dgswe_ctx *ctx, double a, const double *U, double b, const 
                      double g, double *Y, int tag, int r0, int r1, void *stream);
 
 /* ---- fused halo exchange over peer memory (one process per GPU) ----
- * The band's two edge rows (jlo, jhi-1) are computed by dgswe_stage_edge,
- * which also stores them straight into the neighbours' halo rows (peer
- * pointers from CUDA IPC: dgswe_ipc_handle / dgswe_ipc_open) and counts
- * each delivered strip block in the neighbour's receive counter
- * (system-scope atomic after a system fence).  Before computing, an edge
- * row waits until its own receive counter shows the neighbour's edge rows
- * of the previous stage -- so interior rows (dgswe_stage_rows) need no halo
- * at all and run concurrently on another stream, and no host collective is
- * left on the path.  dgswe_set_exchange registers, once per context: the
- * neighbours' level strides and receive counters (NULL at a pole), and this
- * band's own counters: recv_count[2] (south, north deliveries) and
- * stage_ctr[2] (completed edge launches, CTA completion scratch), zeroed.
+ * dgswe_stage_band computes the band's rows [jlo, jhi) in ONE launch: its
+ * two edge rows (jlo, jhi-1) as the first, single-row CTAs, then the
+ * interior rows in chunks.  An edge CTA stores its output row both locally
+ * and straight into the neighbour's halo row (peer pointers from CUDA IPC:
+ * dgswe_ipc_handle / dgswe_ipc_open), then counts each delivered strip
+ * block in the neighbour's receive counter (system-scope atomic after a
+ * system fence).  Before computing, an edge CTA waits (bounded: see
+ * dgswe_set_peer_timeout) until its own receive counter shows the
+ * neighbour's edge rows of the previous stage; interior CTAs need no halo
+ * and run at once -- no host collective, no second stream.
+ * dgswe_set_exchange registers, once per context: the neighbours' level
+ * strides and receive counters (NULL at a pole), and this band's own
+ * counters: recv_count[2] (south, north deliveries) and stage_ctr[2]
+ * (completed band launches, CTA completion scratch), zeroed.
  * peer_row_s / peer_row_n: level-0 base of the neighbour's halo row in the
- * buffer that plays Y's role there (NULL at a pole). */
+ * buffer that plays Y's role there (NULL at a pole).  Nodal states only. */
 int dgswe_set_exchange(dgswe_ctx *ctx, long long peer_zstride_s, unsigned long long *peer_count_s,
                        long long peer_zstride_n, unsigned long long *peer_count_n,
                        unsigned long long *recv_count, unsigned long long *stage_ctr);
-int dgswe_stage_edge(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g, double *Y,
+int dgswe_stage_band(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g, double *Y,
                      int tag, double *peer_row_s, double *peer_row_n, void *stream);
 /* device memory the neighbours can map (zero-filled), and its IPC handles */
 int dgswe_dev_alloc(size_t bytes, void **out);
@@ -254,7 +256,7 @@ int dgswe_status(dgswe_ctx *ctx, uint32_t *flags, int32_t *first_tag, int reset,
  * (POSITIVITY, NONFINITE, MEAN_NONPOS, PEER_TIMEOUT) in tags[b]. */
 int dgswe_status_tags(dgswe_ctx *ctx, uint32_t *flags, int32_t *tags, int reset, void *stream);
 
-/* Bound (ns, default 2 s) on an edge launch's wait for a neighbour's halo
+/* Bound (ns, default 2 s) on a band launch's wait for a neighbour's halo
  * rows; on expiry the launch raises DGSWE_STATUS_PEER_TIMEOUT instead of
  * hanging the GPU (the stage's result is then invalid). */
 int dgswe_set_peer_timeout(dgswe_ctx *ctx, unsigned long long timeout_ns);

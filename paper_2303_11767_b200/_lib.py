@@ -60,7 +60,7 @@ SIGNATURES = {
     "dgswe_stage_rows2": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _I, _I, _I, _I, _VP]),
     "dgswe_stage_rows_checked": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _I, _I, _I, _I, _VP]),
     "dgswe_set_exchange": (_I, [_VP, ctypes.c_longlong, _VP, ctypes.c_longlong, _VP, _VP, _VP]),
-    "dgswe_stage_edge": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _VP, _VP, _VP]),
+    "dgswe_stage_band": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _I, _VP, _VP, _VP]),
     "dgswe_dev_alloc": (_I, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "dgswe_dev_free": (_I, [_VP]),
     "dgswe_ipc_handle": (_I, [_VP, ctypes.c_char_p]),

@@ -17,13 +17,13 @@ is the southern halo (global row j0-1), rows 1..owned are owned, the last
 row is the northern halo.  Halo rows at a pole are never read.
 
 Transports:
-* ``"fused"`` -- no host collective on the path: each stage's two edge rows
-  are computed by one small launch (``dgswe_stage_edge``) that also stores
-  them straight into the neighbours' halo rows over peer memory (CUDA IPC
-  mappings: NVLink/NVSwitch on a B200 node) and bumps the neighbours'
-  receive counters; an edge row first waits for its own counter to show the
-  neighbour's previous-stage rows.  The interior rows need no halo and run
-  concurrently on a second stream.  Buffers must come from
+* ``"fused"`` -- no host collective on the path: one launch per stage
+  (``dgswe_stage_band``) whose first CTAs compute the two edge rows and
+  store them straight into the neighbours' halo rows over peer memory (CUDA
+  IPC mappings: NVLink/NVSwitch on a B200 node), bumping the neighbours'
+  receive counters; an edge row first waits (bounded) for its own counter
+  to show the neighbour's previous-stage rows.  The interior CTAs of the
+  same launch need no halo and run at once.  Buffers must come from
   :meth:`BandOperator.empty` (IPC-mappable) and be registered with
   :meth:`BandOperator.attach`;
 * ``"p2p"`` -- torch.distributed batched isend/irecv on the device tensors
@@ -205,7 +205,6 @@ class BandOperator:
         self._owned_mem = []       # (ptr, keep-alive) of library allocations
         self._opened = []          # peer mappings to close
         self._peer_rows = {}       # data_ptr of our buffer -> (south row ptr, north row ptr)
-        self._aux = None
 
     def empty(self, device=None):
         if self.transport != "fused":
@@ -278,7 +277,6 @@ class BandOperator:
         _lib.check(lib.dgswe_set_exchange(self.ctx.h, zs[0], ctypes.c_void_p(cnt[0] or 0), zs[1],
                                           ctypes.c_void_p(cnt[1] or 0), ctypes.c_void_p(ctrl),
                                           ctypes.c_void_p(ctrl + 16)), "dgswe_set_exchange")
-        self._aux = torch.cuda.Stream()
         torch.cuda.synchronize()
         dist.barrier(group=self.group)          # every rank mapped before any delivery
 
@@ -321,21 +319,17 @@ class BandOperator:
             int(r0), int(r1), int(r2), int(r3), c.stream()), "dgswe_stage_rows2")
 
     def _stage_fused(self, a, U, b, X, g, Y, tag):
-        L, c = self.layout, self.ctx
+        """The whole band in one launch (dgswe_stage_band): edge rows first,
+        stored into the neighbours' halos over peer memory; interior rows
+        need no halo and run at once."""
+        c = self.ctx
         rows = self._peer_rows.get(Y.data_ptr())
         if rows is None:
             raise ValueError("fused transport: Y was not registered with attach()")
-        cur = torch.cuda.current_stream()
-        self._aux.wait_stream(cur)
-        with torch.cuda.stream(self._aux):
-            _lib.check(c.lib.dgswe_stage_edge(
-                c.h, float(a), ctypes.c_void_p(U.data_ptr() if U is not None else 0), float(b),
-                ctypes.c_void_p(X.data_ptr()), float(g), ctypes.c_void_p(Y.data_ptr()), int(tag),
-                ctypes.c_void_p(rows[0] or 0), ctypes.c_void_p(rows[1] or 0),
-                ctypes.c_void_p(self._aux.cuda_stream)), "dgswe_stage_edge")
-        if L.owned > 2:
-            self._launch(a, U, b, X, g, Y, tag, L.jlo + 1, L.jhi - 1)    # no halo needed
-        cur.wait_stream(self._aux)
+        _lib.check(c.lib.dgswe_stage_band(
+            c.h, float(a), ctypes.c_void_p(U.data_ptr() if U is not None else 0), float(b),
+            ctypes.c_void_p(X.data_ptr()), float(g), ctypes.c_void_p(Y.data_ptr()), int(tag),
+            ctypes.c_void_p(rows[0] or 0), ctypes.c_void_p(rows[1] or 0), c.stream()), "dgswe_stage_band")
 
     def stage(self, a, U, b, X, g, Y, tag=0):
         """Halo exchange of X, then Y = a U + b X + g RHS(X) on owned rows."""

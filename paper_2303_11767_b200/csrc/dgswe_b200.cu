@@ -466,20 +466,15 @@ int dgswe_set_peer_timeout(dgswe_ctx *ctx, unsigned long long timeout_ns)
     return DGSWE_OK;
 }
 
-int dgswe_stage_edge(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g, double *Y,
+int dgswe_stage_band(dgswe_ctx *ctx, double a, const double *U, double b, const double *X, double g, double *Y,
                      int tag, double *peer_row_s, double *peer_row_n, void *stream)
 {
     if (!ctx) return dgswe_fail(DGSWE_EINVAL, "null context");
     if (!ctx->stage_ctr) return dgswe_fail(DGSWE_EINVAL, "dgswe_set_exchange first");
-    if (!ctx->basis) return dgswe_fail(DGSWE_EINVAL, "edge launches take nodal states (dgswe_set_basis)");
-    const int lo = ctx->cfg.jlo, hi = ctx->cfg.jhi;
+    if (!ctx->basis) return dgswe_fail(DGSWE_EINVAL, "band launches take nodal states (dgswe_set_basis)");
     ctx->edge_row[0] = peer_row_s;
     ctx->edge_row[1] = peer_row_n;
-    StageCall sc = stage_call(a, U, b, X, g, Y, tag, lo, hi - lo >= 2 ? lo + 1 : hi);
-    if (hi - lo >= 2) {
-        sc.r2 = hi - 1;
-        sc.r3 = hi;
-    }
+    StageCall sc = stage_call(a, U, b, X, g, Y, tag, ctx->cfg.jlo, ctx->cfg.jhi);
     sc.edge = true;
     return launch_stage(ctx, sc, (cudaStream_t)stream);
 }

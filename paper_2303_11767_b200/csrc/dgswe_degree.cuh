@@ -109,16 +109,28 @@ int launch_variant(dgswe_ctx *c, const StageParams &kp0, cudaStream_t s)
     const int o = occupancy<P, F>(c);
     if (o < 0) return o;
     StageParams kp = kp0;
-    const int rows1 = kp.j_end - kp.j_begin, rows2 = kp.j_end2 - kp.j_begin2;
-    const int rows = rows1 > rows2 ? rows1 : rows2;
-    if (rows <= 0) return DGSWE_OK;
-    int rc = (F & dgswe::kEdge) ? 1 : kp.rc;
-    if (rc <= 0) rc = chunk_rows<P>(c, rows, o);
-    kp.rc = rc;
-    int nchunks = (rows1 + rc - 1) / rc;
-    if (rows2 > 0) {   // a second row range in the same launch
-        kp.nchunk1 = nchunks;
-        nchunks += (rows2 + rc - 1) / rc;
+    int nchunks;
+    if (F & dgswe::kEdge) {
+        // the whole band: its two edge rows as single-row CTAs, then the
+        // interior rows [band_lo+1, band_hi-1) in chunks
+        const int nedge = kp.band_hi - kp.band_lo < 2 ? kp.band_hi - kp.band_lo : 2;
+        const int inner = kp.band_hi - kp.band_lo - 2 > 0 ? kp.band_hi - kp.band_lo - 2 : 0;
+        int rc = kp.rc;
+        if (rc <= 0) rc = inner > 0 ? chunk_rows<P>(c, inner, o) : 1;
+        kp.rc = rc;
+        nchunks = nedge + (inner + rc - 1) / rc;
+    } else {
+        const int rows1 = kp.j_end - kp.j_begin, rows2 = kp.j_end2 - kp.j_begin2;
+        const int rows = rows1 > rows2 ? rows1 : rows2;
+        if (rows <= 0) return DGSWE_OK;
+        int rc = kp.rc;
+        if (rc <= 0) rc = chunk_rows<P>(c, rows, o);
+        kp.rc = rc;
+        nchunks = (rows1 + rc - 1) / rc;
+        if (rows2 > 0) {   // a second row range in the same launch
+            kp.nchunk1 = nchunks;
+            nchunks += (rows2 + rc - 1) / rc;
+        }
     }
     const dim3 grid(c->nstrip, nchunks, c->cfg.nz);
     dgswe::stage_kernel<P, F><<<grid, dgswe::kThreads, stage_smem<P, F>(c), s>>>(kp);

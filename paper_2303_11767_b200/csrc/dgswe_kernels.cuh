@@ -910,10 +910,25 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
     const int strip = blockIdx.x;
     const int nvalid = min(kLanes, nx - strip * kLanes);
     const bool owned = lane < nvalid;
-    const bool second = (int)blockIdx.y >= kp.nchunk1;   // one launch can cover two row ranges
-    const int jb = second ? kp.j_begin2 + ((int)blockIdx.y - kp.nchunk1) * kp.rc : kp.j_begin + blockIdx.y * kp.rc;
-    const int je = min(jb + kp.rc, second ? kp.j_end2 : kp.j_end);
-    if (jb >= je) return;
+    int jb, je;
+    if constexpr (EDGE) {
+        // a whole band in one launch: blockIdx.y 0 / 1 = its southern / northern
+        // edge row (one row each, scheduled first), then chunks of rc interior rows
+        const int nedge = min(2, kp.band_hi - kp.band_lo);
+        const int y = blockIdx.y;
+        if (y < nedge) {
+            jb = y == 0 ? kp.band_lo : kp.band_hi - 1;
+            je = jb + 1;
+        } else {
+            jb = kp.band_lo + 1 + (y - nedge) * kp.rc;
+            je = min(jb + kp.rc, kp.band_hi - 1);
+        }
+    } else {
+        const bool second = (int)blockIdx.y >= kp.nchunk1;   // one launch can cover two row ranges
+        jb = second ? kp.j_begin2 + ((int)blockIdx.y - kp.nchunk1) * kp.rc : kp.j_begin + blockIdx.y * kp.rc;
+        je = min(jb + kp.rc, second ? kp.j_end2 : kp.j_end);
+        if (jb >= je) return;
+    }
     unsigned bad = 0;
     // fused halo exchange: an edge row first waits until the neighbour has
     // delivered this stage's halo row (its previous stage's edge row):
@@ -924,7 +939,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
         if (threadIdx.x == 0) {
             const unsigned long long need =
                 ld_acquire_sys(kp.stage_ctr) * (unsigned long long)kp.nstrip * gridDim.z;
-            const int g = kp.row0 + jb;
+            const int g = kp.row0 + jb;   // only the edge rows' CTAs wait
             bool ok = true;
             if (jb == kp.band_lo && g > 0) ok &= wait_counter(kp.recv_count, need, kp.peer_timeout_ns);
             if (jb == kp.band_hi - 1 && g + 1 < kp.ny)

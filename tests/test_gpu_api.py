@@ -204,7 +204,7 @@ def test_misaligned_state_rejected(P):
 
 
 def test_peer_wait_times_out(P):
-    """An edge launch whose neighbour never delivers: bounded wait, the
+    """A band launch whose neighbour never delivers: bounded wait, the
     PEER_TIMEOUT status bit, no hung GPU (the band is row0 > 0, so it waits
     for its southern halo; the receive counter never moves)."""
     from paper_2303_11767_b200.bands import BandLayout, BandOperator
@@ -222,9 +222,9 @@ def test_peer_wait_times_out(P):
     u[:, :, 0] = 1000.0                                    # positive h
     c.set_basis(True)
     try:
-        P._lib.check(c.lib.dgswe_stage_edge(c.h, 0.0, None, 1.0, ctypes.c_void_p(u.data_ptr()), 1.0,
+        P._lib.check(c.lib.dgswe_stage_band(c.h, 0.0, None, 1.0, ctypes.c_void_p(u.data_ptr()), 1.0,
                                             ctypes.c_void_p(y.data_ptr()), 0, None, None, c.stream()),
-                     "stage_edge")
+                     "stage_band")
         flags, tags = c.status_tags()
     finally:
         c.set_basis(False)
