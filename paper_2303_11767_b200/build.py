@@ -44,8 +44,8 @@ def _stale() -> bool:
         os.path.getmtime(header) > t
 
 
-def _compile(src: str, extra: list, verbose: bool) -> str:
-    obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
+def _compile(src: str, extra: list, verbose: bool, objdir: str = OBJ) -> str:
+    obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
     cmd = [nvcc(), *NVCC_FLAGS, *extra, *(["-Xptxas", "-v"] if verbose else []), "-c", "-o", obj,
            os.path.join(SRC, src)]
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -61,9 +61,10 @@ def build(force: bool = False, verbose: bool = False, out: str = OUT, extra: lis
     flags serve experiment builds (e.g. ``-DDG_TIMING``)."""
     if not force and out == OUT and not extra and not _stale():
         return out
-    os.makedirs(OBJ, exist_ok=True)
+    objdir = OBJ if out == OUT else out + ".objs"
+    os.makedirs(objdir, exist_ok=True)
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, extra or [], verbose), SOURCES))
+        objs = list(ex.map(lambda s: _compile(s, extra or [], verbose, objdir), SOURCES))
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", out + ".tmp", *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

@@ -81,6 +81,7 @@ struct dgswe_ctx {
     int device = 0;
     int sms = 148;
     int smem_pad = 0;             // experiment knob: extra dynamic smem per CTA
+    int even_chunks = 0;          // experiment knob (DGSWE_CHUNKS): fixed chunk count, even split
     int occ[32] = {};             // resident CTAs per SM of each stage-kernel variant (0: not queried)
     // fused halo exchange (bands.py transport "fused"): set by dgswe_set_exchange
     long long peer_zstride[2] = {0, 0};

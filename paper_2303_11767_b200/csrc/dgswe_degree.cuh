@@ -54,8 +54,13 @@ int occupancy(dgswe_ctx *c)
 // work, measured ~1.4 rows) favours long chunks.  Narrow grids get one full
 // wave; wide grids, whose strips alone outnumber the slots, get several
 // waves of short chunks instead of one under-filled wave of very long ones.
+struct ChunkPlan {
+    int rc;     // rows per chunk (uniform chunks), or
+    int even;   // > 0: this many chunks of floor/ceil(rows / even) rows
+};
+
 template <int P>
-int chunk_rows(const dgswe_ctx *c, int rows, int o)
+ChunkPlan chunk_plan(const dgswe_ctx *c, int rows, int o)
 {
     constexpr double kChunkOverhead = 1.5;
     const long long slots = (long long)c->sms * o;
@@ -73,34 +78,36 @@ int chunk_rows(const dgswe_ctx *c, int rows, int o)
             best_chunks = ch;
         }
     }
-    // Second look, by the busiest SM's row work: CTAs share their SM's issue
-    // and FP64 throughput, so a one-wave grid that puts o CTAs on some SMs
-    // and o-1 on the others runs at the pace of the former.  Chunks long
-    // enough for at most o-1 CTAs per SM win when that load is clearly lower
-    // (C3: 23 strips x 19 chunks of 19 rows, 3 per SM, instead of 24 chunks
-    // of 15, 4 on 108 SMs: +1.4%; C2 +2%).  Measured for p = 3 only: at
-    // p = 2 the lighter CTAs want the 4th CTA's latency hiding (-3%), at
-    // p >= 4 o - 1 = 1 CTA per SM.
-    if (P == 3 && o > 1) {
-        auto sm_load = [&](long long ch) {
-            const long long per = (rows + ch - 1) / ch;
+    ChunkPlan plan{(int)((rows + best_chunks - 1) / best_chunks), 0};
+    // Second look (p = 3), by the busiest SM's row work: CTAs share their
+    // SM's issue and FP64 throughput, so a one-wave grid runs at the pace of
+    // its most loaded SMs.  Candidates: uniform chunks long enough for at
+    // most o-1 CTAs per SM, and the largest one-wave grid of evenly split
+    // chunks (o CTAs on most SMs; a fully occupied SM hides latency better:
+    // ~5% more row work per unit time, measured at 4 vs 3 CTAs).  C3: 23
+    // strips x 25 even chunks of 14-15 rows (575 CTAs, 4 on 131 SMs) beats
+    // 19 x 19 rows at 3 per SM (+1.7%), which beat 24 x 15 at 4 on 108 SMs
+    // (+1.4%).  At p = 2 the lighter CTAs want every slot (-3% with o-1),
+    // at p >= 4 o - 1 = 1 CTA per SM.
+    if (P == 3 && o > 1 && cols * best_chunks <= slots) {
+        auto sm_load = [&](long long ch, bool even) {
+            const double per = even ? (double)rows / (double)ch : (double)((rows + ch - 1) / ch);
             const long long per_sm = (cols * ch + c->sms - 1) / c->sms;
-            return (double)per_sm * ((double)per + 1.0);
+            return (double)per_sm * (per + 1.0) / (per_sm >= o ? 1.05 : 1.0);
         };
-        const double cur = sm_load(best_chunks);
-        long long alt = 0;
-        double alt_cost = 1e300;
+        double cost = sm_load(best_chunks, false);
         for (long long ch = 1; ch <= rows && cols * ch <= (long long)c->sms * (o - 1); ++ch) {
             if ((cols * ch + c->sms - 1) / c->sms != o - 1) continue;   // exactly o-1 on the busiest SM
-            const double t = sm_load(ch);
-            if (t < alt_cost - 1e-9) {
-                alt_cost = t;
-                alt = ch;
+            const double t = sm_load(ch, false);
+            if (t < 0.95 * cost) {
+                cost = t;
+                plan = ChunkPlan{(int)((rows + ch - 1) / ch), 0};
             }
         }
-        if (alt > 0 && alt_cost < 0.95 * cur) best_chunks = alt;
+        const long long ch = slots / cols < rows ? slots / cols : rows;
+        if (ch >= 1 && (double)rows / (double)ch >= 4.0 && sm_load(ch, true) < cost) plan = ChunkPlan{0, (int)ch};
     }
-    return (int)((rows + best_chunks - 1) / best_chunks);
+    return plan;
 }
 
 template <int P, int F>
@@ -115,18 +122,30 @@ int launch_variant(dgswe_ctx *c, const StageParams &kp0, cudaStream_t s)
         // interior rows [band_lo+1, band_hi-1) in chunks
         const int nedge = kp.band_hi - kp.band_lo < 2 ? kp.band_hi - kp.band_lo : 2;
         const int inner = kp.band_hi - kp.band_lo - 2 > 0 ? kp.band_hi - kp.band_lo - 2 : 0;
-        int rc = kp.rc;
-        if (rc <= 0) rc = inner > 0 ? chunk_rows<P>(c, inner, o) : 1;
-        kp.rc = rc;
-        nchunks = nedge + (inner + rc - 1) / rc;
+        ChunkPlan plan{kp.rc > 0 ? kp.rc : 1, 0};
+        if (kp.rc <= 0 && inner > 0) plan = c->even_chunks > 0 ? ChunkPlan{0, c->even_chunks} : chunk_plan<P>(c, inner, o);
+        if (plan.even > 0) {
+            kp.even = plan.even < inner ? plan.even : inner;
+            nchunks = nedge + kp.even;
+        } else {
+            kp.rc = plan.rc;
+            nchunks = nedge + (inner + plan.rc - 1) / plan.rc;
+        }
     } else {
         const int rows1 = kp.j_end - kp.j_begin, rows2 = kp.j_end2 - kp.j_begin2;
         const int rows = rows1 > rows2 ? rows1 : rows2;
         if (rows <= 0) return DGSWE_OK;
-        int rc = kp.rc;
-        if (rc <= 0) rc = chunk_rows<P>(c, rows, o);
-        kp.rc = rc;
-        nchunks = (rows1 + rc - 1) / rc;
+        ChunkPlan plan{kp.rc, 0};
+        if (kp.rc <= 0) plan = c->even_chunks > 0 ? ChunkPlan{0, c->even_chunks} : chunk_plan<P>(c, rows, o);
+        if (plan.even > 0 && rows2 > 0) plan = ChunkPlan{(rows + plan.even - 1) / plan.even, 0};
+        const int rc = plan.rc;
+        if (plan.even > 0) {
+            kp.even = plan.even < rows1 ? plan.even : rows1;
+            nchunks = kp.even;
+        } else {
+            kp.rc = rc;
+            nchunks = (rows1 + rc - 1) / rc;
+        }
         if (rows2 > 0) {   // a second row range in the same launch
             kp.nchunk1 = nchunks;
             nchunks += (rows2 + rc - 1) / rc;

@@ -67,6 +67,10 @@ __host__ __device__ constexpr int min_blocks() { return P <= 3 ? 4 : 2; }
 template <int P>
 __host__ __device__ constexpr bool vol_rolled() { return P >= 2; }
 
+#ifndef DG_CELER_SEL
+#define DG_CELER_SEL 0
+#endif
+
 // DG_TIMING builds record per-role phase durations (clock cycles) of every
 // row: [role][A work, barrier-1 wait, B work, barrier-2 wait, C work, rows]
 #ifdef DG_TIMING
@@ -162,23 +166,27 @@ struct Smem {
     static constexpr int N = P + 1;
     static constexpr int NP = N * N;
     static constexpr int TILE = 3 * NP * kLanes;         // one row of coefficients, all vars
-    static constexpr int TR = 3 * N * kLanes;            // one trace / face-flux set
+    static constexpr int LD = kLanes + 1;                // leading dimension of trace / flux arrays:
+                                                         // columns 0..31 = lanes, column 32 = a strip-
+                                                         // border value (halo traces, border face flux)
+    static constexpr int TR = 3 * N * LD;                // one trace / face-flux set [3][N][LD]
     // offsets in doubles
     static constexpr int XR0 = 0;                        // coefficient ring slot 0 [var][mode][lane]
     static constexpr int XR1 = XR0 + TILE;               // slot 1
     static constexpr int E = XR1 + TILE;                 // row-local volume terms [3][NP][32] (rolled volume)
-    static constexpr int XL = E + (vol_rolled<P>() ? TILE : 0);   // L traces [3][N][32]
-    static constexpr int XRT = XL + TR;
+    static constexpr int XL = E + (vol_rolled<P>() ? TILE : 0);   // L traces [3][N][LD]
+    static constexpr int XRT = XL + TR;                  // R traces
     static constexpr int TT = XRT + TR;                  // top traces of current row
-    static constexpr int FX = TT + TR;                   // x-face fluxes [3][N][32], column c = right face of lane c
-                                                         // (face 0 lives in F0, double-buffered)
-    static constexpr int FY0 = FX + TR;                  // y-face flux buffers [3][N][32]
+    static constexpr int FX = TT + TR;                   // x-face fluxes, column c = right face of lane c
+    static constexpr int FY0 = FX + TR;                  // y-face flux buffers
     static constexpr int FY1 = FY0 + TR;
-    static constexpr int HL = FY1 + TR;                  // left-halo R trace [3][N]
-    static constexpr int HR = HL + 3 * N;                // right-halo L trace [3][N]
-    static constexpr int E0 = HR + 3 * N;                // element 0's L trace [3][N] (face warp)
-    static constexpr int F0 = E0 + 3 * N;                // face 0 flux [row parity][3][N]
-    static constexpr int HB = F0 + 6 * N;                // next row's neighbour coefficients [2][3][NP]
+    // column 32 of those arrays (face warp): halo / border values
+    static constexpr int HR = XL + kLanes;               // right neighbour's L trace (x-face of the last lane)
+    static constexpr int HL = XRT + kLanes;              // left neighbour's R trace (border face "in")
+    static constexpr int E0 = TT + kLanes;               // element 0's L trace (border face "out")
+    static constexpr int F0A = FX + kLanes;              // border face 0 flux, even rows
+    static constexpr int F0B = FY0 + kLanes;             // odd rows
+    static constexpr int HB = FY1 + TR;                  // next row's neighbour coefficients [2][3][NP]
     static constexpr int ROW = HB + 6 * NP;              // row-table ring, 3 rows
     static constexpr int MBAR = ROW + 3 * RowLayout<P>::SSTRIDE;  // 6 mbarriers [slot][var]
     static constexpr int TOTAL = MBAR + 6;
@@ -203,7 +211,6 @@ __device__ __forceinline__ bool ge_pos(double x, double y)
 {
     return __double_as_longlong(x) >= __double_as_longlong(y);
 }
-__device__ __forceinline__ bool gt_zero(double x) { return __double_as_longlong(x) > 0; }
 
 // max of two non-negative values (same integer trick)
 __device__ __forceinline__ double max_nn(double x, double y) { return max_pos(x, y); }
@@ -230,14 +237,20 @@ __device__ __forceinline__ double rsqrt64(double x)
 
 // 1/hf with hf = max(h, floor) (models.py:161-166) and the celerity
 // sqrt(g max(h, 0)) (models.py:254-258) from ONE rsqrt of h: below the floor
-// 1/hf is the constant 1/floor, and h <= 0 (flagged by the positivity
-// check) gives c = 0 like the reference.
+// 1/hf is the constant 1/floor.  h <= 0 or NaN at any trace node sets the
+// positivity status bit, which discards the whole step (PositivityError,
+// dg.py:359-372), so c there only has to stay finite (it is <= 0 instead of
+// the reference's 0; the rsqrt argument is clamped to DBL_MIN).
 __device__ __forceinline__ void inv_and_celerity(double h, double h_floor, double inv_floor, double sqrt_g,
                                                  double &r, double &c)
 {
     const double y = rsqrt64(max_pos(h, 2.2250738585072014e-308));
     r = ge_pos(h, h_floor) ? y * y : inv_floor;   // branches compared on the integer pipe
-    c = gt_zero(h) ? sqrt_g * (h * y) : 0.0;
+#if DG_CELER_SEL
+    c = __double_as_longlong(h) > 0 ? sqrt_g * (h * y) : 0.0;
+#else
+    c = sqrt_g * (h * y);
+#endif
 }
 
 // --- TMA bulk copies and mbarriers (one elected lane per variable warp) ---
@@ -345,9 +358,9 @@ __device__ __forceinline__ unsigned traces_row(const double (&u)[P + 1][P + 1], 
     ytrace<P, false>(u, t);
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-        sXL[q * kLanes + lane] = l[q];
-        sXR[q * kLanes + lane] = r[q];
-        sT[q * kLanes + lane] = t[q];
+        sXL[q * Smem<P>::LD + lane] = l[q];
+        sXR[q * Smem<P>::LD + lane] = r[q];
+        sT[q * Smem<P>::LD + lane] = t[q];
     }
     if (check) {
 #pragma unroll
@@ -386,10 +399,10 @@ struct FaceArgs {
 // instructions of a kernel whose speed tracks its instruction-cache
 // footprint; sF may alias the "out" traces.)
 template <int P>
-__device__ __forceinline__ void face_flux_body(int in_off, int in_ld, int in_col, int out_off, int out_ld,
-                                               int out_col, int dst_off, int dst_ld, int dst_col, FaceArgs fa)
+__device__ __forceinline__ void face_flux_body(int in, int out, int dst, FaceArgs fa)
 {
     constexpr int N = P + 1;
+    constexpr int LD = Smem<P>::LD;
     extern __shared__ double smem[];
     // variables by role: h, the normal momentum (hu across an x-face, hv
     // across a y-face) and the tangential one, addressed through the
@@ -398,12 +411,12 @@ __device__ __forceinline__ void face_flux_body(int in_off, int in_ld, int in_col
     double hI[N], nI[N], tI[N], hO[N], nO[N], tO[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-        hI[k] = smem[in_off + k * in_ld + in_col];
-        nI[k] = smem[in_off + (vn * N + k) * in_ld + in_col];
-        tI[k] = smem[in_off + (vt * N + k) * in_ld + in_col];
-        hO[k] = smem[out_off + k * out_ld + out_col];
-        nO[k] = smem[out_off + (vn * N + k) * out_ld + out_col];
-        tO[k] = smem[out_off + (vt * N + k) * out_ld + out_col];
+        hI[k] = smem[in + k * LD];
+        nI[k] = smem[in + (vn * N + k) * LD];
+        tI[k] = smem[in + (vt * N + k) * LD];
+        hO[k] = smem[out + k * LD];
+        nO[k] = smem[out + (vn * N + k) * LD];
+        tO[k] = smem[out + (vt * N + k) * LD];
     }
     double rin[N], rout[N];
     double am[N];
@@ -429,29 +442,27 @@ __device__ __forceinline__ void face_flux_body(int in_off, int in_ld, int in_col
         const double wi = nI[k] * rin[k], wo = nO[k] * rout[k];
         const double fni = fma(nI[k], wi, gi), fno = fma(nO[k], wo, go);   // normal: m w + g h^2/2
         const double fti = tI[k] * wi, fto = tO[k] * wo;                   // tangential: m_t w
-        smem[dst_off + k * dst_ld + dst_col] = fma(hs, nI[k] + nO[k], -ha * (hO[k] - hI[k]));
-        smem[dst_off + (vn * N + k) * dst_ld + dst_col] = fma(hs, fni + fno, -ha * (nO[k] - nI[k]));
-        smem[dst_off + (vt * N + k) * dst_ld + dst_col] = fma(hs, fti + fto, -ha * (tO[k] - tI[k]));
+        smem[dst + k * LD] = fma(hs, nI[k] + nO[k], -ha * (hO[k] - hI[k]));
+        smem[dst + (vn * N + k) * LD] = fma(hs, fni + fno, -ha * (nO[k] - nI[k]));
+        smem[dst + (vt * N + k) * LD] = fma(hs, fti + fto, -ha * (tO[k] - tI[k]));
     }
 }
 
 template <int P>
-__device__ __noinline__ void face_flux_noinline(int in_off, int in_ld, int in_col, int out_off, int out_ld,
-                                                int out_col, int dst_off, int dst_ld, int dst_col, FaceArgs fa)
+__device__ __noinline__ void face_flux_noinline(int in, int out, int dst, FaceArgs fa)
 {
-    face_flux_body<P>(in_off, in_ld, in_col, out_off, out_ld, out_col, dst_off, dst_ld, dst_col, fa);
+    face_flux_body<P>(in, out, dst, fa);
 }
 
 // p >= 2: the shared non-inlined copy; p <= 1: inlined (the face work is a
 // large share of a low-order element and the call's overhead shows, measured)
 template <int P>
-__device__ __forceinline__ void face_flux_call(int in_off, int in_ld, int in_col, int out_off, int out_ld,
-                                               int out_col, int dst_off, int dst_ld, int dst_col, FaceArgs fa)
+__device__ __forceinline__ void face_flux_call(int in, int out, int dst, FaceArgs fa)
 {
     if constexpr (P <= 1)
-        face_flux_body<P>(in_off, in_ld, in_col, out_off, out_ld, out_col, dst_off, dst_ld, dst_col, fa);
+        face_flux_body<P>(in, out, dst, fa);
     else
-        face_flux_noinline<P>(in_off, in_ld, in_col, out_off, out_ld, out_col, dst_off, dst_ld, dst_col, fa);
+        face_flux_noinline<P>(in, out, dst, fa);
 }
 
 
@@ -624,28 +635,22 @@ __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v
 // Boundary lifts, diagonal mass, stage combination and store for variable v.
 // Face values are scale * f* at the face's nodes (bd_det folded in by the
 // face warps); x lifts run along xi with mu, y lifts along eta.
-// Uv / Yv point at this lane's element of the variable's strip block
+// `un` holds u^n (HAS_U); Yv points at this lane's element of the variable's strip block
 // (node stride 32 doubles: immediate offsets).  MODAL: U, A, Y, Y2 hold
 // modal coefficients; the nodal parts b X + g K and g2 K are converted to
 // modes in registers before the u^n / accumulator terms are added.
 template <int P, bool HAS_U, bool HAS_Y2, bool MODAL>
 __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const double *cur,
-                                             const double *Uv, const double *Av, double *Y2v, int v,
+                                             const double *Av, double *Y2v, int v,
                                              const double *sFX, const double *sF0,
                                              const double *sFtop, const double *sFbot,
                                              const double *row, int lane, bool owned,
-                                             double *Yv, const StageParams &kp, double *Ypeer = nullptr,
-                                             double *Ypeer2 = nullptr)
+                                             double *Yv, const StageParams &kp, double *Ypeer,
+                                             double *Ypeer2, const double (&un_in)[P + 1][P + 1])
 {
     constexpr int N = P + 1;
     using RL = RowLayout<P>;
-    double un[N][N];
-    if (HAS_U) {                       // u^n: plain loads (U may alias Y)
-#pragma unroll
-        for (int a = 0; a < N; ++a)
-#pragma unroll
-            for (int b = 0; b < N; ++b) un[a][b] = Uv[(a * N + b) * kLanes];
-    }
+    const double (&un)[N][N] = un_in;  // u^n, loaded by the caller before barrier 2 (U may alias Y)
     double an[HAS_Y2 ? N : 1][HAS_Y2 ? N : 1];
     if constexpr (HAS_Y2) {            // second output's addend (may alias Y2)
 #pragma unroll
@@ -660,13 +665,14 @@ __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const 
 #pragma unroll
             for (int j = 0; j < N; ++j) acc[i][j] += sE[(i * N + j) * kLanes + lane];
     }
-    const int o = (v * N) * kLanes;    // x-face column c: right face of lane c (lane 0's left face: F0)
+    constexpr int LD = Smem<P>::LD;
+    const int o = (v * N) * LD;        // x-face column c: right face of lane c (lane 0's left face: F0)
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-        const double l = lane == 0 ? sF0[v * N + q] : sFX[o + q * kLanes + ((lane + kLanes - 1) & (kLanes - 1))];
-        const double r = sFX[o + q * kLanes + lane];
-        const double t = sFtop[o + q * kLanes + lane];     // zero at a pole (the face warp)
-        const double bo = sFbot[o + q * kLanes + lane];
+        const double l = lane == 0 ? sF0[o + q * LD] : sFX[o + q * LD + lane - 1];
+        const double r = sFX[o + q * LD + lane];
+        const double t = sFtop[o + q * LD + lane];     // zero at a pole (the face warp)
+        const double bo = sFbot[o + q * LD + lane];
 #pragma unroll
         for (int k = 0; k < N; ++k) {
             // x faces at eta node q lift along xi (column q); y faces at xi node q along eta (row q)
@@ -812,7 +818,7 @@ __device__ __forceinline__ void border_traces(const double *sHB, const double *r
             xtrace<P, true>(c, tr);                  // L traces of element 0 / the right neighbour
         double *dst = side == 0 ? sHL : side == 1 ? sE0 : sHR;
 #pragma unroll
-        for (int q = 0; q < N; ++q) dst[v * N + q] = tr[q];
+        for (int q = 0; q < N; ++q) dst[(v * N + q) * Smem<P>::LD] = tr[q];
     }
     __syncwarp();
 }
@@ -829,7 +835,7 @@ __device__ __forceinline__ unsigned stage_bottom(const double *tile, double *dst
     unsigned bad = 0;
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-        dst[q * kLanes + lane] = bt[q];
+        dst[q * Smem<P>::LD + lane] = bt[q];
         if (check) bad |= !(bt[q] > 0.0);
     }
     return bad;
@@ -919,14 +925,24 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
         if (y < nedge) {
             jb = y == 0 ? kp.band_lo : kp.band_hi - 1;
             je = jb + 1;
+        } else if (kp.even > 0) {
+            const int inner = kp.band_hi - kp.band_lo - 2;
+            jb = kp.band_lo + 1 + (y - nedge) * inner / kp.even;
+            je = kp.band_lo + 1 + (y - nedge + 1) * inner / kp.even;
         } else {
             jb = kp.band_lo + 1 + (y - nedge) * kp.rc;
             je = min(jb + kp.rc, kp.band_hi - 1);
         }
     } else {
         const bool second = (int)blockIdx.y >= kp.nchunk1;   // one launch can cover two row ranges
-        jb = second ? kp.j_begin2 + ((int)blockIdx.y - kp.nchunk1) * kp.rc : kp.j_begin + blockIdx.y * kp.rc;
-        je = min(jb + kp.rc, second ? kp.j_end2 : kp.j_end);
+        if (!second && kp.even > 0) {
+            const int rows = kp.j_end - kp.j_begin;
+            jb = kp.j_begin + (int)blockIdx.y * rows / kp.even;
+            je = kp.j_begin + ((int)blockIdx.y + 1) * rows / kp.even;
+        } else {
+            jb = second ? kp.j_begin2 + ((int)blockIdx.y - kp.nchunk1) * kp.rc : kp.j_begin + blockIdx.y * kp.rc;
+            je = min(jb + kp.rc, second ? kp.j_end2 : kp.j_end);
+        }
         if (jb >= je) return;
     }
     unsigned bad = 0;
@@ -1036,13 +1052,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
         double tt[N];
         ytrace<P, false>(c, tt);
 #pragma unroll
-        for (int q = 0; q < N; ++q) sT[(v * N + q) * kLanes + lane] = tt[q];
+        for (int q = 0; q < N; ++q) sT[(v * N + q) * SM::LD + lane] = tt[q];
     }
     if (!face_warp) {
         mbar_wait(mbar + v, 0);                    // row jb landed (this variable)
         if constexpr (MODAL) tile_to_nodal<P>(ring0, lane);
         // its bottom traces: the face below row jb (the face warp's pre-iteration)
-        bad |= owned & stage_bottom<P>(ring0, sFb + v * N * kLanes, lane, chk);
+        bad |= owned & stage_bottom<P>(ring0, sFb + v * N * SM::LD, lane, chk);
     }
     // periodic neighbours of the strip's border elements
     const int eL = (strip * kLanes - 1 + nx) % nx;
@@ -1088,7 +1104,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
             if (it + 1 <= last_fetch && (!pre || below)) {
                 const int dst = (int)((pre ? fb : fa) - smem);
                 const double *above = sRow + ((k + 1) % 3) * RL::SSTRIDE;
-                face_flux_call<P>(SM::TT, kLanes, lane, dst, kLanes, lane, dst, kLanes, lane,
+                face_flux_call<P>(SM::TT + lane, dst + lane, dst + lane,
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
                                            kp.alpha_mode, 1, above[RL::CRB], above[RL::COSB], alpha_y,
                                            kp.bdx});
@@ -1096,7 +1112,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
                 // a pole: no face, no flux (dg.py:483-495) -- the lift reads zeros
                 double *dst = pre ? fb : fa;
 #pragma unroll
-                for (int q = 0; q < 3 * N; ++q) dst[q * kLanes + lane] = 0.0;
+                for (int q = 0; q < 3 * N; ++q) dst[q * SM::LD + lane] = 0.0;
             }
             TSTAMP(c);
             __syncthreads();                           // barrier 2 of row it (prologue barrier B)
@@ -1112,7 +1128,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
                 border_traces<P, MODAL>(smem + SM::HB, next_tile, smem + SM::HL, smem + SM::E0, smem + SM::HR,
                                         lane);
                 // every lane computes the same face (uniform control flow, identical stores)
-                face_flux_call<P>(SM::HL, 1, 0, SM::E0, 1, 0, SM::F0 + ((k + 1) & 1) * 3 * N, 1, 0,
+                face_flux_call<P>(SM::HL, SM::E0, ((k + 1) & 1) ? SM::F0B : SM::F0A,
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
                                            kp.alpha_mode, 0, 0.0, 0.0, alpha_x, kp.bdy});
             }
@@ -1141,7 +1157,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
             {
                 double c[N][N];
                 tile_read<P>(c, cur, lane);            // X(jl)
-                bad |= owned & traces_row<P>(c, sXL + v * N * kLanes, sXR + v * N * kLanes, sT + v * N * kLanes,
+                bad |= owned & traces_row<P>(c, sXL + v * N * SM::LD, sXR + v * N * SM::LD, sT + v * N * SM::LD,
                                              lane, chk);
             }
             TSTAMP(0);
@@ -1149,7 +1165,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
                 mbar_wait(mbar + (slot ^ 1) * 3 + v, ((k + 1) >> 1) & 1);   // X(jl+1)
                 if constexpr (MODAL) tile_to_nodal<P>(ring0 + (slot ^ 1) * SM::TILE, lane);
                 // its bottom traces for the face warp's y-face above row jl
-                bad |= owned & stage_bottom<P>(ring0 + (slot ^ 1) * SM::TILE, sFa + v * N * kLanes, lane, chk);
+                bad |= owned & stage_bottom<P>(ring0 + (slot ^ 1) * SM::TILE, sFa + v * N * SM::LD, lane, chk);
             }
             TSTAMP(1);
             __syncthreads();                           // barrier 1
@@ -1159,8 +1175,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
                 // the h warp has the lightest volume work: it takes the x-faces 1..32
                 // (right face of every lane; the last valid lane's neighbour is the halo)
                 const bool last = lane == nvalid - 1;
-                face_flux_call<P>(SM::XRT, kLanes, lane, last ? SM::HR : SM::XL, last ? 1 : kLanes,
-                                  last ? 0 : min(lane + 1, kLanes - 1), SM::FX, kLanes, lane,
+                face_flux_call<P>(SM::XRT + lane, SM::XL + (last ? kLanes : min(lane + 1, kLanes - 1)), SM::FX + lane,
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
                                            kp.alpha_mode, 0, 0.0, 0.0, alpha_x, kp.bdy});
             }
@@ -1181,6 +1196,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
                     volume<P, true, OROG>(vol, v, ringS + slot * SM::TILE, row, lane, kp, sB);
             }
             TSTAMP(3);
+            double unr[N][N];                          // u^n loads in flight across barrier 2
+            if constexpr (HAS_U) {
+                const double *Uv = Uz + (size_t)jl * kp.rstride;
+#pragma unroll
+                for (int a = 0; a < N; ++a)
+#pragma unroll
+                    for (int b = 0; b < N; ++b) unr[a][b] = Uv[(a * N + b) * kLanes];
+            }
             __syncthreads();                           // barrier 2
             TSTAMP(4);
             const size_t roff = (size_t)jl * kp.rstride;
@@ -1194,10 +1217,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
                 if (jl == kp.band_hi - 1 && kp.peer_row[1])
                     Ypeer2 = kp.peer_row[1] + (size_t)blockIdx.z * kp.peer_zstride[1] + off;
             }
-            bad |= finalize<P, HAS_U, HAS_Y2, MODAL>(vol, cur, HAS_U ? Uz + roff : nullptr,
-                                                     HAS_Y2 ? Az + roff : nullptr, HAS_Y2 ? Y2z + roff : nullptr,
-                                                     v, sFX, smem + SM::F0 + slot * 3 * N, sFa, sFb, row, lane,
-                                                     owned, Yz + roff, kp, Ypeer, Ypeer2);
+            bad |= finalize<P, HAS_U, HAS_Y2, MODAL>(vol, cur, HAS_Y2 ? Az + roff : nullptr, HAS_Y2 ? Y2z + roff : nullptr,
+                                                     v, sFX, smem + (slot ? SM::F0B : SM::F0A), sFa, sFb, row, lane,
+                                                     owned, Yz + roff, kp, Ypeer, Ypeer2, unr);
             // X(jl) is consumed: stream row jl+2 into its slot (L2-warm by now)
             __syncwarp();
             if (lane == 0 && jl + 2 <= last_fetch) {

@@ -34,6 +34,8 @@ struct StageParams {
     int nx, nstrip, ny, row0, nrows;
     int j_begin, j_end, rc;   // local rows [j_begin, j_end), rc rows per CTA
     int nchunk1;              // chunks of the first range; later chunks cover [j_begin2, j_end2)
+    int even;                 // > 0: the first range (edge launches: the interior rows) is split
+                              // into `even` chunks of floor/ceil(rows/even) rows instead of rc
     int j_begin2, j_end2;
     double a, b, g;       // Y = a U + b X + g RHS(X)
     double dx[kMaxP + 1][kMaxP + 1];   // (1/R)(determ/bd_det_x) dh: the xi derivative of F

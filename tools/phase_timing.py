@@ -1,6 +1,6 @@
 """Per-role phase timing of the stage kernel (DG_TIMING experiment build).
 
-    DGSWE_LIB=build/variants/<timing>.so python tools/phase_timing.py [--config c3]
+    DGSWE_LIB=build/variants/<timing>.so python tools/phase_timing.py [nx ny p]
 Prints average cycles per row for each warp role and phase.
 """
 import ctypes
@@ -16,13 +16,15 @@ from paper_2303_11767_b200 import SpatialOperator, _lib, build_case, default_con
 
 
 def main():
-    nx, ny, p, dt = 720, 360, 3, 5e-3
+    a = sys.argv[1:]
+    nx, ny, p = (int(x) for x in (a[0:3] if len(a) >= 3 else (720, 360, 3)))
+    dt = 5e-3
     cfg = default_config("williamson_tc6").override(nx=nx, ny=ny, p=p)
     setup = build_case(cfg)
     op = SpatialOperator(setup.mesh, p, setup.model)
     st = op.project_state(setup.ic)
     lib = _lib.load()
-    fn = lib.dgswe_debug_timing
+    fn = getattr(lib, f"dgswe_debug_timing_p{p}")
     fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
     buf = (ctypes.c_ulonglong * 28)()
     op.ssprk3_steps(st, dt, 3)
