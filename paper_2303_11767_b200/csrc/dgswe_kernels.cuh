@@ -166,7 +166,10 @@ struct Smem {
     static constexpr int N = P + 1;
     static constexpr int NP = N * N;
     static constexpr int TILE = 3 * NP * kLanes;         // one row of coefficients, all vars
-    static constexpr int LD = kLanes + 1;                // leading dimension of trace / flux arrays:
+#ifndef DG_LD
+#define DG_LD 33
+#endif
+    static constexpr int LD = DG_LD;                     // leading dimension of trace / flux arrays:
                                                          // columns 0..31 = lanes, column 32 = a strip-
                                                          // border value (halo traces, border face flux)
     static constexpr int TR = 3 * N * LD;                // one trace / face-flux set [3][N][LD]
@@ -177,15 +180,16 @@ struct Smem {
     static constexpr int XL = E + (vol_rolled<P>() ? TILE : 0);   // L traces [3][N][LD]
     static constexpr int XRT = XL + TR;                  // R traces
     static constexpr int TT = XRT + TR;                  // top traces of current row
-    static constexpr int FX = TT + TR;                   // x-face fluxes, column c = right face of lane c
+    static constexpr int FX = TT + TR;                   // x-face fluxes, column c = LEFT face of lane c
+                                                         // (column 0: the strip's border face)
     static constexpr int FY0 = FX + TR;                  // y-face flux buffers
     static constexpr int FY1 = FY0 + TR;
     // column 32 of those arrays (face warp): halo / border values
     static constexpr int HR = XL + kLanes;               // right neighbour's L trace (x-face of the last lane)
     static constexpr int HL = XRT + kLanes;              // left neighbour's R trace (border face "in")
     static constexpr int E0 = TT + kLanes;               // element 0's L trace (border face "out")
-    static constexpr int F0A = FX + kLanes;              // border face 0 flux, even rows
-    static constexpr int F0B = FY0 + kLanes;             // odd rows
+    static constexpr int F0T = FY0 + kLanes;             // next row's border face flux (copied to FX
+                                                         // column 0 after that row's barrier 1)
     static constexpr int HB = FY1 + TR;                  // next row's neighbour coefficients [2][3][NP]
     static constexpr int ROW = HB + 6 * NP;              // row-table ring, 3 rows
     static constexpr int MBAR = ROW + 3 * RowLayout<P>::SSTRIDE;  // 6 mbarriers [slot][var]
@@ -642,7 +646,7 @@ __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v
 template <int P, bool HAS_U, bool HAS_Y2, bool MODAL>
 __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const double *cur,
                                              const double *Av, double *Y2v, int v,
-                                             const double *sFX, const double *sF0,
+                                             const double *sFX,
                                              const double *sFtop, const double *sFbot,
                                              const double *row, int lane, bool owned,
                                              double *Yv, const StageParams &kp, double *Ypeer,
@@ -666,11 +670,11 @@ __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const 
             for (int j = 0; j < N; ++j) acc[i][j] += sE[(i * N + j) * kLanes + lane];
     }
     constexpr int LD = Smem<P>::LD;
-    const int o = (v * N) * LD;        // x-face column c: right face of lane c (lane 0's left face: F0)
+    const int o = (v * N) * LD;        // x-face column c: left face of lane c
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-        const double l = lane == 0 ? sF0[o + q * LD] : sFX[o + q * LD + lane - 1];
-        const double r = sFX[o + q * LD + lane];
+        const double l = sFX[o + q * LD + lane];
+        const double r = sFX[o + q * LD + lane + 1];
         const double t = sFtop[o + q * LD + lane];     // zero at a pole (the face warp)
         const double bo = sFbot[o + q * LD + lane];
 #pragma unroll
@@ -1086,6 +1090,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
             if (!pre) __syncthreads();                 // barrier 1 of row it
             TSTAMP(b);
             if (!pre) {
+                // this row's border face (formed in the last window) into FX column 0:
+                // the previous row's finalize, its last reader, is done
+                if (lane < 3 * N) smem[SM::FX + lane * SM::LD] = smem[SM::F0T + lane * SM::LD];
                 // async gathers, consumed after barrier 2: the next row's neighbour
                 // coefficients and the table of row it+2 (its slot held row it-1)
                 if (it + 1 < je)
@@ -1128,7 +1135,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
                 border_traces<P, MODAL>(smem + SM::HB, next_tile, smem + SM::HL, smem + SM::E0, smem + SM::HR,
                                         lane);
                 // every lane computes the same face (uniform control flow, identical stores)
-                face_flux_call<P>(SM::HL, SM::E0, ((k + 1) & 1) ? SM::F0B : SM::F0A,
+                face_flux_call<P>(SM::HL, SM::E0, SM::F0T,
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
                                            kp.alpha_mode, 0, 0.0, 0.0, alpha_x, kp.bdy});
             }
@@ -1175,7 +1182,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
                 // the h warp has the lightest volume work: it takes the x-faces 1..32
                 // (right face of every lane; the last valid lane's neighbour is the halo)
                 const bool last = lane == nvalid - 1;
-                face_flux_call<P>(SM::XRT + lane, SM::XL + (last ? kLanes : min(lane + 1, kLanes - 1)), SM::FX + lane,
+                face_flux_call<P>(SM::XRT + lane, SM::XL + (last ? kLanes : min(lane + 1, kLanes - 1)), SM::FX + lane + 1,
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
                                            kp.alpha_mode, 0, 0.0, 0.0, alpha_x, kp.bdy});
             }
@@ -1218,7 +1225,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
                     Ypeer2 = kp.peer_row[1] + (size_t)blockIdx.z * kp.peer_zstride[1] + off;
             }
             bad |= finalize<P, HAS_U, HAS_Y2, MODAL>(vol, cur, HAS_Y2 ? Az + roff : nullptr, HAS_Y2 ? Y2z + roff : nullptr,
-                                                     v, sFX, smem + (slot ? SM::F0B : SM::F0A), sFa, sFb, row, lane,
+                                                     v, sFX, sFa, sFb, row, lane,
                                                      owned, Yz + roff, kp, Ypeer, Ypeer2, unr);
             // X(jl) is consumed: stream row jl+2 into its slot (L2-warm by now)
             __syncwarp();
