@@ -67,9 +67,6 @@ __host__ __device__ constexpr int min_blocks() { return P <= 3 ? 4 : 2; }
 template <int P>
 __host__ __device__ constexpr bool vol_rolled() { return P >= 2; }
 
-#ifndef DG_CELER_SEL
-#define DG_CELER_SEL 0
-#endif
 
 // DG_TIMING builds record per-role phase durations (clock cycles) of every
 // row: [role][A work, barrier-1 wait, B work, barrier-2 wait, C work, rows]
@@ -166,10 +163,7 @@ struct Smem {
     static constexpr int N = P + 1;
     static constexpr int NP = N * N;
     static constexpr int TILE = 3 * NP * kLanes;         // one row of coefficients, all vars
-#ifndef DG_LD
-#define DG_LD 33
-#endif
-    static constexpr int LD = DG_LD;                     // leading dimension of trace / flux arrays:
+    static constexpr int LD = kLanes + 1;                // leading dimension of trace / flux arrays:
                                                          // columns 0..31 = lanes, column 32 = a strip-
                                                          // border value (halo traces, border face flux)
     static constexpr int TR = 3 * N * LD;                // one trace / face-flux set [3][N][LD]
@@ -250,11 +244,7 @@ __device__ __forceinline__ void inv_and_celerity(double h, double h_floor, doubl
 {
     const double y = rsqrt64(max_pos(h, 2.2250738585072014e-308));
     r = ge_pos(h, h_floor) ? y * y : inv_floor;   // branches compared on the integer pipe
-#if DG_CELER_SEL
-    c = __double_as_longlong(h) > 0 ? sqrt_g * (h * y) : 0.0;
-#else
     c = sqrt_g * (h * y);
-#endif
 }
 
 // --- TMA bulk copies and mbarriers (one elected lane per variable warp) ---
@@ -586,9 +576,9 @@ __device__ __forceinline__ void volume(double (&acc)[P + 1][P + 1], int v, const
 // Same terms with the loop over node rows kept rolled (a quarter of the
 // code): the row-local G/S terms of row i go to shared memory sE (this
 // warp's [NP][32] block) and are added in finalize; F still scatters into
-// the register tile through the i-th column of Dx.  The h equation's
-// row-local term (G = hv cos/R) is formed by the hv warp (KIND 2): the h
-// warp's x-face work leaves it the longest volume phase otherwise.
+// the register tile through the i-th column of Dx.  Every variable warp
+// forms its own row-local term (the h warp's: G = hv cos/R); the momentum
+// warps' physics is the longest phase-B work, so nothing moves onto them.
 template <int P, int KIND, bool OROG>
 __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v, const double *sU,
                                               const double *row, int lane, const StageParams &kp, double *sE,
@@ -604,28 +594,12 @@ __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v
     for (int i = 0; i < N; ++i) {
         double F[N], G[N], S[N];
         node_physics<P, KIND, OROG>(false, i, sU, rr, lane, kp, sB, F, G, S);
-        if constexpr (KIND != 0) {
 #pragma unroll
-            for (int j = 0; j < N; ++j) {
-                double e = S[j];
+        for (int j = 0; j < N; ++j) {
+            double e = S[j];
 #pragma unroll
-                for (int k = 0; k < N; ++k) e = fma(c_nod[P].dh[j][k], G[k], e);
-                sE[(i * N + j) * kLanes + lane] = e;
-            }
-        }
-        if constexpr (KIND == 2) {
-            constexpr int NP = N * N;
-            double gh[N];
-#pragma unroll
-            for (int k = 0; k < N; ++k) gh[k] = sU[(2 * NP + i * N + k) * kLanes + lane] * rr.crc(k);
-            double *sEh = sE - KIND * NP * kLanes;
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                double e = c_nod[P].dh[j][0] * gh[0];
-#pragma unroll
-                for (int k = 1; k < N; ++k) e = fma(c_nod[P].dh[j][k], gh[k], e);
-                sEh[(i * N + j) * kLanes + lane] = e;
-            }
+            for (int k = 0; k < N; ++k) e = fma(c_nod[P].dh[j][k], G[k], e);
+            sE[(i * N + j) * kLanes + lane] = e;
         }
 #pragma unroll
         for (int ii = 0; ii < N; ++ii) {

@@ -21,6 +21,8 @@ KEYS = [
     "lts__t_sector_hit_rate.pct", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
     "sm__cycles_elapsed.avg.per_second",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.max", "smsp__inst_executed.avg",
+    "smsp__cycles_active.avg", "sm__warps_active.avg.per_cycle_active",
 ]
 
 
