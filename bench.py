@@ -407,8 +407,8 @@ def run_gpu(args):
             k: local_dofs * (16.0 if k == 1 else 24.0) / (v * 1e-3) / 1e9 for k, v in per_stage.items()}
 
     # the reference's own entry point on a device state: rk_step(state,
-    # op.assemble_rhs, dt, tableau(3)) -- three single-launch modal stage
-    # kernels per step (in-kernel modal<->nodal conversion) and the per-step
+    # op.assemble_rhs, dt, tableau(3)) -- three stage kernels per step on the
+    # state's nodal values (converted once, back when read) and the per-step
     # status read the reference's exceptions need (timestep.py:149-167)
     api = None
     if world == 1 and not args.no_api and not big:
@@ -428,8 +428,9 @@ def run_gpu(args):
         torch.cuda.synchronize()
         ms_api = a0.elapsed_time(a1) / k3
         ach = dofs * B_ALG / (ms_api / 3 * 1e-3) / 1e9
-        api = {"path": "rk_step(state, op.assemble_rhs, dt, tableau(3)): 3 modal single-launch stage "
-                       "kernels + 1 status read per step", "value": dofs * 3 / (ms_api * 1e-3), "unit": UNIT,
+        api = {"path": "rk_step(state, op.assemble_rhs, dt, tableau(3)): 3 stage kernels (one CUDA graph replay) on the "
+                       "lazily converted nodal state + 1 status read (host sync) per step",
+               "value": dofs * 3 / (ms_api * 1e-3), "unit": UNIT,
                "ms_per_step": ms_api, "steps": k3, "gpu_launches": op.launch_count() - n_api,
                "achieved_gbs": ach, "frac": ach / measured_peaks().get("hbm_gbs", 6650.0)}
         del st_api, ws

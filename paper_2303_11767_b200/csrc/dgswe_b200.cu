@@ -359,8 +359,10 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
               cudaMalloc(&ctx->alpha, 2 * sizeof(double)) == cudaSuccess &&
               cudaMalloc(&ctx->status, sizeof(DevStatus)) == cudaSuccess &&
               cudaMalloc(&ctx->diag, ctx->diag_doubles * sizeof(double)) == cudaSuccess &&
+              cudaMallocHost(&ctx->status_host, 2 * sizeof(DevStatus)) == cudaSuccess &&
               (ob.empty() || cudaMalloc(&ctx->orog, ob.size() * sizeof(double)) == cudaSuccess);
     if (ok) {
+        ctx->status_host[1] = kStatus0;   // the reset value, copied from pinned memory
         ok = cudaMemcpy(ctx->rowtab, rt.data(), rt.size() * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess &&
              cudaMemcpy(ctx->cos_edge, t->cos_edge, (c.ny + 1) * sizeof(double), cudaMemcpyHostToDevice) ==
                  cudaSuccess &&
@@ -388,6 +390,7 @@ void dgswe_destroy(dgswe_ctx *ctx)
     cudaFree(ctx->status);
     cudaFree(ctx->diag);
     cudaFree(ctx->orog);
+    if (ctx->status_host) cudaFreeHost(ctx->status_host);
     delete ctx;
 }
 
@@ -693,16 +696,14 @@ int dgswe_status_tags(dgswe_ctx *ctx, uint32_t *flags, int32_t *tags, int reset,
 {
     if (!ctx) return dgswe_fail(DGSWE_EINVAL, "null context");
     cudaStream_t s = (cudaStream_t)stream;
-    DevStatus h;
-    CUDA_TRY(cudaMemcpyAsync(&h, ctx->status, sizeof h, cudaMemcpyDeviceToHost, s));
+    // read (into pinned host memory) and reset in stream order, one synchronisation
+    DevStatus *h = ctx->status_host;
+    CUDA_TRY(cudaMemcpyAsync(h, ctx->status, sizeof *h, cudaMemcpyDeviceToHost, s));
+    if (reset) CUDA_TRY(cudaMemcpyAsync(ctx->status, h + 1, sizeof *h, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaStreamSynchronize(s));
-    if (flags) *flags = h.flags;
+    if (flags) *flags = h->flags;
     if (tags)
-        for (int b = 0; b < dgswe::kStatusBits; ++b) tags[b] = h.first_tag[b];
-    if (reset) {
-        CUDA_TRY(cudaMemcpyAsync(ctx->status, &kStatus0, sizeof kStatus0, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
-    }
+        for (int b = 0; b < dgswe::kStatusBits; ++b) tags[b] = h->first_tag[b];
     return DGSWE_OK;
 }
 

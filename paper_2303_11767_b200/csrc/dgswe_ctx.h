@@ -75,6 +75,7 @@ struct dgswe_ctx {
     double *cos_edge = nullptr;   // device, ny+1
     double *alpha = nullptr;      // device, 2 doubles
     DevStatus *status = nullptr;  // device
+    DevStatus *status_host = nullptr;   // pinned host [2]: last read, reset value
     double *orog = nullptr;       // device [nrows][2][nstrip][nphi][32] orography factors, or null
     int external_alpha = 0;
     long long launches = 0;

@@ -102,6 +102,14 @@ class State:
     ``interior_coeffs(name)`` returns a host copy shaped like the
     reference's (nx, ny, nz, nphi) view; writes to it do not reach the
     device (use :meth:`set_interior_coeffs`).
+
+    Between consecutive fused ``rk_step`` calls the buffer may hold the
+    values at the Gauss nodes instead of the modal coefficients (the stage
+    kernels' own basis): every read through ``data``
+    (and so every method below, the diagnostics and the Butcher path)
+    converts it back first, in place, with one elementwise kernel.  The
+    raw buffer is ``_data``; ``_nodal`` is the operator whose nodal basis
+    it currently holds (None: modal).
     """
 
     def __init__(self, data: torch.Tensor, nx: int, ny: int, nz: int, nphi: int):
@@ -112,9 +120,31 @@ class State:
                              f"(nz, ny, 3, nstrip, nphi, {STRIP}), got {tuple(data.shape)}")
         if data.data_ptr() % 16:
             raise ValueError("State data must be 16-byte aligned (the kernels move row tiles by TMA)")
-        self.data = data
+        self._data = data
+        self._nodal = None
         self.names = VAR_NAMES
         self.nx, self.ny, self.nz, self.nphi = nx, ny, nz, nphi
+
+    @property
+    def data(self) -> torch.Tensor:
+        """The modal coefficients (converted back in place if the buffer holds nodal values)."""
+        if self._nodal is not None:
+            op, self._nodal = self._nodal, None
+            op._ctx.convert(self._data, False, 0, self.ny)
+        return self._data
+
+    @data.setter
+    def data(self, value: torch.Tensor):
+        self._data = value
+        self._nodal = None
+
+    def _as_nodal(self, op) -> torch.Tensor:
+        """The raw buffer holding ``op``'s nodal values (converted in place if modal)."""
+        if self._nodal is not op:
+            raw = self.data                      # modal (converting back from another operator's basis)
+            op._ctx.convert(raw, True, 0, self.ny)
+            self._nodal = op
+        return self._data
 
     @property
     def fields(self) -> dict:
@@ -274,6 +304,7 @@ class SpatialOperator:
                                  self.Minv_rows, row_chunk=row_chunk, bottom=self.bottom_nodal)
         self._phi_dev = None
         self._scratch = {}
+        self._replayed = 0          # kernel launches replayed from Python-captured CUDA graphs
 
     def _bottom_at_nodes(self):
         """(ny, nx, n*n) orography b at every element's Gauss nodes (q = qi n + qj,
@@ -503,49 +534,86 @@ class SpatialOperator:
         cur.wait_stream(s_out)
         cur.wait_stream(s_in)
 
-    def rk_step_fused(self, state: State, dt: float, order: int, bufs, tag: int = 0) -> State:
-        """One step of tableau(order) (1..4) in fused stage form on modal
-        states: ``order`` single-launch stage kernels (each converts its
-        tiles to nodal values in shared memory and its outputs back to modes;
-        no other kernel, no allocation), the last one writing the new state
-        into ``bufs[order-1]`` with the non-finite check.  Returns that buffer;
-        ``state`` is left untouched (the caller swaps on success, so a
-        PositivityError leaves u^n in place like the reference)."""
+    def rk_step_fused(self, state: State, dt: float, order: int, bufs, tag: int = 0) -> torch.Tensor:
+        """One step of tableau(order) (1..4) in fused stage form on the
+        nodal values: ``state`` is converted to nodal values in place if it
+        holds modes (once; it stays nodal until it is read, see State), then
+        ``order`` stage kernels -- the same launches as a step of
+        ``rk_steps`` (no other kernel, no allocation) -- the last one writing
+        the new state into ``bufs[order-1]`` with the non-finite check.
+        Returns that raw (nodal) buffer; ``state`` keeps u^n (the caller
+        swaps on success, so a PositivityError leaves u^n in place like the
+        reference)."""
         c = self._ctx
-        st = c.stream()
-        u = state.data
+        if state._nodal is self:
+            u = state._data
+        else:
+            # first fused step of a modal state: convert a copy (the spare
+            # buffer), so a PositivityError leaves the caller's modes untouched
+            spare = bufs[-1]
+            spare._data.copy_(state.data)
+            spare._nodal = None
+            u = spare._as_nodal(self)
+            bufs = bufs[:-1]
 
         def stage(a, U, b, X, g, Y, check=False):
             _lib.check(c.lib.dgswe_stage_rows_checked(
                 c.h, float(a), _ptr(U), float(b), _ptr(X), float(g), _ptr(Y), int(tag), 0, self.mesh.ny,
-                int(check), 0, st), "dgswe_stage_rows_checked")
+                int(check), 0, c.stream()), "dgswe_stage_rows_checked")
 
         def stage2(a, U, b, X, g, Y, A, g2, Y2):
             _lib.check(c.lib.dgswe_stage2(c.h, float(a), _ptr(U), float(b), _ptr(X), float(g), _ptr(Y),
-                                          _ptr(A), float(g2), _ptr(Y2), int(tag), 0, self.mesh.ny, st),
+                                          _ptr(A), float(g2), _ptr(Y2), int(tag), 0, self.mesh.ny, c.stream()),
                        "dgswe_stage2")
 
-        b = [x.data if isinstance(x, State) else x for x in bufs]
-        if order == 1:
-            stage(0.0, None, 1.0, u, dt, b[0], check=True)
-            return b[0]
-        if order == 2:
-            stage(0.0, None, 1.0, u, dt, b[0])
-            stage(0.5, u, 0.5, b[0], 0.5 * dt, b[1], check=True)
-            return b[1]
-        if order == 3:
-            stage(0.0, None, 1.0, u, dt, b[0])
-            stage(0.75, u, 0.25, b[0], 0.25 * dt, b[1])
-            stage(1.0 / 3.0, u, 2.0 / 3.0, b[1], (2.0 / 3.0) * dt, b[2], check=True)
-            return b[2]
-        if order == 4:
+        b = [x._data if isinstance(x, State) else x for x in bufs]
+        if order not in (1, 2, 3, 4):
+            raise ValueError(f"unsupported RK order {order}; choose 1..4")
+        # the step's launches are captured once per (buffers, dt, order) and
+        # replayed as one CUDA graph (the state/workspace swap alternates
+        # between two buffer assignments, so two graphs serve a run)
+        key = ("rkstep", order, float(dt), int(tag), u.data_ptr(), tuple(x.data_ptr() for x in b[:order]))
+        g = self._scratch.get(key)
+        if g is not None and self.rusanov.mode == "local":
+            g.replay()
+            self._replayed += order
+            return b[order - 1]
+        out = self._rk_stages(u, b, dt, order, tag, stage, stage2)
+        if self.rusanov.mode == "local":
+            if sum(1 for k in self._scratch if isinstance(k, tuple) and k[0] == "rkstep") >= 8:
+                for k in [k for k in self._scratch if isinstance(k, tuple) and k[0] == "rkstep"]:
+                    del self._scratch[k]
+            g = torch.cuda.CUDAGraph()              # captured, not run: this call's step was the eager one
+            with torch.cuda.graph(g):
+                self._rk_stages(u, b, dt, order, tag, stage, stage2)
+            self._replayed -= order                 # the C counter counted the captured launches
+            self._scratch[key] = g
+        return out
+
+    def _rk_stages(self, u, b, dt, order, tag, stage, stage2):
+        c = self._ctx
+        c.set_basis(True)
+        try:
+            if order == 1:
+                stage(0.0, None, 1.0, u, dt, b[0], check=True)
+                return b[0]
+            if order == 2:
+                stage(0.0, None, 1.0, u, dt, b[0])
+                stage(0.5, u, 0.5, b[0], 0.5 * dt, b[1], check=True)
+                return b[1]
+            if order == 3:
+                stage(0.0, None, 1.0, u, dt, b[0])
+                stage(0.75, u, 0.25, b[0], 0.25 * dt, b[1])
+                stage(1.0 / 3.0, u, 2.0 / 3.0, b[1], (2.0 / 3.0) * dt, b[2], check=True)
+                return b[2]
             w1, w2, acc, out = b[0], b[1], b[2], b[3]
             stage2(0.0, None, 1.0, u, 0.5 * dt, w1, u, dt / 6.0, acc)
             stage2(1.0, u, 0.0, w1, 0.5 * dt, w2, acc, dt / 3.0, acc)
             stage2(1.0, u, 0.0, w2, dt, w1, acc, dt / 3.0, acc)
             stage(1.0, acc, 0.0, w1, dt / 6.0, out, check=True)
             return out
-        raise ValueError(f"unsupported RK order {order}; choose 1..4")
+        finally:
+            c.set_basis(False)
 
     def stage2(self, a: float, U: State | None, b: float, X: State, g: float, Y: State, A: State,
                g2: float, Y2: State, tag: int = 0):
@@ -563,7 +631,7 @@ class SpatialOperator:
         return self._ctx.status_tags(reset)
 
     def launch_count(self) -> int:
-        return self._ctx.launches()
+        return self._ctx.launches() + self._replayed
 
     # -- host-side helpers (diagnostics / step control) ---------------------
 

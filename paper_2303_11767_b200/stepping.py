@@ -4,8 +4,10 @@ Same API as /root/reference/pkg/src/dgswe/timestep.py (``ButcherTableau``,
 ``tableau``, ``TimeControls``, ``DivergenceError``, ``StepLog``,
 ``rk_step``, ``integrate``).  Two device paths:
 
-* ``rk_step`` -- with ``tableau(1..4)`` one single-launch stage kernel per
-  stage on the modal state (Shu-Osher / RK4-accumulator forms); any other
+* ``rk_step`` -- with ``tableau(1..4)`` one stage kernel per stage
+  (Shu-Osher / RK4-accumulator forms) on the state's nodal values: the
+  state is converted in place on the first call and stays nodal until it
+  is read (``State.data`` converts back); any other
   tableau (or ``fused=False``) in Butcher form: per stage a device copy,
   axpy launches (two roundings, like ``_axpy`` timestep.py:132-141) and one
   RHS launch.  One status read per step.
@@ -122,6 +124,7 @@ class _RKWorkspace:
     def __init__(self, state, stages: int):
         self.stage_input = state.copy()
         self.k = [state.copy() for _ in range(stages)]
+        self.spare = state.copy()   # fused rk_step: nodal copy of a modal u^n (first step)
 
 
 def _device_operator(rhs_fn):
@@ -147,10 +150,12 @@ def rk_step(state, rhs_fn, dt: float, tab: ButcherTableau, workspace: _RKWorkspa
     """One explicit RK step, updating ``state`` in place (timestep.py:149-167).
 
     With our operator's ``assemble_rhs`` and ``tableau(1..4)`` (``fused``):
-    one single-launch stage kernel per stage on the modal state (the stage
+    one stage kernel per stage on the state's nodal values (the stage
     combination fused into the RHS kernel: SSPRK3 moves 21.3 B/DOF instead
-    of the Butcher form's copies and axpys), the new state written into a
-    workspace buffer that is swapped into ``state`` on success.  Otherwise
+    of the Butcher form's copies and axpys; the state is converted to nodal
+    values once and back only when something reads it), the new state
+    written into a workspace buffer that is swapped into ``state`` on
+    success.  Otherwise
     (or ``fused=False``) the Butcher form of the reference: per stage a
     copy, axpys with two roundings and one RHS launch.  Both read the status
     once per step: PositivityError (from any stage's RHS) leaves ``state``
@@ -163,13 +168,14 @@ def rk_step(state, rhs_fn, dt: float, tab: ButcherTableau, workspace: _RKWorkspa
         return _rk_step_generic(state, rhs_fn, dt, tab, ws)
     order = _fused_order(tab) if fused else None
     if order is not None:
-        bufs = [ws.stage_input] + list(ws.k)
+        bufs = [ws.stage_input] + list(ws.k) + [ws.spare]
         new = op.rk_step_fused(state, dt, order, bufs)
         flags, _ = op.status(reset=True)
         op.raise_on_status(flags)                   # PositivityError: state still u^n
-        # the new state becomes ``state``; its old buffer joins the workspace
-        slot = next(b for b in bufs if b.data is new)
-        state.data, slot.data = new, state.data
+        # the new (nodal) state becomes ``state``; its old buffer joins the workspace
+        slot = next(b for b in bufs if b._data is new)
+        state._data, slot._data = new, state._data
+        state._nodal, slot._nodal = op, None
         if flags & _lib.STATUS_NONFINITE:
             raise DivergenceError("non-finite state after RK update", -1, float("nan"))
         return state
