@@ -988,9 +988,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
     const int r_last = min(kp.nrows - 1, kp.ny - 1 - kp.row0);
     const int last_fetch = min(je, r_last);        // rows jb..last_fetch stream through the ring
 
-    if (threadIdx.x == 0) {
-        for (int k = 0; k < 6; ++k) mbar_init(mbar + k, 1);
+    // each variable warp's elected lane initialises its own two ring
+    // mbarriers and starts streaming rows jb, jb+1 at once: the copies are
+    // in flight while the row tables and the row below the chunk load
+    if (!face_warp && lane == 0) {
+        mbar_init(mbar + v, 1);
+        mbar_init(mbar + 3 + v, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        issue_row(0, jb);
+        if (jb + 1 <= last_fetch) issue_row(1, jb + 1);
     }
 
     // row-table ring: slot (r - jb) % 3 holds local row r (rows jb, jb+1 now,
@@ -1003,20 +1009,6 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
             sRow[idx] = kp.rowtab[(size_t)(gfirst + r) * RL::STRIDE + (idx - r * RL::SSTRIDE)];
         }
     }
-    __syncthreads();
-
-    // prologue: the var warps' elected lanes start streaming rows jb, jb+1
-    if (!face_warp && lane == 0) {
-        issue_row(0, jb);
-        if (jb + 1 <= last_fetch) issue_row(1, jb + 1);
-    }
-
-    double alpha_x = kp.alpha, alpha_y = kp.alpha;
-    if (kp.alpha_mode == 2) {
-        alpha_x = kp.alpha_dev[0];
-        alpha_y = kp.alpha_dev[1];
-    }
-
     // top traces of the row below the chunk (its first row's bottom face)
     const bool below = gfirst > 0;
     if (below && !face_warp) {
@@ -1031,6 +1023,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
         ytrace<P, false>(c, tt);
 #pragma unroll
         for (int q = 0; q < N; ++q) sT[(v * N + q) * SM::LD + lane] = tt[q];
+    }
+    __syncthreads();
+    double alpha_x = kp.alpha, alpha_y = kp.alpha;
+    if (kp.alpha_mode == 2) {
+        alpha_x = kp.alpha_dev[0];
+        alpha_y = kp.alpha_dev[1];
     }
     if (!face_warp) {
         mbar_wait(mbar + v, 0);                    // row jb landed (this variable)
