@@ -868,6 +868,17 @@ __device__ __forceinline__ bool wait_counter(const unsigned long long *ctr, unsi
     return true;
 }
 
+// First row of chunk c when `rows` rows are split into n chunks of
+// floor/ceil(rows / n) rows, the longer chunks first (lowest blockIdx.y):
+// the block scheduler hands out CTAs in index order, one per SM per round,
+// so the long chunks spread over distinct SMs instead of stacking on some
+// (C3: +1.5% over interleaved lengths).
+__device__ __forceinline__ int even_start(int c, int rows, int n)
+{
+    const int q = rows / n, r = rows - q * n;
+    return c * q + min(c, r);
+}
+
 template <int P, int F>
 __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageParams kp)
 {
@@ -905,8 +916,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
             je = jb + 1;
         } else if (kp.even > 0) {
             const int inner = kp.band_hi - kp.band_lo - 2;
-            jb = kp.band_lo + 1 + (y - nedge) * inner / kp.even;
-            je = kp.band_lo + 1 + (y - nedge + 1) * inner / kp.even;
+            jb = kp.band_lo + 1 + even_start(y - nedge, inner, kp.even);
+            je = kp.band_lo + 1 + even_start(y - nedge + 1, inner, kp.even);
         } else {
             jb = kp.band_lo + 1 + (y - nedge) * kp.rc;
             je = min(jb + kp.rc, kp.band_hi - 1);
@@ -915,8 +926,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
         const bool second = (int)blockIdx.y >= kp.nchunk1;   // one launch can cover two row ranges
         if (!second && kp.even > 0) {
             const int rows = kp.j_end - kp.j_begin;
-            jb = kp.j_begin + (int)blockIdx.y * rows / kp.even;
-            je = kp.j_begin + ((int)blockIdx.y + 1) * rows / kp.even;
+            jb = kp.j_begin + even_start(blockIdx.y, rows, kp.even);
+            je = kp.j_begin + even_start(blockIdx.y + 1, rows, kp.even);
         } else {
             jb = second ? kp.j_begin2 + ((int)blockIdx.y - kp.nchunk1) * kp.rc : kp.j_begin + blockIdx.y * kp.rc;
             je = min(jb + kp.rc, second ? kp.j_end2 : kp.j_end);
