@@ -64,7 +64,12 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """nvidia-smi clocks / throttle reasons during the timed region.
+
+    Started before the warm-up, so the NVML start-up of nvidia-smi is not
+    inside the timed region; every line is stamped on arrival and
+    ``summary(t0, t1)`` keeps the samples taken while the timed region ran
+    (20 ms period: several samples even in a 40 ms region)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -79,7 +84,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
@@ -89,21 +94,29 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *exc):
         if self.proc is not None:
-            time.sleep(0.25)
+            time.sleep(0.1)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
         sm, mx, reasons = [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        lines = self.lines
+        if t0 is not None:
+            # a sample is printed up to one period after it is taken
+            inside = [ln for ts, ln in lines if t0 <= ts <= t1 + 0.03]
+            later = [ln for ts, ln in lines if ts > t1 + 0.03][:1]
+            lines = inside or later
+        else:
+            lines = [ln for _, ln in lines]
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -337,7 +350,9 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # warm-up (also builds the CUDA graph for k = steps)
+    # warm-up (also builds the CUDA graph for k = steps); the clock sampler
+    # starts here so its start-up is outside the timed region
+    clk = ClockSampler(local).__enter__()
     steps(args.warmup)
     steps(args.steps)
     torch.cuda.synchronize()
@@ -346,14 +361,17 @@ def run_gpu(args):
     # timed region: K steps, device events, max over ranks
     n0 = counter()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        steps(args.steps)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
+    barrier()
+    torch.cuda.synchronize()
+    t_in = time.time()
+    ev0.record(stream)
+    steps(args.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    t_out = time.time()
+    barrier()
+    clk.__exit__(None, None, None)
+    clocks = clk.summary(t_in, t_out)
     launches = counter() - n0
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     if world == 1:
@@ -507,7 +525,7 @@ def run_gpu(args):
                              f"(3 states) > 126 MB L2" if args.config != "c2" else
                              "C2 states (25 MB each) fit in L2; roofline inflated"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "api_rk_step": api,
-            "clocks": clk.summary(), "gpu_launches": int(launches),
+            "clocks": clocks, "gpu_launches": int(launches),
             "dofs_per_gpu": local_dofs, "per_gpu_value": value / world,
         }
         print(json.dumps(line), flush=True)

@@ -1094,6 +1094,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
             if (it + 1 <= last_fetch && (!pre || below)) {
                 const int dst = (int)((pre ? fb : fa) - smem);
                 const double *above = sRow + ((k + 1) % 3) * RL::SSTRIDE;
+                if (owned)
                 face_flux_call<P>(SM::TT + lane, dst + lane, dst + lane,
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
                                            kp.alpha_mode, 1, above[RL::CRB], above[RL::COSB], alpha_y,
@@ -1117,7 +1118,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
             if (it + 1 < je) {
                 border_traces<P, MODAL>(smem + SM::HB, next_tile, smem + SM::HL, smem + SM::E0, smem + SM::HR,
                                         lane);
-                // every lane computes the same face (uniform control flow, identical stores)
+                // one face for the whole strip: lane 0 alone (the other lanes would
+                // repeat it -- ~9% of the stage's FP64 lane work, i.e. power)
+                if (lane == 0)
                 face_flux_call<P>(SM::HL, SM::E0, SM::F0T,
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
                                            kp.alpha_mode, 0, 0.0, 0.0, alpha_x, kp.bdy});
@@ -1165,6 +1168,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
                 // the h warp has the lightest volume work: it takes the x-faces 1..32
                 // (right face of every lane; the last valid lane's neighbour is the halo)
                 const bool last = lane == nvalid - 1;
+                if (owned)   // padding lanes' faces are never read
                 face_flux_call<P>(SM::XRT + lane, SM::XL + (last ? kLanes : min(lane + 1, kLanes - 1)), SM::FX + lane + 1,
                                   FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r,
                                            kp.alpha_mode, 0, 0.0, 0.0, alpha_x, kp.bdy});
