@@ -249,6 +249,7 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
     ctx->rc = c.row_chunk > 0 ? c.row_chunk : 0;
     if (const char *env = getenv("DGSWE_ROW_CHUNK")) ctx->rc = atoi(env);
     if (const char *env = getenv("DGSWE_CHUNKS")) ctx->even_chunks = atoi(env);
+    if (const char *env = getenv("DGSWE_NO_LO")) ctx->no_lo = atoi(env);
     if (const char *env = getenv("DGSWE_SMEM_PAD")) ctx->smem_pad = atoi(env);
 
     // nodal tables (dgswe_params.h NodTab) from the Legendre ones, in long

@@ -83,6 +83,8 @@ struct dgswe_ctx {
     int sms = 148;
     int smem_pad = 0;             // experiment knob: extra dynamic smem per CTA
     int even_chunks = 0;          // experiment knob (DGSWE_CHUNKS): fixed chunk count, even split
+    int occ_lo[2] = {};           // resident CTAs per SM of the low-order kernel (without / with u^n)
+    int no_lo = 0;                // experiment knob (DGSWE_NO_LO): p <= 1 on the main kernel
     int occ[32] = {};             // resident CTAs per SM of each stage-kernel variant (0: not queried)
     // fused halo exchange (bands.py transport "fused"): set by dgswe_set_exchange
     long long peer_zstride[2] = {0, 0};

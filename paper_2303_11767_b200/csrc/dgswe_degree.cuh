@@ -11,6 +11,7 @@
 
 #include "dgswe_ctx.h"
 #include "dgswe_kernels.cuh"
+#include "dgswe_lo.cuh"
 
 namespace dgswe_deg {
 
@@ -110,9 +111,46 @@ ChunkPlan chunk_plan(const dgswe_ctx *c, int rows, int o)
     return plan;
 }
 
+// Low-order degrees (p <= 1), nodal stages: the barrier-free kernel of
+// dgswe_lo.cuh, four strips per CTA, evenly split row chunks filling one
+// wave of resident CTAs (or several waves of ~8-row chunks on wide grids).
+template <int P, int F>
+int launch_lo(dgswe_ctx *c, const StageParams &kp0, cudaStream_t s)
+{
+    int &o = c->occ_lo[F & 1];
+    if (!o) {
+        int q = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, dgswe::lo_stage_kernel<P, F>,
+                                                               dgswe::kLoWarps * dgswe::kLanes, 0));
+        o = q > 0 ? q : 1;
+    }
+    StageParams kp = kp0;
+    const int rows = kp.j_end - kp.j_begin;
+    const long long cols = (long long)((c->nstrip + dgswe::kLoWarps - 1) / dgswe::kLoWarps) * c->cfg.nz;
+    const long long slots = (long long)c->sms * o;
+    long long nch = slots / cols;                        // one full wave
+    if (nch < 1) nch = (rows + 7) / 8;                   // wide grids: ~8-row chunks, several waves
+    if (c->even_chunks > 0) nch = c->even_chunks;
+    if (nch > rows) nch = rows;
+    if (kp.rc > 0) {                                     // explicit rows per chunk (row_chunk)
+        nch = (rows + kp.rc - 1) / kp.rc;
+        kp.even = 0;
+    } else {
+        kp.even = (int)nch;
+    }
+    const dim3 grid((c->nstrip + dgswe::kLoWarps - 1) / dgswe::kLoWarps, (unsigned)nch, c->cfg.nz);
+    dgswe::lo_stage_kernel<P, F><<<grid, dgswe::kLoWarps * dgswe::kLanes, 0, s>>>(kp);
+    CUDA_TRY(cudaGetLastError());
+    c->launches += 1;
+    return DGSWE_OK;
+}
+
 template <int P, int F>
 int launch_variant(dgswe_ctx *c, const StageParams &kp0, cudaStream_t s)
 {
+    if constexpr (dgswe::lo_kernel_degree<P>() && (F & ~dgswe::kHasU) == 0) {
+        if (!c->no_lo && kp0.j_end2 <= kp0.j_begin2) return launch_lo<P, F>(c, kp0, s);
+    }
     const int o = occupancy<P, F>(c);
     if (o < 0) return o;
     StageParams kp = kp0;

@@ -392,26 +392,17 @@ struct FaceArgs {
 // register array crosses the call.  (Three inlined copies cost ~1k SASS
 // instructions of a kernel whose speed tracks its instruction-cache
 // footprint; sF may alias the "out" traces.)
+// The flux arithmetic of one face from register traces (h, normal and
+// tangential momentum on the "in" / "out" side) into fh / fn / ft: shared
+// by the shared-memory face routine below and the low-order kernel
+// (dgswe_lo.cuh), so both give identical bits.
 template <int P>
-__device__ __forceinline__ void face_flux_body(int in, int out, int dst, FaceArgs fa)
+__device__ __forceinline__ void face_core(const double (&hI)[P + 1], const double (&nI)[P + 1],
+                                          const double (&tI)[P + 1], const double (&hO)[P + 1],
+                                          const double (&nO)[P + 1], const double (&tO)[P + 1], const FaceArgs &fa,
+                                          double (&fh)[P + 1], double (&fn)[P + 1], double (&ft)[P + 1])
 {
     constexpr int N = P + 1;
-    constexpr int LD = Smem<P>::LD;
-    extern __shared__ double smem[];
-    // variables by role: h, the normal momentum (hu across an x-face, hv
-    // across a y-face) and the tangential one, addressed through the
-    // runtime direction instead of per-node selects
-    const int vn = 1 + fa.dir, vt = 2 - fa.dir;
-    double hI[N], nI[N], tI[N], hO[N], nO[N], tO[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-        hI[k] = smem[in + k * LD];
-        nI[k] = smem[in + (vn * N + k) * LD];
-        tI[k] = smem[in + (vt * N + k) * LD];
-        hO[k] = smem[out + k * LD];
-        nO[k] = smem[out + (vn * N + k) * LD];
-        tO[k] = smem[out + (vt * N + k) * LD];
-    }
     double rin[N], rout[N];
     double am[N];
 #pragma unroll
@@ -435,10 +426,43 @@ __device__ __forceinline__ void face_flux_body(int in, int out, int dst, FaceArg
         const double gi = hI[k] * hI[k] * fa.half_g, go = hO[k] * hO[k] * fa.half_g;
         const double wi = nI[k] * rin[k], wo = nO[k] * rout[k];
         const double fni = fma(nI[k], wi, gi), fno = fma(nO[k], wo, go);   // normal: m w + g h^2/2
-        const double fti = tI[k] * wi, fto = tO[k] * wo;                   // tangential: m_t w
-        smem[dst + k * LD] = fma(hs, nI[k] + nO[k], -ha * (hO[k] - hI[k]));
-        smem[dst + (vn * N + k) * LD] = fma(hs, fni + fno, -ha * (nO[k] - nI[k]));
-        smem[dst + (vt * N + k) * LD] = fma(hs, fti + fto, -ha * (tO[k] - tI[k]));
+        // tangential: m_t w on both sides, summed with an explicit fma (a plain
+        // a*b + c*d lets the compiler pick which product it fuses, which can
+        // differ between inlining contexts: one rounding apart)
+        const double ft_sum = fma(tI[k], wi, tO[k] * wo);
+        fh[k] = fma(hs, nI[k] + nO[k], -ha * (hO[k] - hI[k]));
+        fn[k] = fma(hs, fni + fno, -ha * (nO[k] - nI[k]));
+        ft[k] = fma(hs, ft_sum, -ha * (tO[k] - tI[k]));
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void face_flux_body(int in, int out, int dst, FaceArgs fa)
+{
+    constexpr int N = P + 1;
+    constexpr int LD = Smem<P>::LD;
+    extern __shared__ double smem[];
+    // variables by role: h, the normal momentum (hu across an x-face, hv
+    // across a y-face) and the tangential one, addressed through the
+    // runtime direction instead of per-node selects
+    const int vn = 1 + fa.dir, vt = 2 - fa.dir;
+    double hI[N], nI[N], tI[N], hO[N], nO[N], tO[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        hI[k] = smem[in + k * LD];
+        nI[k] = smem[in + (vn * N + k) * LD];
+        tI[k] = smem[in + (vt * N + k) * LD];
+        hO[k] = smem[out + k * LD];
+        nO[k] = smem[out + (vn * N + k) * LD];
+        tO[k] = smem[out + (vt * N + k) * LD];
+    }
+    double fh[N], fn[N], ft[N];
+    face_core<P>(hI, nI, tI, hO, nO, tO, fa, fh, fn, ft);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        smem[dst + k * LD] = fh[k];
+        smem[dst + (vn * N + k) * LD] = fn[k];
+        smem[dst + (vt * N + k) * LD] = ft[k];
     }
 }
 
@@ -498,7 +522,7 @@ struct RowRegs {
 // momentum sources gain h * B (B = this equation's orography factor at the
 // node, the warp's staged tile sB: -(g/R) db/dlambda resp. -(g cos/R)
 // db/dtheta, determ folded in).
-template <int P, int KIND, bool OROG, typename RT>
+template <int P, int KIND, bool OROG, typename RT, int STRIDE = kLanes>
 __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU, const RT &row, int lane,
                                              const StageParams &kp, const double *sB, double (&F)[P + 1],
                                              double (&G)[P + 1], double (&S)[P + 1])
@@ -508,15 +532,15 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
 #pragma unroll
     for (int qj = 0; qj < N; ++qj) {
         const int q = qi * N + qj;
-        const double hu = sU[(1 * NP + q) * kLanes + lane];
-        const double hv = sU[(2 * NP + q) * kLanes + lane];
+        const double hu = sU[(1 * NP + q) * STRIDE + lane];
+        const double hv = sU[(2 * NP + q) * STRIDE + lane];
         const double crc = row.crc(qj);
         if constexpr (KIND == 0) {
             F[qj] = hu;
             G[qj] = hv * crc;
             S[qj] = 0.0;
         } else {
-            const double h = sU[(0 * NP + q) * kLanes + lane];
+            const double h = sU[(0 * NP + q) * STRIDE + lane];
             // 1/max(h, floor) as rcp(h) + select: the reciprocal starts at once
             const double r = ge_pos(h, kp.h_floor) ? rcp64(h) : kp.inv_floor;
             const double gh2 = h * h * kp.half_g;
@@ -536,7 +560,7 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
                 G[qj] = fma(is_v ? hv : hu, w, is_v ? gh2 : 0.0) * crc;
                 S[qj] = fma(is_v ? -gh2 : 0.0, srs, t * (is_v ? -hu : hv));
             }
-            if constexpr (OROG) S[qj] = fma(h, sB[q * kLanes + lane], S[qj]);
+            if constexpr (OROG) S[qj] = fma(h, sB[q * STRIDE + lane], S[qj]);
         }
     }
 }
@@ -548,7 +572,7 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
 // common 1/(determ cos_j) is applied in finalize.  Node row i (fixed xi
 // node) is evaluated at once: its G/S terms land in acc[i][.], its F
 // scatters into every acc[.][j].
-template <int P, bool MOM, bool OROG>
+template <int P, bool MOM, bool OROG, int STRIDE = kLanes>
 __device__ __forceinline__ void volume(double (&acc)[P + 1][P + 1], int v, const double *sU,
                                        const double *row, int lane, const StageParams &kp, const double *sB)
 {
@@ -556,7 +580,7 @@ __device__ __forceinline__ void volume(double (&acc)[P + 1][P + 1], int v, const
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         double F[N], G[N], S[N];
-        node_physics<P, MOM ? 3 : 0, OROG>(v == 2, i, sU, RowRef<P>{row}, lane, kp, sB, F, G, S);
+        node_physics<P, MOM ? 3 : 0, OROG, RowRef<P>, STRIDE>(v == 2, i, sU, RowRef<P>{row}, lane, kp, sB, F, G, S);
 #pragma unroll
         for (int j = 0; j < N; ++j) {
             double e = MOM ? S[j] : 0.0;

@@ -538,3 +538,26 @@ def test_host_state_step_pipelined(P, case, nx, ny, p, nz, chunks):
     for _ in range(3):
         op.ssprk3_steps(st, dt, 1)
     assert torch.equal(host, st.data.cpu())
+
+
+@pytest.mark.parametrize("p", [0, 1])
+@pytest.mark.parametrize("nx", [31, 32, 33, 64, 97])
+def test_low_order_kernel_bitwise(P, p, nx, monkeypatch):
+    """p <= 1 nodal stages run on the barrier-free low-order kernel
+    (csrc/dgswe_lo.cuh); it must give the main kernel's bits: same traces,
+    face arithmetic, volume and stage combination, different data path
+    (partial strips, strip borders, poles, check_mean)."""
+    ny = 12
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=nx, ny=ny, p=p))
+    out = []
+    for no_lo in ("1", "0"):
+        monkeypatch.setenv("DGSWE_NO_LO", no_lo)
+        op = P.SpatialOperator(setup.mesh, p, setup.model)
+        st = op.project_state(setup.ic)
+        op.ssprk3_steps(st, 20.0, 3, check_mean=True)
+        op.rk_steps(st, 20.0, 2, order=2)
+        op.rk_steps(st, 20.0, 1, order=1)
+        flags, _ = op.status()
+        assert flags == 0
+        out.append(st.to_numpy())
+    assert np.array_equal(out[0], out[1])
