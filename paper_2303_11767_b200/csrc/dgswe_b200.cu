@@ -116,6 +116,7 @@ int launch_stage(dgswe_ctx *c, const StageCall &sc, cudaStream_t s)
     kp.check_mean = sc.check_mean;
     kp.modal = sc.modal ? 1 : 0;
     kp.orog = c->orog;
+    kp.orog_mask = c->orog_mask;
     kp.orog_rstride = 2 * c->vstride;
     if (sc.edge) {
         kp.edge = 1;
@@ -311,6 +312,7 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
     // Stored per buffer row as the nodal factors B (determ folded in, like
     // the row table's source factors): S_hu += h B_x, S_hv += h B_y.
     std::vector<double> ob;
+    std::vector<unsigned char> om;   // per (row, strip): 1 if the orography tile is non-zero
     if (t->orog) {
         long double D[dgswe::kMaxP + 1][dgswe::kMaxP + 1];   // D[i][k] = l_k'(x_i)
         for (int i = 0; i < n; ++i)
@@ -344,6 +346,16 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
                     }
             }
         }
+        // which (row, strip) tiles have a non-zero factor: the others are
+        // neither copied nor used (an isolated mountain covers a few % of
+        // the sphere; h * 0 adds nothing, so skipping is exact)
+        om.assign((size_t)c.nrows * ctx->nstrip, 0);
+        for (int r = 0; r < c.nrows; ++r)
+            for (int st = 0; st < ctx->nstrip; ++st) {
+                const size_t o = (size_t)r * 2 * ctx->vstride + (size_t)st * np * DGSWE_STRIP;
+                for (int q = 0; q < np * DGSWE_STRIP && !om[(size_t)r * ctx->nstrip + st]; ++q)
+                    if (ob[o + q] != 0.0 || ob[o + ctx->vstride + q] != 0.0) om[(size_t)r * ctx->nstrip + st] = 1;
+            }
     }
 
     // diagnostics scratch, sized once: mass (ny*nphi + 2ny + 2), l2 with a
@@ -361,7 +373,8 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
               cudaMalloc(&ctx->status, sizeof(DevStatus)) == cudaSuccess &&
               cudaMalloc(&ctx->diag, ctx->diag_doubles * sizeof(double)) == cudaSuccess &&
               cudaMallocHost(&ctx->status_host, 2 * sizeof(DevStatus)) == cudaSuccess &&
-              (ob.empty() || cudaMalloc(&ctx->orog, ob.size() * sizeof(double)) == cudaSuccess);
+              (ob.empty() || cudaMalloc(&ctx->orog, ob.size() * sizeof(double)) == cudaSuccess) &&
+              (om.empty() || cudaMalloc(&ctx->orog_mask, om.size()) == cudaSuccess);
     if (ok) {
         ctx->status_host[1] = kStatus0;   // the reset value, copied from pinned memory
         ok = cudaMemcpy(ctx->rowtab, rt.data(), rt.size() * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess &&
@@ -370,7 +383,8 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
              cudaMemset(ctx->alpha, 0, 2 * sizeof(double)) == cudaSuccess &&
              cudaMemcpy(ctx->status, &kStatus0, sizeof kStatus0, cudaMemcpyHostToDevice) == cudaSuccess &&
              (ob.empty() ||
-              cudaMemcpy(ctx->orog, ob.data(), ob.size() * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess);
+              cudaMemcpy(ctx->orog, ob.data(), ob.size() * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess) &&
+             (om.empty() || cudaMemcpy(ctx->orog_mask, om.data(), om.size(), cudaMemcpyHostToDevice) == cudaSuccess);
     }
     if (!ok) {
         cudaError_t le = cudaGetLastError();
@@ -391,6 +405,7 @@ void dgswe_destroy(dgswe_ctx *ctx)
     cudaFree(ctx->status);
     cudaFree(ctx->diag);
     cudaFree(ctx->orog);
+    cudaFree(ctx->orog_mask);
     if (ctx->status_host) cudaFreeHost(ctx->status_host);
     delete ctx;
 }

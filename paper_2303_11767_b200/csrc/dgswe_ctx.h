@@ -77,6 +77,7 @@ struct dgswe_ctx {
     DevStatus *status = nullptr;  // device
     DevStatus *status_host = nullptr;   // pinned host [2]: last read, reset value
     double *orog = nullptr;       // device [nrows][2][nstrip][nphi][32] orography factors, or null
+    unsigned char *orog_mask = nullptr;   // device [nrows][nstrip]: 1 where a strip's factor tile is non-zero
     int external_alpha = 0;
     long long launches = 0;
     int device = 0;

@@ -560,7 +560,9 @@ __device__ __forceinline__ void node_physics(bool is_v, int qi, const double *sU
                 G[qj] = fma(is_v ? hv : hu, w, is_v ? gh2 : 0.0) * crc;
                 S[qj] = fma(is_v ? -gh2 : 0.0, srs, t * (is_v ? -hu : hv));
             }
-            if constexpr (OROG) S[qj] = fma(h, sB[q * STRIDE + lane], S[qj]);
+            if constexpr (OROG) {
+                if (sB) S[qj] = fma(h, sB[q * STRIDE + lane], S[qj]);   // null: an all-zero tile
+            }
         }
     }
 }
@@ -1007,10 +1009,17 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
     const bool chk = (v == 0) && !face_warp;
 
     // the row tile (and orography tile) of local row r into ring slot `slot`
-    auto issue_row = [&](int slot, int r) {
+    // orography: whether ring slot 0 / 1 holds a (non-zero) factor tile; the
+    // mask byte of a row is read two rows ahead by every lane, so neither the
+    // copy nor the volume waits on it
+    bool ob_on0 = false, ob_on1 = false;
+    auto ob_mask = [&](int r) {
+        return OROG && v > 0 && !face_warp && kp.orog_mask[(size_t)r * kp.nstrip + strip] != 0;
+    };
+    auto issue_row = [&](int slot, int r, bool ob) {
         double *dst = ring0 + slot * SM::TILE;
         if constexpr (OROG) {
-            if (v > 0) {
+            if (ob) {
                 tma_row2(dst, Xz + (size_t)r * kp.rstride, sOB + slot * 2 * NP * kLanes,
                          Oz + (size_t)r * kp.orog_rstride, kTileBytes, mbar + slot * 3 + v);
                 return;
@@ -1026,12 +1035,16 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
     // each variable warp's elected lane initialises its own two ring
     // mbarriers and starts streaming rows jb, jb+1 at once: the copies are
     // in flight while the row tables and the row below the chunk load
+    if constexpr (OROG) {
+        ob_on0 = ob_mask(jb);
+        ob_on1 = jb + 1 <= last_fetch && ob_mask(jb + 1);
+    }
     if (!face_warp && lane == 0) {
         mbar_init(mbar + v, 1);
         mbar_init(mbar + 3 + v, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        issue_row(0, jb);
-        if (jb + 1 <= last_fetch) issue_row(1, jb + 1);
+        issue_row(0, jb, ob_on0);
+        if (jb + 1 <= last_fetch) issue_row(1, jb + 1, ob_on1);
     }
 
     // row-table ring: slot (r - jb) % 3 holds local row r (rows jb, jb+1 now,
@@ -1166,6 +1179,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
             const double *row = sRow + (k % 3) * RL::SSTRIDE;
             TSTAMP(s);
 
+            const bool ob2 = OROG && jl + 2 <= last_fetch && ob_mask(jl + 2);
             // warm L2 for this row's u^n and for row jl+2 (copied in after finalize)
             if (lane == 0) {
                 if (HAS_U) prefetch_l2_bulk(Uz - lane + (size_t)jl * kp.rstride, kTileBytes);
@@ -1198,7 +1212,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
                                            kp.alpha_mode, 0, 0.0, 0.0, alpha_x, kp.bdy});
             }
             double vol[N][N];
-            const double *sB = OROG ? sOB + slot * 2 * NP * kLanes : nullptr;
+            const double *sB = OROG && (slot ? ob_on1 : ob_on0) ? sOB + slot * 2 * NP * kLanes : nullptr;
             if constexpr (vol_rolled<P>()) {
                 double *sE = smem + SM::E + v * NP * kLanes;
                 if (v == 0)
@@ -1242,7 +1256,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
             __syncwarp();
             if (lane == 0 && jl + 2 <= last_fetch) {
                 fence_proxy_async();
-                issue_row(slot, jl + 2);
+                issue_row(slot, jl + 2, ob2);
+            }
+            if constexpr (OROG) {
+                if (slot) ob_on1 = ob2; else ob_on0 = ob2;
             }
             TSTAMP(5);
             TACC(0, tk0 - tks);   // phase A work (eval)

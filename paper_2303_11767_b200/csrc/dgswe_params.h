@@ -67,6 +67,7 @@ struct StageParams {
     // factors -(g/R) db/dlambda and -(g cos/R) db/dtheta with determ folded in
     const double *orog;
     long long orog_rstride;             // doubles per row of `orog` (2 * vstride / 3)
+    const unsigned char *orog_mask;     // [nrows][nstrip]: 0 = the row's factor tile is all zero
 };
 
 constexpr int kStatusBits = 4;          // POSITIVITY, NONFINITE, MEAN_NONPOS, PEER_TIMEOUT
