@@ -41,6 +41,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "dgswe_params.h"
 
 namespace dgswe {
@@ -64,8 +66,18 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 // local terms through shared memory) for p >= 2.
 template <int P>
 __host__ __device__ constexpr int min_blocks() { return P <= 3 ? 4 : 2; }
+// per variant: the orography tiles' shared memory leaves room for 3 CTAs at
+// p = 3 (so 168 registers, no spills); p = 6 fits one CTA per SM
+template <int P, int F>
+__host__ __device__ constexpr int min_blocks_f() { return P == 3 && (F & kOrog) ? 3 : P >= 6 ? 1 : min_blocks<P>(); }
 template <int P>
 __host__ __device__ constexpr bool vol_rolled() { return P >= 2; }
+// u^n loaded into registers before barrier 2 (in flight during the wait) up
+// to p = 5 except with RK4's second output (its addend needs those
+// registers: it spilled); at p = 6 the 49 doubles next to the 49
+// accumulators would.  Otherwise finalize loads u^n before its first store.
+template <int P, int F>
+__host__ __device__ constexpr bool early_u() { return P <= 5 && (F & kHasY2) == 0; }
 
 
 // DG_TIMING builds record per-role phase durations (clock cycles) of every
@@ -615,7 +627,10 @@ __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v
     for (int ii = 0; ii < N; ++ii)
 #pragma unroll
         for (int j = 0; j < N; ++j) acc[ii][j] = 0.0;
-    const RowRegs<P> rr(row);   // the row's physics factors in registers across the loop
+    // the row's physics factors in registers across the loop (p = 6: read
+    // from the shared row table, their 42 registers would spill)
+    using RowT = typename std::conditional<(P >= 6), RowRef<P>, RowRegs<P>>::type;
+    const RowT rr{row};
 #pragma unroll 1
     for (int i = 0; i < N; ++i) {
         double F[N], G[N], S[N];
@@ -643,18 +658,28 @@ __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v
 // (node stride 32 doubles: immediate offsets).  MODAL: U, A, Y, Y2 hold
 // modal coefficients; the nodal parts b X + g K and g2 K are converted to
 // modes in registers before the u^n / accumulator terms are added.
-template <int P, bool HAS_U, bool HAS_Y2, bool MODAL>
+template <int P, bool HAS_U, bool HAS_Y2, bool MODAL, bool EARLY_U>
 __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const double *cur,
                                              const double *Av, double *Y2v, int v,
                                              const double *sFX,
                                              const double *sFtop, const double *sFbot,
                                              const double *row, int lane, bool owned,
                                              double *Yv, const StageParams &kp, double *Ypeer,
-                                             double *Ypeer2, const double (&un_in)[P + 1][P + 1])
+                                             double *Ypeer2, const double (&un_in)[P + 1][P + 1],
+                                             const double *Uv)
 {
     constexpr int N = P + 1;
     using RL = RowLayout<P>;
-    const double (&un)[N][N] = un_in;  // u^n, loaded by the caller before barrier 2 (U may alias Y)
+    // u^n: loaded by the caller before barrier 2 (early_u), else all of it
+    // here, before the first store (U may alias Y)
+    double unl[EARLY_U ? 1 : N][EARLY_U ? 1 : N];
+    if constexpr (HAS_U && !EARLY_U) {
+#pragma unroll
+        for (int a = 0; a < N; ++a)
+#pragma unroll
+            for (int b = 0; b < N; ++b) unl[a][b] = Uv[(a * N + b) * kLanes];
+    }
+#define UN(a, b) (EARLY_U ? un_in[a][b] : unl[EARLY_U ? 0 : (a)][EARLY_U ? 0 : (b)])
     double an[HAS_Y2 ? N : 1][HAS_Y2 ? N : 1];
     if constexpr (HAS_Y2) {            // second output's addend (may alias Y2)
 #pragma unroll
@@ -715,7 +740,7 @@ __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const 
 #pragma unroll
             for (int j = 0; j < N; ++j) {
                 double y = acc[i][j];
-                if (HAS_U) y = fma(kp.a, un[i][j], y);
+                if (HAS_U) y = fma(kp.a, UN(i, j), y);
                 if (owned) Yv[(i * N + j) * kLanes] = y;
                 acc[i][j] = y;
             }
@@ -728,7 +753,7 @@ __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const 
             for (int i = 0; i < N; ++i) {
                 const double k = acc[i][j];
                 double y = fma(kp.b, cur[(i * N + j) * kLanes + lane], gr * k);
-                if (HAS_U) y = fma(kp.a, un[i][j], y);
+                if (HAS_U) y = fma(kp.a, UN(i, j), y);
                 if (owned) Yv[(i * N + j) * kLanes] = y;
                 if (owned && Ypeer) Ypeer[(i * N + j) * kLanes] = y;   // fused halo exchange (NVLink store)
                 if (owned && Ypeer2) Ypeer2[(i * N + j) * kLanes] = y;
@@ -740,6 +765,7 @@ __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const 
             }
         }
     }
+#undef UN
     unsigned bad = 0;
     if (owned) {
         if (kp.check_finite) {   // Inf or NaN: max exponent field of the outputs (integer pipe)
@@ -906,7 +932,7 @@ __device__ __forceinline__ int even_start(int c, int rows, int n)
 }
 
 template <int P, int F>
-__global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageParams kp)
+__global__ void __launch_bounds__(kThreads, (min_blocks_f<P, F>())) stage_kernel(StageParams kp)
 {
     constexpr bool HAS_U = (F & kHasU) != 0;
     constexpr bool HAS_Y2 = (F & kHasY2) != 0;
@@ -1229,7 +1255,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
             }
             TSTAMP(3);
             double unr[N][N];                          // u^n loads in flight across barrier 2
-            if constexpr (HAS_U) {
+            if constexpr (HAS_U && early_u<P, F>()) {
                 const double *Uv = Uz + (size_t)jl * kp.rstride;
 #pragma unroll
                 for (int a = 0; a < N; ++a)
@@ -1249,9 +1275,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks<P>()) stage_kernel(StageP
                 if (jl == kp.band_hi - 1 && kp.peer_row[1])
                     Ypeer2 = kp.peer_row[1] + (size_t)blockIdx.z * kp.peer_zstride[1] + off;
             }
-            bad |= finalize<P, HAS_U, HAS_Y2, MODAL>(vol, cur, HAS_Y2 ? Az + roff : nullptr, HAS_Y2 ? Y2z + roff : nullptr,
+            bad |= finalize<P, HAS_U, HAS_Y2, MODAL, early_u<P, F>()>(vol, cur, HAS_Y2 ? Az + roff : nullptr, HAS_Y2 ? Y2z + roff : nullptr,
                                                      v, sFX, sFa, sFb, row, lane,
-                                                     owned, Yz + roff, kp, Ypeer, Ypeer2, unr);
+                                                     owned, Yz + roff, kp, Ypeer, Ypeer2, unr,
+                                                     HAS_U ? Uz + roff : nullptr);
             // X(jl) is consumed: stream row jl+2 into its slot (L2-warm by now)
             __syncwarp();
             if (lane == 0 && jl + 2 <= last_fetch) {
