@@ -25,3 +25,4 @@ from .stepping import (ButcherTableau, DivergenceError, StepLog, TimeControls,  
 from .williamson import (CASE_IDS, CaseConfig, RunSetup, build_case, default_config,  # noqa: F401
                          ic_williamson_tc2, ic_williamson_tc5, ic_williamson_tc6, tc5_bottom, tc6_fields)
 from .operator import RusanovParams, SpatialOperator, State  # noqa: F401
+from .tracing import LaunchRegion, set_op_recorder  # noqa: F401

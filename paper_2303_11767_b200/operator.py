@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, tracing
 from .geometry import (Mesh, build_vander, gauss_legendre, node_latitudes, project_initial,
                        sphere_row_mass_matrices)
 from .physics import PositivityError, SphereSWEModel
@@ -395,6 +395,7 @@ class SpatialOperator:
         c = self._ctx
         _lib.check(c.lib.dgswe_rhs(c.h, _ptr(state.data), _ptr(out.data), c.stream()), "dgswe_rhs")
         self.timers.end("main")
+        self._record("rhs", "dgswe_rhs", 16.0)
         if check:
             flags, _ = c.status(reset=True)
             self.raise_on_status(flags)
@@ -406,12 +407,14 @@ class SpatialOperator:
         _lib.check(c.lib.dgswe_stage(c.h, float(a), _ptr(U.data if U is not None else None),
                                      float(b), _ptr(X.data), float(g), _ptr(Y.data), int(tag),
                                      c.stream()), "dgswe_stage")
+        self._record("stage", "dgswe_stage", 24.0 if U is not None and a != 0.0 else 16.0)
 
     def axpy(self, coef: float, x: State, y: State, check_finite: bool = False, tag: int = 0):
         """y += x*coef with the reference's two roundings (timestep.py:137-141)."""
         c = self._ctx
         _lib.check(c.lib.dgswe_axpy(c.h, float(coef), _ptr(x.data), _ptr(y.data),
                                     int(check_finite), int(tag), c.stream()), "dgswe_axpy")
+        self._record("axpy", "dgswe_axpy", 24.0, flops=2.0)
 
     def rk_steps(self, state: State, dt: float, nsteps: int, order: int = 3, check_mean: bool = False):
         """nsteps fused steps of tableau(order) (1..4) in place, one CUDA graph:
@@ -429,6 +432,10 @@ class SpatialOperator:
         _lib.check(c.lib.dgswe_rk_steps(c.h, int(order), _ptr(state.data), _ptr(ws[0]), _ptr(ws[1]),
                                         _ptr(ws[2]), float(dt), int(nsteps), int(check_mean), c.stream()),
                    "dgswe_rk_steps")
+        # stage bytes per step: Euler 16, Heun 16 + 24, SSPRK3 16 + 24 + 24, RK4 (accumulator) 32 + 40 + 40 + 24
+        per_step = {1: 16.0, 2: 40.0, 3: 64.0, 4: 136.0}[int(order)]
+        self._record("rk_steps", f"dgswe_rk_steps(order={int(order)})", per_step * nsteps,
+                     flops=tracing.stage_flops_per_dof(self.p) * int(order) * nsteps)
 
     def ssprk3_steps(self, state: State, dt: float, nsteps: int, check_mean: bool = False):
         """nsteps fused Shu-Osher SSPRK3 steps in place (one CUDA graph)."""
@@ -629,6 +636,13 @@ class SpatialOperator:
 
     def status_tags(self, reset: bool = True):
         return self._ctx.status_tags(reset)
+
+    def _record(self, kind: str, op: str, bytes_per_dof: float, flops: float | None = None):
+        """One op-recorder entry (tracing.set_op_recorder) for a launch over all rows."""
+        if tracing.get_op_recorder() is not None:
+            rgn = tracing.LaunchRegion((self.mesh.nx, self.mesh.ny, self.nz), self.p)
+            tracing.record(kind, op, rgn, bytes_per_dof,
+                           tracing.stage_flops_per_dof(self.p) if flops is None else flops)
 
     def launch_count(self) -> int:
         return self._ctx.launches() + self._replayed

@@ -137,3 +137,30 @@ def test_rusanov_params():
     with pytest.raises(ValueError):
         P.RusanovParams("bogus")
     assert P.RusanovParams().mode == "local"
+
+
+def test_op_recorder_hook():
+    """set_op_recorder (fields.py:66-76) mirror: entries carry the launch
+    region, analytic flops and algorithmic bytes; None clears the hook."""
+    import paper_2303_11767_b200 as P
+    from paper_2303_11767_b200 import tracing
+
+    class Rec:
+        def __init__(self):
+            self.rows = []
+
+        def record(self, kind, op, rgn, flops, nbytes):
+            self.rows.append((kind, op, rgn, flops, nbytes))
+
+    rec = Rec()
+    P.set_op_recorder(rec)
+    try:
+        rgn = tracing.LaunchRegion((720, 360, 1), 3)
+        tracing.record("stage", "dgswe_stage", rgn, 24.0, tracing.stage_flops_per_dof(3))
+    finally:
+        P.set_op_recorder(None)
+    tracing.record("stage", "ignored", rgn, 16.0, 1.0)      # no recorder: nothing happens
+    assert len(rec.rows) == 1
+    kind, op, r, flops, nbytes = rec.rows[0]
+    assert (kind, op) == ("stage", "dgswe_stage") and r.dofs == 720 * 360 * 48
+    assert nbytes == 24 * r.dofs and flops > 20 * r.dofs
