@@ -613,7 +613,7 @@ __device__ __forceinline__ void volume(double (&acc)[P + 1][P + 1], int v, const
 
 // Same terms with the loop over node rows kept rolled (a quarter of the
 // code): the row-local G/S terms of row i go to shared memory sE (this
-// warp's [NP][32] block) and are added in finalize; F still scatters into
+// warp's [NP][32] block) and are added at the end; F still scatters into
 // the register tile through the i-th column of Dx.  Every variable warp
 // forms its own row-local term (the h warp's: G = hv cos/R); the momentum
 // warps' physics is the longest phase-B work, so nothing moves onto them.
@@ -649,6 +649,14 @@ __device__ __forceinline__ void volume_rolled(double (&acc)[P + 1][P + 1], int v
             for (int j = 0; j < N; ++j) acc[ii][j] = fma(d, F[j], acc[ii][j]);
         }
     }
+    // the row-local terms are this warp's own: add them now, before barrier
+    // 2, so finalize starts on the faces (their shared-memory latency is
+    // spent while the warp would wait at the barrier anyway; every lane
+    // reads only its own column)
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j < N; ++j) acc[i][j] += sE[(i * N + j) * kLanes + lane];
 }
 
 // Boundary lifts, diagonal mass, stage combination and store for variable v.
@@ -686,13 +694,6 @@ __device__ __forceinline__ unsigned finalize(double (&acc)[P + 1][P + 1], const 
         for (int a = 0; a < N; ++a)
 #pragma unroll
             for (int b = 0; b < N; ++b) an[a][b] = Av[(a * N + b) * kLanes];
-    }
-    if constexpr (vol_rolled<P>()) {
-        const double *sE = smem_base() + Smem<P>::E + v * N * N * kLanes;
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-            for (int j = 0; j < N; ++j) acc[i][j] += sE[(i * N + j) * kLanes + lane];
     }
     constexpr int LD = Smem<P>::LD;
     const int o = (v * N) * LD;        // x-face column c: left face of lane c
