@@ -66,10 +66,21 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 // local terms through shared memory) for p >= 2.
 template <int P>
 __host__ __device__ constexpr int min_blocks() { return P <= 3 ? 4 : 2; }
-// per variant: the orography tiles' shared memory leaves room for 3 CTAs at
-// p = 3 (so 168 registers, no spills); p = 6 fits one CTA per SM
+// per variant: the plain nodal stages (the SSPRK3 path) at p = 1 / 2 fit 6 /
+// 5 CTAs at 80 / 96 registers without spills (+9% / +1.8%; the modal, band
+// and orography variants would spill there); at p = 3 the orography and
+// RK4-accumulator variants run 3 CTAs at 168 registers (the orography
+// tiles' shared memory leaves no room for a fourth; RK4's second output
+// spilled at 128); p = 6 fits one CTA per SM
 template <int P, int F>
-__host__ __device__ constexpr int min_blocks_f() { return P == 3 && (F & kOrog) ? 3 : P >= 6 ? 1 : min_blocks<P>(); }
+__host__ __device__ constexpr int min_blocks_f()
+{
+    return (F & ~kHasU) == 0 && P == 1   ? 6
+           : (F & ~kHasU) == 0 && P == 2 ? 5
+           : P == 3 && (F & (kOrog | kHasY2)) ? 3
+           : P >= 6                      ? 1
+                                         : min_blocks<P>();
+}
 template <int P>
 __host__ __device__ constexpr bool vol_rolled() { return P >= 2; }
 // u^n loaded into registers before barrier 2 (in flight during the wait) up
