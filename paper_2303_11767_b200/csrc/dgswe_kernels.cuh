@@ -30,8 +30,10 @@
 // of the fused halo exchange, modal in/out states (the reference's own
 // coefficients: every tile is converted to the Gauss nodes in shared memory
 // as it lands and the output back to modes in registers -- the single-launch
-// form of assemble_rhs / rk_step) and the orography source of Williamson
-// TC5 (-g h grad b, not in the reference: SPEC.md:157).
+// form of assemble_rhs and the modal stage entry points) and the orography
+// source of Williamson TC5 (-g h grad b, not in the reference: SPEC.md:157).
+// At p = 0 the plain nodal stages run on the barrier-free kernel of
+// dgswe_lo.cuh instead (same arithmetic, identical bits).
 //
 // Floating point: FMA contraction, refined MUFU reciprocals and a different
 // summation order than the reference; results agree with the reference's
