@@ -85,7 +85,7 @@
 extern "C" {
 #endif
 
-#define DGSWE_ABI_VERSION 4
+#define DGSWE_ABI_VERSION 5
 #define DGSWE_STRIP 32          /* longitude elements per strip block */
 
 /* status bits (dgswe_status) */
@@ -119,6 +119,9 @@ typedef struct dgswe_cfg {
     int alpha_mode;           /* DGSWE_ALPHA_* */
     double alpha;             /* pinned alpha for DGSWE_ALPHA_GLOBAL_PINNED */
     int row_chunk;            /* latitude rows per CTA, 0 = automatic */
+    int periodic_y;           /* 1: y-periodic planar mesh (mesh.py:120-132): rows wrap, no pole
+                                 faces; the lat-lon tables then describe the plane (cos = 1,
+                                 sin = 0, f = const, radius = 1).  Single band only. */
 } dgswe_cfg;
 
 /* Host tables; copied during dgswe_create, not retained. */

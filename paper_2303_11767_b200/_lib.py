@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdgswe_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "dgswe_b200.h")
 
-ABI_VERSION = 4            # DGSWE_ABI_VERSION
+ABI_VERSION = 5            # DGSWE_ABI_VERSION
 STRIP = 32                 # DGSWE_STRIP: longitude elements per strip block
 STATUS_POSITIVITY = 0x1
 STATUS_NONFINITE = 0x2
@@ -35,7 +35,7 @@ class Cfg(ctypes.Structure):
         ("nx", _I), ("ny", _I), ("nz", _I), ("p", _I),
         ("row0", _I), ("nrows", _I), ("jlo", _I), ("jhi", _I),
         ("radius", _D), ("gravity", _D), ("h_floor", _D), ("dx", _D), ("dy", _D),
-        ("alpha_mode", _I), ("alpha", _D), ("row_chunk", _I),
+        ("alpha_mode", _I), ("alpha", _D), ("row_chunk", _I), ("periodic_y", _I),
     ]
 
 

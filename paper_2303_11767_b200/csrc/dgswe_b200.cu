@@ -117,6 +117,7 @@ int launch_stage(dgswe_ctx *c, const StageCall &sc, cudaStream_t s)
     kp.modal = sc.modal ? 1 : 0;
     kp.orog = c->orog;
     kp.orog_mask = c->orog_mask;
+    kp.periodic_y = c->cfg.periodic_y;
     kp.orog_rstride = 2 * c->vstride;
     if (sc.edge) {
         kp.edge = 1;
@@ -220,6 +221,8 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
     if (!t->leg || !t->dleg || !t->weights || !t->cos_r_int || !t->sin_r_int || !t->fcos_int ||
         !t->cos_r_edge || !t->cos_edge || !t->minv)
         return dgswe_fail(DGSWE_EINVAL, "missing table");
+    if (c.periodic_y && (c.row0 != 0 || c.nrows != c.ny || c.jlo != 0 || c.jhi != c.ny || t->orog))
+        return dgswe_fail(DGSWE_EINVAL, "a y-periodic mesh runs as one band without orography");
 
     dgswe_ctx *ctx = new (std::nothrow) dgswe_ctx();
     if (!ctx) return dgswe_fail(DGSWE_ENOMEM, "out of host memory");

@@ -1056,7 +1056,12 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_f<P, F>())) stage_kernel
     auto ob_mask = [&](int r) {
         return OROG && v > 0 && !face_warp && kp.orog_mask[(size_t)r * kp.nstrip + strip] != 0;
     };
-    auto issue_row = [&](int slot, int r, bool ob) {
+    // a y-periodic (planar) mesh wraps its rows: local row r is stored at
+    // (r + ny) % ny (single-band contexts only; the host checks)
+    const bool yper = kp.periodic_y != 0;
+    auto wrap = [&](int r) { return yper ? (r + kp.ny) % kp.ny : r; };
+    auto issue_row = [&](int slot, int r_, bool ob) {
+        const int r = wrap(r_);
         double *dst = ring0 + slot * SM::TILE;
         if constexpr (OROG) {
             if (ob) {
@@ -1069,7 +1074,8 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_f<P, F>())) stage_kernel
     };
 
     // rows whose coefficients exist: local r with global row0+r in [0, ny)
-    const int r_last = min(kp.nrows - 1, kp.ny - 1 - kp.row0);
+    // (every row, wrapped, on a y-periodic mesh: no pole)
+    const int r_last = yper ? je : min(kp.nrows - 1, kp.ny - 1 - kp.row0);
     const int last_fetch = min(je, r_last);        // rows jb..last_fetch stream through the ring
 
     // each variable warp's elected lane initialises its own two ring
@@ -1091,16 +1097,16 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_f<P, F>())) stage_kernel
     // row jl+2 staged by the face warp during iteration jl)
     const int gfirst = kp.row0 + jb;
     {
-        const int nload = min(2, kp.ny - gfirst);
+        const int nload = yper ? 2 : min(2, kp.ny - gfirst);
         for (int idx = threadIdx.x; idx < nload * RL::SSTRIDE; idx += kThreads) {
             const int r = idx / RL::SSTRIDE;
-            sRow[idx] = kp.rowtab[(size_t)(gfirst + r) * RL::STRIDE + (idx - r * RL::SSTRIDE)];
+            sRow[idx] = kp.rowtab[(size_t)wrap(gfirst + r) * RL::STRIDE + (idx - r * RL::SSTRIDE)];
         }
     }
     // top traces of the row below the chunk (its first row's bottom face)
-    const bool below = gfirst > 0;
+    const bool below = yper || gfirst > 0;
     if (below && !face_warp) {
-        const double *src = Xz + (size_t)(jb - 1) * kp.rstride + lane;
+        const double *src = Xz + (size_t)wrap(jb - 1) * kp.rstride + lane;
         double c[N][N];
 #pragma unroll
         for (int a = 0; a < N; ++a)
@@ -1158,9 +1164,9 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_f<P, F>())) stage_kernel
                 if (it + 1 < je)
                     fetch_neighbours<P>(kp.X + (size_t)blockIdx.z * kp.zstride + (size_t)(it + 1) * kp.rstride,
                                         eL, eR, smem + SM::HB, lane, kp.vstride);
-                if (it + 2 <= je && kp.row0 + it + 2 < kp.ny) {
+                if (it + 2 <= je && (yper || kp.row0 + it + 2 < kp.ny)) {
                     double *dst = sRow + ((k + 2) % 3) * RL::SSTRIDE;
-                    const double *src = kp.rowtab + (size_t)(kp.row0 + it + 2) * RL::STRIDE;
+                    const double *src = kp.rowtab + (size_t)wrap(kp.row0 + it + 2) * RL::STRIDE;
                     for (int idx = lane; idx < RL::SSTRIDE; idx += kLanes) cp_async8(dst + idx, src + idx);
                 }
                 cp_commit();
@@ -1223,7 +1229,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks_f<P, F>())) stage_kernel
             // warm L2 for this row's u^n and for row jl+2 (copied in after finalize)
             if (lane == 0) {
                 if (HAS_U) prefetch_l2_bulk(Uz - lane + (size_t)jl * kp.rstride, kTileBytes);
-                if (jl + 2 <= last_fetch) prefetch_l2_bulk(Xz + (size_t)(jl + 2) * kp.rstride, kTileBytes);
+                if (jl + 2 <= last_fetch) prefetch_l2_bulk(Xz + (size_t)wrap(jl + 2) * kp.rstride, kTileBytes);
             }
             {
                 double c[N][N];

@@ -68,6 +68,7 @@ struct StageParams {
     const double *orog;
     long long orog_rstride;             // doubles per row of `orog` (2 * vstride / 3)
     const unsigned char *orog_mask;     // [nrows][nstrip]: 0 = the row's factor tile is all zero
+    int periodic_y;                     // 1: y-periodic (planar) mesh, rows wrap, no poles
 };
 
 constexpr int kStatusBits = 4;          // POSITIVITY, NONFINITE, MEAN_NONPOS, PEER_TIMEOUT

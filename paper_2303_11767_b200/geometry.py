@@ -9,8 +9,10 @@ uploaded to the device by :mod:`.operator`; tables are bit-identical to the
 reference's (tests/test_host_setup.py pins them against the golden
 fixtures), so the device sees exactly the reference's constants.
 
-Only the spherical (lat-lon) geometry named by the north star is provided;
-planar meshes are out of scope.
+The lat-lon sphere is the north star's geometry; the doubly periodic
+planar mesh of the reference's f-plane case (mesh.py:120-132,
+basis.py:152-156) runs on the same kernels with cos = 1, sin = 0, R = 1
+and wrapped rows.
 """
 
 from __future__ import annotations
@@ -115,9 +117,22 @@ def build_latlon_mesh(nx: int, ny: int, radius: float = EARTH.radius) -> Mesh:
                 float(radius), False)
 
 
+def build_planar_mesh(nx: int, ny: int, length: float) -> Mesh:
+    """Uniform periodic mesh of the square [0, length]^2 (mesh.py:120-132)."""
+    if nx < 1 or ny < 1:
+        raise ValueError("element counts must be at least 1")
+    if length <= 0:
+        raise ValueError("domain length must be positive")
+    return Mesh("planar", int(nx), int(ny), np.linspace(0.0, length, nx + 1),
+                np.linspace(0.0, length, ny + 1), None, True)
+
+
 def min_effective_diameter(mesh: Mesh) -> float:
     """min over rows of R*dtheta and R*cos(theta_far)*dlambda, the far
-    latitude replaced by the near one on pole rows (mesh.py:155-174)."""
+    latitude replaced by the near one on pole rows (mesh.py:155-174);
+    min(dx, dy) on the plane."""
+    if mesh.kind == "planar":
+        return min(mesh.dx, mesh.dy)
     R = mesh.radius
     best = math.inf
     for j in range(mesh.ny):
@@ -242,6 +257,23 @@ def mass_matrix_sphere(p: int, theta_bounds, quad: Quadrature, dlam: float) -> M
     return MassMatrix(M, np.linalg.inv(M))
 
 
+def mass_matrix_planar(p: int, determ: float) -> MassMatrix:
+    """Diagonal mass matrix of the orthogonal tensor Legendre basis
+    (basis.py:152-156)."""
+    norms = np.array([2.0 / (2 * a + 1) for a in range(p + 1)])
+    diag = determ * np.outer(norms, norms).reshape(-1)
+    return MassMatrix(np.diag(diag), np.diag(1.0 / diag))
+
+
+def row_mass_matrices(p: int, mesh: Mesh, quad: Quadrature):
+    """(ny, nphi, nphi) mass matrices and inverses of every row: the
+    cos-weighted ones on the sphere, the planar diagonal one repeated."""
+    if mesh.kind == "planar":
+        m = mass_matrix_planar(p, mesh.determ)
+        return np.stack([m.M] * mesh.ny), np.stack([m.Minv] * mesh.ny)
+    return sphere_row_mass_matrices(p, mesh, quad)
+
+
 def sphere_row_mass_matrices(p: int, mesh: Mesh, quad: Quadrature):
     """(ny, nphi, nphi) mass matrices and inverses, one per latitude row."""
     out = [mass_matrix_sphere(p, (mesh.y_edges[j], mesh.y_edges[j + 1]), quad, mesh.dx)
@@ -259,12 +291,17 @@ def element_node_coords(mesh: Mesh, nodes: np.ndarray):
 
 
 def project_initial(f, mesh: Mesh, vander: Vander) -> np.ndarray:
-    """cos-weighted L2 projection of f(lambda, theta): (nx, ny, nphi)."""
+    """cos-weighted L2 projection of f(lambda, theta): (nx, ny, nphi); on
+    the plane the unweighted one against the diagonal mass (basis.py:206-233)."""
     n = vander.n_1d
     lam, th = element_node_coords(mesh, vander.nodes)
     vals = np.broadcast_to(f(lam[:, None, :, None], th[None, :, None, :]),
                            (mesh.nx, mesh.ny, n, n)).reshape(mesh.nx, mesh.ny, n * n)
     w2 = np.outer(vander.w_edge, vander.w_edge).reshape(-1)
+    if mesh.kind == "planar":
+        rhs = mesh.determ * np.einsum("xyq,q,qm->xym", vals, w2, vander.phi)
+        mm = mass_matrix_planar(vander.p, mesh.determ)
+        return np.ascontiguousarray(rhs * (1.0 / np.diag(mm.M))[None, None, :])
     w_rows = (w2.reshape(n, n)[None, :, :] * np.cos(th)[:, None, :]).reshape(mesh.ny, n * n)
     moments = mesh.determ * np.einsum("xyq,yq,qm->xym", vals, w_rows, vander.phi)
     _, Minv = sphere_row_mass_matrices(vander.p, mesh, gauss_legendre(n))

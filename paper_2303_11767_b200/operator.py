@@ -26,7 +26,7 @@ import torch
 
 from . import _lib, tracing
 from .geometry import (Mesh, build_vander, gauss_legendre, node_latitudes, project_initial,
-                       sphere_row_mass_matrices)
+                       row_mass_matrices)
 from .physics import PositivityError, SphereSWEModel
 
 VAR_NAMES = ("h", "hu", "hv")
@@ -188,16 +188,30 @@ class _Context:
         nrows = ny if nrows is None else nrows
         jlo = 0 if jlo is None else jlo
         jhi = nrows if jhi is None else jhi
-        const = model.constants
-        th = node_latitudes(mesh, quad.nodes)                 # (ny, n)
-        R = const.radius
-        arrs = {
-            "leg": vander.leg, "dleg": vander.dleg, "weights": quad.weights,
-            "cos_r_int": np.cos(th) / R, "sin_r_int": np.sin(th) / R,
-            "fcos_int": 2.0 * const.omega * np.sin(th) * np.cos(th),
-            "cos_r_edge": np.cos(mesh.y_edges) / R, "cos_edge": np.cos(mesh.y_edges),
-            "minv": Minv,
-        }
+        n = quad.nodes.shape[0]
+        if mesh.kind == "planar":
+            # the plane as the lat-lon operator with cos = 1, sin = 0, R = 1:
+            # F, G and the mass unweighted, the source f (hv, -hu)
+            # (models.py:176-227), rows wrapping instead of poles
+            R = 1.0
+            arrs = {
+                "leg": vander.leg, "dleg": vander.dleg, "weights": quad.weights,
+                "cos_r_int": np.ones((ny, n)), "sin_r_int": np.zeros((ny, n)),
+                "fcos_int": np.full((ny, n), model.coriolis_f),
+                "cos_r_edge": np.ones(ny + 1), "cos_edge": np.ones(ny + 1),
+                "minv": Minv,
+            }
+        else:
+            const = model.constants
+            th = node_latitudes(mesh, quad.nodes)                 # (ny, n)
+            R = const.radius
+            arrs = {
+                "leg": vander.leg, "dleg": vander.dleg, "weights": quad.weights,
+                "cos_r_int": np.cos(th) / R, "sin_r_int": np.sin(th) / R,
+                "fcos_int": 2.0 * const.omega * np.sin(th) * np.cos(th),
+                "cos_r_edge": np.cos(mesh.y_edges) / R, "cos_edge": np.cos(mesh.y_edges),
+                "minv": Minv,
+            }
         if bottom is not None:
             arrs["orog"] = bottom                             # (ny, nx, n*n) b at the Gauss nodes
         keep = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in arrs.items()}
@@ -212,7 +226,7 @@ class _Context:
         cfg = _lib.Cfg(nx=mesh.nx, ny=ny, nz=nz, p=p, row0=row0, nrows=nrows, jlo=jlo, jhi=jhi,
                        radius=R, gravity=model.gravity, h_floor=model.h_floor,
                        dx=mesh.dx, dy=mesh.dy, alpha_mode=mode, alpha=alpha,
-                       row_chunk=int(row_chunk))
+                       row_chunk=int(row_chunk), periodic_y=int(mesh.kind == "planar"))
         handle = ctypes.c_void_p()
         _lib.check(lib.dgswe_create(ctypes.byref(cfg), ctypes.byref(tabs), ctypes.byref(handle)),
                    "dgswe_create")
@@ -282,8 +296,9 @@ class SpatialOperator:
 
     def __init__(self, mesh: Mesh, p: int, model: SphereSWEModel, rusanov: RusanovParams | None = None,
                  nz: int = 1, timers=None, device=None, row_chunk: int = 0):
-        if not getattr(model, "is_spherical", False) or mesh.kind != "latlon":
-            raise ValueError("model/mesh geometry mismatch (only the lat-lon sphere is supported)")
+        if bool(getattr(model, "is_spherical", False)) != (mesh.kind == "latlon") or \
+                mesh.kind not in ("latlon", "planar"):
+            raise ValueError("model/mesh geometry mismatch (lat-lon sphere or periodic plane)")
         if not torch.cuda.is_available():
             raise RuntimeError("SpatialOperator needs a CUDA device (no CPU fallback)")
         self.mesh, self.p, self.model = mesh, int(p), model
@@ -296,8 +311,8 @@ class SpatialOperator:
         self.vander = build_vander(self.p, self.quad)
         self.nphi, self.n1, self.nq = self.vander.nphi, self.vander.n_1d, self.vander.n_q
         self.halo_shape = (mesh.nx + 2, mesh.ny + 2, self.nz)
-        self.M_rows, self.Minv_rows = sphere_row_mass_matrices(self.p, mesh, self.quad)
-        self.M_planar = None
+        self.M_rows, self.Minv_rows = row_mass_matrices(self.p, mesh, self.quad)
+        self.M_planar = self.M_rows[0] if mesh.kind == "planar" else None
         self.bottom_nodal = self._bottom_at_nodes()
         with torch.cuda.device(self.device):
             self._ctx = _Context(mesh, self.p, model, self.rusanov, self.nz, self.quad, self.vander,
@@ -364,7 +379,8 @@ class SpatialOperator:
         f = torch.stack([reference_nodal(ic_funcs.get(name, zero), lam, th, self.device)
                          for name in VAR_NAMES])               # (3, ny, nx, n*n)
         out = self.zero_state()
-        cosn = np.ascontiguousarray(np.cos(th), dtype=np.float64)
+        cosn = np.ascontiguousarray(np.ones_like(th) if self.mesh.kind == "planar" else np.cos(th),
+                                    dtype=np.float64)
         c = self._ctx
         _lib.check(c.lib.dgswe_project(c.h, _ptr(f), cosn.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                        float(self.mesh.determ), _ptr(out.data), c.stream()),

@@ -79,3 +79,43 @@ class SphereSWEModel:
 def swe_sphere_model(constants: PhysicalConstants, h_ref: float = 1.0, bottom=None) -> SphereSWEModel:
     """models.py:293-295; ``bottom`` (extension) is the orography b(lambda, theta)."""
     return SphereSWEModel(constants, h_ref, bottom)
+
+
+class PlanarSWEModel:
+    """Shallow water on the doubly periodic plane with an f-plane Coriolis
+    source (models.py:176-227): the lat-lon operator with cos = 1, sin = 0
+    and R = 1 -- the row tables the kernels read carry exactly that
+    (operator.py) -- and rows that wrap instead of poles."""
+
+    n_vars = 3
+    var_names = ("h", "hu", "hv")
+    has_source = True
+    is_spherical = False
+    bottom = None
+
+    def __init__(self, gravity: float, coriolis_f: float, h_ref: float = 1.0):
+        if gravity <= 0:
+            raise ValueError("gravity must be positive")
+        self.gravity = float(gravity)
+        self.coriolis_f = float(coriolis_f)
+        self.h_floor = 1e-8 * float(h_ref)
+
+    def wavespeed_nodes(self, U, coords, direction):
+        h = U["h"]
+        mom = U["hu"] if direction == X_DIR else U["hv"]
+        vel = mom / np.maximum(h, self.h_floor)
+        return np.abs(vel) + np.sqrt(self.gravity * np.maximum(h, 0.0))
+
+    def alpha_nodes(self, U, coords, direction):
+        return self.wavespeed_nodes(U, coords, direction)
+
+    def max_wavespeed(self, U, coords, direction) -> float:
+        return float(np.max(self.wavespeed_nodes(U, coords, direction)))
+
+    def max_physical_speed(self, U, coords=None) -> float:
+        return max(self.max_wavespeed(U, coords, X_DIR), self.max_wavespeed(U, coords, Y_DIR))
+
+
+def swe_planar_model(gravity: float, coriolis_f: float, h_ref: float = 1.0) -> PlanarSWEModel:
+    """Planar shallow water with constant Coriolis parameter f (models.py:288-290)."""
+    return PlanarSWEModel(gravity, coriolis_f, h_ref)

@@ -4,8 +4,10 @@ API of /root/reference/pkg/src/dgswe/cases.py (``CaseConfig``,
 ``default_config``, ``build_case``, ``RunSetup``, ``ic_williamson_tc2``,
 ``ic_williamson_tc6``) for the two spherical cases of the reference.
 Williamson et al. (1992) equations: TC2 (90)-(95) with alpha = 0,
-TC6 (142)-(149).  The planar cases (advection, geostrophic adjustment) are
-outside the spherical hot path and raise NotImplementedError.
+TC6 (142)-(149).  The planar f-plane case (geostrophic adjustment,
+cases.py:113-123) runs on the same kernels (y-periodic plane); the scalar
+advection case (a one-variable model, cases.py:99-110) is outside the
+shallow-water hot path and raises NotImplementedError.
 Williamson TC5 (flow over an isolated mountain) is an extension: the
 reference has no orography; its bottom topography enters the
 model's momentum sources (physics.py) and the oracle restates the same
@@ -19,12 +21,19 @@ from dataclasses import dataclass, replace
 
 import numpy as np
 
-from .geometry import EARTH, PhysicalConstants, build_latlon_mesh
-from .physics import swe_sphere_model
+from .geometry import EARTH, PhysicalConstants, build_latlon_mesh, build_planar_mesh
+from .physics import swe_planar_model, swe_sphere_model
 
 DAY = 86400.0
 TC2_U0 = 2.0 * math.pi * EARTH.radius / (12.0 * DAY)
 TC2_GH0 = 2.94e4
+# geostrophic adjustment on the f-plane (cases.py:58-63)
+ADJ_LENGTH = 1.0e7          # m
+ADJ_H0 = 1000.0             # m
+ADJ_H1 = 5.0                # m
+ADJ_SIGMA = ADJ_LENGTH / 20.0
+ADJ_F = 1.0e-4              # s^-1
+
 TC6_OMEGA = 7.848e-6
 TC6_K = 7.848e-6
 TC6_H0 = 8.0e3
@@ -174,6 +183,17 @@ class RunSetup:
     constants: PhysicalConstants = EARTH
 
 
+def ic_geostrophic_adjustment():
+    """Gaussian height bump at rest on the f-plane (cases.py:113-123)."""
+
+    def h0(x, y):
+        r2 = (x - ADJ_LENGTH / 2) ** 2 + (y - ADJ_LENGTH / 2) ** 2
+        return ADJ_H0 + ADJ_H1 * np.exp(-r2 / (2.0 * ADJ_SIGMA ** 2))
+
+    zero = lambda x, y: np.zeros(np.broadcast(x, y).shape)   # noqa: E731
+    return {"h": h0, "hu": zero, "hv": zero}
+
+
 def build_case(config: CaseConfig, constants: PhysicalConstants = EARTH) -> RunSetup:
     case = config.case
     if case == "williamson_tc2":
@@ -191,6 +211,10 @@ def build_case(config: CaseConfig, constants: PhysicalConstants = EARTH) -> RunS
         model = swe_sphere_model(constants, h_ref=TC5_H0, bottom=tc5_bottom)
         return RunSetup(config, build_latlon_mesh(config.nx, config.ny, constants.radius), model,
                         ic_williamson_tc5(constants), None, constants)
+    if case == "geostrophic_adjustment":
+        model = swe_planar_model(constants.gravity, ADJ_F, h_ref=ADJ_H0)
+        return RunSetup(config, build_planar_mesh(config.nx, config.ny, ADJ_LENGTH), model,
+                        ic_geostrophic_adjustment(), None, constants)
     if case in CASE_IDS:
-        raise NotImplementedError(f"{case!r} is a planar case, outside the spherical hot path")
+        raise NotImplementedError(f"{case!r}: scalar advection is outside the shallow-water hot path")
     raise ValueError(f"unknown case {case!r}; choose from {CASE_IDS}")

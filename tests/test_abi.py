@@ -32,7 +32,7 @@ def test_exports_every_declared_symbol():
 
 def test_abi_version_and_error_string():
     lib = _lib.load()
-    assert lib.dgswe_abi_version() == _lib.ABI_VERSION == 4
+    assert lib.dgswe_abi_version() == _lib.ABI_VERSION == 5
     assert isinstance(lib.dgswe_last_error(), bytes)
 
 
