@@ -143,6 +143,23 @@ typedef struct dgswe_tables {
 
 typedef struct dgswe_ctx dgswe_ctx;
 
+/* Linear advection u_t + beta . grad u = 0 on the doubly periodic plane
+ * (the reference's advection model and advection_sine case, models.py:114-140,
+ * cases.py:99-110): one fused stage kernel, Y = a U + b X + g RHS(X), on
+ * modal coefficients laid out [nz][ny][nphi][nx].  RHS(X) = stage(0, NULL,
+ * 0, X, 1, Y).  Y must not alias X. */
+typedef struct dgswe_adv_cfg {
+    int nx, ny, nz, p;
+    double dx, dy;            /* element extents (mesh.py:66-72) */
+    double beta_x, beta_y;    /* advection velocity (models.py:117-121) */
+} dgswe_adv_cfg;
+typedef struct dgswe_adv_ctx dgswe_adv_ctx;
+int dgswe_adv_create(const dgswe_adv_cfg *cfg, const double *leg, const double *dleg, const double *weights,
+                     dgswe_adv_ctx **out);
+int dgswe_adv_stage(dgswe_adv_ctx *ctx, double a, const double *U, double b, const double *X, double g, double *Y,
+                    void *stream);
+void dgswe_adv_destroy(dgswe_adv_ctx *ctx);
+
 int dgswe_abi_version(void);
 const char *dgswe_last_error(void);
 

@@ -25,7 +25,8 @@ from .monitors import (convergence_rate, l2_error, l2_error_host, mass_integral,
 from .stepping import (ButcherTableau, DivergenceError, StepLog, TimeControls,  # noqa: F401
                        integrate, rk_step, tableau)
 from .williamson import (CASE_IDS, CaseConfig, RunSetup, build_case, default_config,  # noqa: F401
-                         ic_geostrophic_adjustment, ic_williamson_tc2, ic_williamson_tc5, ic_williamson_tc6,
+                         ic_advection_sine, ic_geostrophic_adjustment, ic_williamson_tc2, ic_williamson_tc5, ic_williamson_tc6,
                          tc5_bottom, tc6_fields)
 from .operator import RusanovParams, SpatialOperator, State  # noqa: F401
+from .advection import AdvectionModel, AdvectionOperator, AdvState, advection_model  # noqa: F401
 from .tracing import LaunchRegion, set_op_recorder  # noqa: F401

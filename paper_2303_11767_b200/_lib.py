@@ -39,6 +39,11 @@ class Cfg(ctypes.Structure):
     ]
 
 
+class AdvCfg(ctypes.Structure):
+    _fields_ = [("nx", _I), ("ny", _I), ("nz", _I), ("p", _I), ("dx", _D), ("dy", _D),
+                ("beta_x", _D), ("beta_y", _D)]
+
+
 class Tables(ctypes.Structure):
     _fields_ = [(name, _PD) for name in (
         "leg", "dleg", "weights", "cos_r_int", "sin_r_int", "fcos_int",
@@ -51,6 +56,9 @@ SIGNATURES = {
     "dgswe_last_error": (ctypes.c_char_p, []),
     "dgswe_create": (_I, [ctypes.POINTER(Cfg), ctypes.POINTER(Tables), ctypes.POINTER(_VP)]),
     "dgswe_destroy": (None, [_VP]),
+    "dgswe_adv_create": (_I, [ctypes.POINTER(AdvCfg), _PD, _PD, _PD, ctypes.POINTER(_VP)]),
+    "dgswe_adv_stage": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _VP]),
+    "dgswe_adv_destroy": (None, [_VP]),
     "dgswe_state_elems": (ctypes.c_int64, [_VP]),
     "dgswe_rhs": (_I, [_VP, _VP, _VP, _VP]),
     "dgswe_set_basis": (_I, [_VP, _I]),

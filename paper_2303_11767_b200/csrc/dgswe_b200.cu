@@ -49,6 +49,34 @@ __global__ void axpy_kernel(const double *__restrict__ x, double *__restrict__ y
     }
 }
 
+// nodal tables (dgswe_params.h NodTab) of degree n-1 from the reference's
+// Legendre tables, in long double: l_i(x) = sum_a (2a+1)/2 w_i P_a(x_i) P_a(x)
+// (the Gauss rule projects the degree-p Lagrange polynomial exactly)
+dgswe::NodTab nodal_tables(const double *leg, const double *dleg, const double *weights, int n)
+{
+    dgswe::NodTab nt;
+    memset(&nt, 0, sizeof nt);
+    for (int i = 0; i < n; ++i) {
+        const long double wi = weights[i];
+        long double lm = 0.0L;
+        for (int a = 0; a < n; ++a) lm += 0.5L * (2 * a + 1) * wi * leg[a * n + i] * ((a & 1) ? -1.0L : 1.0L);
+        nt.lm[i] = (double)lm;
+        nt.mu[i] = (double)(lm / wi);
+        nt.w[i] = (double)wi;
+        for (int k = 0; k < n; ++k) {
+            long double d = 0.0L;   // w_k l_i'(x_k) / w_i
+            for (int a = 0; a < n; ++a)
+                d += 0.5L * (2 * a + 1) * (long double)leg[a * n + i] * weights[k] * dleg[a * n + k];
+            nt.dh[i][k] = (double)d;
+        }
+        for (int a = 0; a < n; ++a) {
+            nt.leg[a][i] = leg[a * n + i];
+            nt.wp[a][i] = weights[i] * leg[a * n + i];
+        }
+    }
+    return nt;
+}
+
 constexpr DevStatus kStatus0 = {0u, {INT_MAX, INT_MAX, INT_MAX, INT_MAX}};
 
 bool misaligned(const void *p) { return ((uintptr_t)p & 15u) != 0; }
@@ -256,30 +284,7 @@ int dgswe_create(const dgswe_cfg *cfg, const dgswe_tables *t, dgswe_ctx **out)
     if (const char *env = getenv("DGSWE_NO_LO")) ctx->no_lo = atoi(env);
     if (const char *env = getenv("DGSWE_SMEM_PAD")) ctx->smem_pad = atoi(env);
 
-    // nodal tables (dgswe_params.h NodTab) from the Legendre ones, in long
-    // double: l_i(x) = sum_a (2a+1)/2 w_i P_a(x_i) P_a(x) (the Gauss rule
-    // projects the degree-p Lagrange polynomial exactly)
-    dgswe::NodTab nt;
-    memset(&nt, 0, sizeof nt);
-    for (int i = 0; i < n; ++i) {
-        const long double wi = t->weights[i];
-        long double lm = 0.0L;
-        for (int a = 0; a < n; ++a)
-            lm += 0.5L * (2 * a + 1) * wi * t->leg[a * n + i] * ((a & 1) ? -1.0L : 1.0L);
-        nt.lm[i] = (double)lm;
-        nt.mu[i] = (double)(lm / wi);
-        nt.w[i] = (double)wi;
-        for (int k = 0; k < n; ++k) {
-            long double d = 0.0L;   // w_k l_i'(x_k) / w_i
-            for (int a = 0; a < n; ++a)
-                d += 0.5L * (2 * a + 1) * (long double)t->leg[a * n + i] * t->weights[k] * t->dleg[a * n + k];
-            nt.dh[i][k] = (double)d;
-        }
-        for (int a = 0; a < n; ++a) {
-            nt.leg[a][i] = t->leg[a * n + i];
-            nt.wp[a][i] = t->weights[i] * t->leg[a * n + i];
-        }
-    }
+    const dgswe::NodTab nt = nodal_tables(t->leg, t->dleg, t->weights, n);
     int rc = ctx->ops->upload(nt);
     if (rc) {
         delete ctx;
@@ -724,6 +729,67 @@ int dgswe_status_tags(dgswe_ctx *ctx, uint32_t *flags, int32_t *tags, int reset,
     if (tags)
         for (int b = 0; b < dgswe::kStatusBits; ++b) tags[b] = h->first_tag[b];
     return DGSWE_OK;
+}
+
+// -- linear advection on the periodic plane (dgswe_adv.cuh) ---------------
+
+struct dgswe_adv_ctx {
+    dgswe_adv_cfg cfg;
+    dgswe::AdvParams ap;
+    const DegreeOps *ops;
+};
+
+int dgswe_adv_create(const dgswe_adv_cfg *cfg, const double *leg, const double *dleg, const double *weights,
+                     dgswe_adv_ctx **out)
+{
+    if (!cfg || !leg || !dleg || !weights || !out) return dgswe_fail(DGSWE_EINVAL, "null argument");
+    *out = nullptr;
+    const dgswe_adv_cfg &c = *cfg;
+    if (c.p < 0 || c.p > dgswe::kMaxP) return dgswe_fail(DGSWE_EUNSUPPORTED, "degree %d outside 0..%d", c.p, dgswe::kMaxP);
+    if (c.nx < 1 || c.ny < 1 || c.nz < 1 || !(c.dx > 0) || !(c.dy > 0) || !std::isfinite(c.beta_x) ||
+        !std::isfinite(c.beta_y))
+        return dgswe_fail(DGSWE_EINVAL, "bad advection configuration");
+    const int n = c.p + 1;
+    const DegreeOps *ops = dgswe_degree_ops(c.p);
+    const int rc = ops->upload(nodal_tables(leg, dleg, weights, n));
+    if (rc) return rc;
+    dgswe_adv_ctx *ctx = new (std::nothrow) dgswe_adv_ctx();
+    if (!ctx) return dgswe_fail(DGSWE_ENOMEM, "out of host memory");
+    ctx->cfg = c;
+    ctx->ops = ops;
+    dgswe::AdvParams &ap = ctx->ap;
+    // mesh scalars as the reference forms them (mesh.py:66-84, dg.py:199-213)
+    const double determ = c.dx * c.dy / 4.0;
+    ap.nx = c.nx;
+    ap.ny = c.ny;
+    ap.zstride = (long long)c.nx * c.ny * n * n;
+    ap.bx = c.beta_x;
+    ap.by = c.beta_y;
+    ap.bdx = c.dx / 2.0;
+    ap.bdy = c.dy / 2.0;
+    ap.cx = determ / ap.bdx;
+    ap.cy = determ / ap.bdy;
+    ap.inv_determ = 1.0 / determ;
+    *out = ctx;
+    return DGSWE_OK;
+}
+
+void dgswe_adv_destroy(dgswe_adv_ctx *ctx) { delete ctx; }
+
+int dgswe_adv_stage(dgswe_adv_ctx *ctx, double a, const double *U, double b, const double *X, double g, double *Y,
+                    void *stream)
+{
+    if (!ctx || !X || !Y) return dgswe_fail(DGSWE_EINVAL, "null argument");
+    if (X == Y) return dgswe_fail(DGSWE_EINVAL, "the output must not alias the stage input");
+    if (a != 0.0 && !U) return dgswe_fail(DGSWE_EINVAL, "U is required when a != 0");
+    dgswe::AdvParams ap = ctx->ap;
+    ap.X = X;
+    ap.U = a != 0.0 ? U : nullptr;
+    ap.Y = Y;
+    ap.a = a;
+    ap.b = b;
+    ap.g = g;
+    return ctx->ops->adv_stage(ap, ctx->cfg.nz, (cudaStream_t)stream);
 }
 
 int dgswe_status(dgswe_ctx *ctx, uint32_t *flags, int32_t *first_tag, int reset, void *stream)

@@ -63,6 +63,8 @@ struct DegreeOps {
     int (*convert)(dgswe_ctx *c, const double *in, double *out, bool to_nodal, int r0, int r1, cudaStream_t s);
     int (*alpha)(dgswe_ctx *c, const double *X, bool modal, cudaStream_t s);
     int (*project)(dgswe_ctx *c, const double *f, const double *cosn, double determ, double *Y, cudaStream_t s);
+    // linear advection on the periodic plane (dgswe_adv.cuh)
+    int (*adv_stage)(const dgswe::AdvParams &ap, int nz, cudaStream_t s);
 };
 const DegreeOps *dgswe_degree_ops(int p);
 

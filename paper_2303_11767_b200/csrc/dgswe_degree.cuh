@@ -12,6 +12,7 @@
 #include "dgswe_ctx.h"
 #include "dgswe_kernels.cuh"
 #include "dgswe_lo.cuh"
+#include "dgswe_adv.cuh"
 
 namespace dgswe_deg {
 
@@ -111,7 +112,7 @@ ChunkPlan chunk_plan(const dgswe_ctx *c, int rows, int o)
     return plan;
 }
 
-// Low-order degrees (p <= 1), nodal stages: the barrier-free kernel of
+// The low-order degree (p = 0), plain nodal stages: the barrier-free kernel of
 // dgswe_lo.cuh, four strips per CTA, evenly split row chunks filling one
 // wave of resident CTAs (or several waves of ~8-row chunks on wide grids).
 template <int P, int F>
@@ -217,6 +218,15 @@ int stage(dgswe_ctx *c, const StageParams &kp, cudaStream_t s)
 }
 
 template <int P>
+int adv_stage(const dgswe::AdvParams &ap, int nz, cudaStream_t s)
+{
+    const dim3 grid((ap.nx + 127) / 128, ap.ny, nz);
+    dgswe::adv_stage_kernel<P><<<grid, 128, 0, s>>>(ap);
+    CUDA_TRY(cudaGetLastError());
+    return DGSWE_OK;
+}
+
+template <int P>
 int convert(dgswe_ctx *c, const double *in, double *out, bool to_nodal, int r0, int r1, cudaStream_t s)
 {
     if (r1 <= r0) return DGSWE_OK;
@@ -284,6 +294,6 @@ int project(dgswe_ctx *c, const double *f, const double *cosn, double determ, do
     {                                                                                            \
         static const DegreeOps ops = {dgswe_deg::upload<P>, dgswe_deg::stage<P>,                 \
                                       dgswe_deg::convert<P>, dgswe_deg::alpha<P>,                \
-                                      dgswe_deg::project<P>};                                    \
+                                      dgswe_deg::project<P>, dgswe_deg::adv_stage<P>};           \
         return &ops;                                                                             \
     }

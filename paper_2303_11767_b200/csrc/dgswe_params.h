@@ -114,6 +114,20 @@ struct NodTab {
     double leg[kMaxP + 1][kMaxP + 1];
     double wp[kMaxP + 1][kMaxP + 1];
 };
+// one stage of the linear advection kernel (dgswe_adv.cuh): Y = a U + b X
+// + g RHS(X), states [nz][ny][nphi][nx] of modal coefficients
+struct AdvParams {
+    const double *X, *U;
+    double *Y;
+    double a, b, g;
+    int nx, ny;
+    long long zstride;                 // nx * ny * nphi
+    double bx, by;                     // advection velocity
+    double bdx, bdy;                   // face Jacobians dx/2, dy/2
+    double cx, cy;                     // determ / bd_det_x, determ / bd_det_y (dg.py:199-202)
+    double inv_determ;                 // the nodal mass 1 / determ
+};
+
 // strided view of a state for the diagnostics / projection kernels
 struct DiagLayout {
     long long zstride, rstride, vstride;

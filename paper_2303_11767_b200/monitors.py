@@ -66,10 +66,19 @@ def _error_rule(op):
     return quad, build_vander(op.p, quad)
 
 
+def _weight_rows(mesh, quad, th) -> np.ndarray:
+    """(ny, n*n) quadrature weights per element row: w_i w_j cos(theta_j)
+    on the sphere, w_i w_j on the plane (diagnostics.py:66-75)."""
+    n = quad.n_1d
+    w2 = np.outer(quad.weights, quad.weights)
+    metric = np.cos(th) if mesh.kind == "latlon" else np.ones_like(th)
+    return np.ascontiguousarray((w2[None, :, :] * metric[:, None, :]).reshape(mesh.ny, n * n))
+
+
 def l2_error_host(state, reference_fn, op, var: str | None = None, relative: bool = False,
                   level: int = 0) -> float:
-    """L2 norm of (numerical - reference), p+2 Gauss rule, cos(theta) metric,
-    reference reduction order (diagnostics.py:42-80)."""
+    """L2 norm of (numerical - reference), p+2 Gauss rule, cos(theta) metric
+    on the sphere, reference reduction order (diagnostics.py:42-80)."""
     mesh = op.mesh
     var = var or state.names[0]
     quad, vander = _error_rule(op)
@@ -79,8 +88,7 @@ def l2_error_host(state, reference_fn, op, var: str | None = None, relative: boo
     lam, th = element_node_coords(mesh, quad.nodes)
     ref = np.broadcast_to(reference_fn(lam[:, None, :, None], th[None, :, None, :]),
                           (mesh.nx, mesh.ny, n, n)).reshape(mesh.nx, mesh.ny, n * n)
-    w2 = np.outer(quad.weights, quad.weights).reshape(-1)
-    w_rows = (w2.reshape(n, n)[None, :, :] * np.cos(th)[:, None, :]).reshape(mesh.ny, n * n)
+    w_rows = _weight_rows(mesh, quad, th)
     err = _ordered_sum(mesh.determ * np.einsum("xyq,yq->xy", (vals - ref) ** 2, w_rows))
     norm = _ordered_sum(mesh.determ * np.einsum("xyq,yq->xy", ref**2, w_rows))
     e = math.sqrt(max(err, 0.0))
@@ -102,8 +110,7 @@ def reference_nodal(reference_fn, lam: np.ndarray, th: np.ndarray, device) -> to
         vals = torch.broadcast_to(vals.to(torch.float64), (ny, nx, n, n))
     except Exception:
         v = reference_fn(lam[None, :, :, None], th[:, None, None, :])
-        vals = torch.from_numpy(np.ascontiguousarray(
-            np.broadcast_to(v, (ny, nx, n, n)), dtype=np.float64)).to(device)
+        vals = torch.from_numpy(np.array(np.broadcast_to(v, (ny, nx, n, n)), dtype=np.float64)).to(device)
     return vals.reshape(ny, nx, n * n).contiguous()
 
 
@@ -120,8 +127,7 @@ def l2_error(state, reference_fn, op, var: str | None = None, relative: bool = F
     n = quad.n_1d
     lam, th = element_node_coords(mesh, quad.nodes)
     ref = reference_nodal(reference_fn, lam, th, state.data.device)
-    w2 = np.outer(quad.weights, quad.weights)
-    w_rows = np.ascontiguousarray((w2[None, :, :] * np.cos(th)[:, None, :]).reshape(mesh.ny, n * n))
+    w_rows = _weight_rows(mesh, quad, th)
     phi2 = np.ascontiguousarray(vander.phi, dtype=np.float64)
     out = (ctypes.c_double * 2)()
     _lib.check(ctx.lib.dgswe_l2_sums(ctx.h, ctypes.c_void_p(state.data.data_ptr()), state.names.index(var),

@@ -6,8 +6,8 @@ API of /root/reference/pkg/src/dgswe/cases.py (``CaseConfig``,
 Williamson et al. (1992) equations: TC2 (90)-(95) with alpha = 0,
 TC6 (142)-(149).  The planar f-plane case (geostrophic adjustment,
 cases.py:113-123) runs on the same kernels (y-periodic plane); the scalar
-advection case (a one-variable model, cases.py:99-110) is outside the
-shallow-water hot path and raises NotImplementedError.
+advection case (a one-variable model, cases.py:99-110) runs on its own
+stage kernel (advection.py, csrc/dgswe_adv.cuh).
 Williamson TC5 (flow over an isolated mountain) is an extension: the
 reference has no orography; its bottom topography enters the
 model's momentum sources (physics.py) and the oracle restates the same
@@ -183,6 +183,23 @@ class RunSetup:
     constants: PhysicalConstants = EARTH
 
 
+ADV_BETA = (1.0, 1.0)
+
+
+def ic_advection_sine():
+    """sin(2 pi x) sin(2 pi y) on the periodic unit square; the exact
+    solution is the profile translated by beta t (cases.py:99-110)."""
+    beta = ADV_BETA
+
+    def u0(x, y):
+        return np.sin(2.0 * math.pi * x) * np.sin(2.0 * math.pi * y)
+
+    def exact(t):
+        return lambda x, y: u0(np.mod(x - beta[0] * t, 1.0), np.mod(y - beta[1] * t, 1.0))
+
+    return {"u": u0}, beta, exact
+
+
 def ic_geostrophic_adjustment():
     """Gaussian height bump at rest on the f-plane (cases.py:113-123)."""
 
@@ -215,6 +232,9 @@ def build_case(config: CaseConfig, constants: PhysicalConstants = EARTH) -> RunS
         model = swe_planar_model(constants.gravity, ADJ_F, h_ref=ADJ_H0)
         return RunSetup(config, build_planar_mesh(config.nx, config.ny, ADJ_LENGTH), model,
                         ic_geostrophic_adjustment(), None, constants)
-    if case in CASE_IDS:
-        raise NotImplementedError(f"{case!r}: scalar advection is outside the shallow-water hot path")
+    if case == "advection_sine":
+        from .advection import advection_model
+        ic, beta, exact = ic_advection_sine()
+        return RunSetup(config, build_planar_mesh(config.nx, config.ny, 1.0), advection_model(beta),
+                        ic, exact, constants)
     raise ValueError(f"unknown case {case!r}; choose from {CASE_IDS}")

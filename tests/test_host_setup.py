@@ -126,8 +126,8 @@ def test_cases_api():
     assert cfg.override(nx=8, dt=None).nx == 8
     with pytest.raises(ValueError):
         P.default_config("nope")
-    with pytest.raises(NotImplementedError):
-        P.build_case(P.default_config("advection_sine"))
+    setup = P.build_case(P.default_config("advection_sine"))
+    assert setup.model.beta == (1.0, 1.0) and setup.mesh.kind == "planar" and setup.mesh.dx == 0.05
     setup = P.build_case(P.default_config("williamson_tc2"))
     assert setup.model.h_floor == 1e-8 * (2.94e4 / 9.81)
     assert setup.exact(123.0) is not None
