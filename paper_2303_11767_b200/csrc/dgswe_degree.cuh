@@ -119,10 +119,12 @@ template <int P, int F>
 int launch_lo(dgswe_ctx *c, const StageParams &kp0, cudaStream_t s)
 {
     int &o = c->occ_lo[F & 1];
+    constexpr int smem = dgswe::lo_smem_bytes<P, (F & dgswe::kHasU) != 0>();
     if (!o) {
+        CUDA_TRY(cudaFuncSetAttribute(dgswe::lo_stage_kernel<P, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int q = 0;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, dgswe::lo_stage_kernel<P, F>,
-                                                               dgswe::kLoWarps * dgswe::kLanes, 0));
+                                                               dgswe::kLoWarps * dgswe::kLanes, smem));
         o = q > 0 ? q : 1;
     }
     StageParams kp = kp0;
@@ -140,7 +142,7 @@ int launch_lo(dgswe_ctx *c, const StageParams &kp0, cudaStream_t s)
         kp.even = (int)nch;
     }
     const dim3 grid((c->nstrip + dgswe::kLoWarps - 1) / dgswe::kLoWarps, (unsigned)nch, c->cfg.nz);
-    dgswe::lo_stage_kernel<P, F><<<grid, dgswe::kLoWarps * dgswe::kLanes, 0, s>>>(kp);
+    dgswe::lo_stage_kernel<P, F><<<grid, dgswe::kLoWarps * dgswe::kLanes, smem, s>>>(kp);
     CUDA_TRY(cudaGetLastError());
     c->launches += 1;
     return DGSWE_OK;

@@ -4,15 +4,20 @@
 // kernel (dgswe_kernels.cuh) then spends its time on per-row barriers, ring
 // waits and one face evaluation per node, not on HBM (C5 sweep: 26% of the
 // roofline).  Here ONE thread owns one
-// element with all three variables in registers and there is no shared
-// memory and no CTA barrier: warp w of a CTA marches north through a chunk
-// of rows of strip 4 blockIdx.x + w, lane l = element 32 s + l.
+// element with all three variables in registers and there is no CTA
+// barrier: warp w of a CTA marches north through a chunk of rows of strip
+// 4 blockIdx.x + w, lane l = element 32 s + l.  Its loads go through a
+// per-warp ring of kLoDepth rows in shared memory filled by cp.async
+// (LDGSTS) kLoDepth - 1 rows ahead (each lane reads back only its own words:
+// no warp barrier); the first version loaded row j+1 into registers and
+// consumed it in the same iteration, one DRAM latency per row (C5 p = 0:
+// 0.29 of the roofline -> 0.35-0.39 with the ring).
 //
 // Per row j (nodal values; SAME arithmetic as the main kernel -- the traces
 // of dgswe_kernels.cuh, face_core, volume<> and the finalize order -- so
 // both kernels give identical bits):
-//   * row j+1 is loaded (coalesced: one 256-byte line per variable and node)
-//     while row j is computed; its bottom traces and row j's top traces give
+//   * row j+1 (coalesced: one 256-byte line per variable and node) has
+//     landed in the ring while row j is computed; its bottom traces and row j's top traces give
 //     the y-face above row j, which is carried in registers as the next
 //     row's bottom face (each y-face evaluated once per strip);
 //   * x-faces: lane l evaluates its right face from its R trace and lane
@@ -33,6 +38,23 @@
 namespace dgswe {
 
 constexpr int kLoWarps = 4;   // strips per CTA
+// rows per warp in the shared-memory ring (kLoDepth - 1 in flight) and
+// resident CTAs per SM: measured at C5 p = 0 (1e9 DOF), depth 3..8 with
+// 1 / 6 / 8 CTAs: 4 rows with 6 CTAs (78 registers, no spill) best, deeper
+// rings slower (more open DRAM pages per SM), 8 CTAs spill
+constexpr int kLoDepth = 4;
+constexpr int kLoMinBlocks = 6;
+
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// dynamic shared memory of one low-order CTA
+template <int P, bool HAS_U>
+constexpr int lo_smem_bytes()
+{
+    constexpr int NP = (P + 1) * (P + 1);
+    return kLoWarps * kLoDepth * ((HAS_U ? 2 : 1) * 3 * NP * kLanes + 2 * 3 * NP) * (int)sizeof(double);
+}
 
 
 // the degrees the low-order kernel serves: p = 0 (1.7x the main kernel);
@@ -118,7 +140,7 @@ __device__ __forceinline__ double lo_shfl(double x, int delta, bool down)
 }
 
 template <int P, int F>
-__global__ void __launch_bounds__(kLoWarps * kLanes) lo_stage_kernel(StageParams kp)
+__global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kernel(StageParams kp)
 {
     static_assert(P <= 1, "low-order kernel");
     static_assert((F & ~kHasU) == 0, "low-order kernel: nodal stages with or without u^n only");
@@ -153,6 +175,65 @@ __global__ void __launch_bounds__(kLoWarps * kLanes) lo_stage_kernel(StageParams
     const double alpha_y = kp.alpha_mode == 2 ? kp.alpha_dev[1] : kp.alpha;
     unsigned bad = 0;
 
+    // per-warp ring of kLoDepth rows in shared memory, filled with
+    // cp.async (LDGSTS) kLoDepth - 1 rows ahead: row j's X, u^n and border
+    // neighbours, one commit group per row.  Each lane reads back only the
+    // words it copied itself, so no warp barrier is needed.
+    extern __shared__ __align__(16) double lo_smem[];
+    constexpr int ROWW = 3 * NP * kLanes;                       // one row of one variable set
+    constexpr int SLOT = (HAS_U ? 2 : 1) * ROWW + 2 * 3 * NP;   // X, u^n, left/right neighbour
+    double *ring = lo_smem + (threadIdx.x >> 5) * (kLoDepth * SLOT);
+    const bool lft = lane == 0, rgt = lane == nvalid - 1;
+    const int x_last = min(je, r_last);                         // rows whose X is read
+    auto issue = [&](int r, int slot) {
+        double *d = ring + slot * SLOT;
+        if (r <= x_last) {
+            const double *xr = X + (size_t)r * kp.rstride + (size_t)(e >> 5) * NP * kLanes + (e & 31);
+#pragma unroll
+            for (int v = 0; v < 3; ++v)
+#pragma unroll
+                for (int m = 0; m < NP; ++m)
+                    cp_async8(d + (v * NP + m) * kLanes + lane, xr + (size_t)v * kp.vstride + m * kLanes);
+            if (r < je) {
+                if constexpr (HAS_U) {
+                    const double *ur = kp.U + lane_off + (size_t)r * kp.rstride;
+#pragma unroll
+                    for (int v = 0; v < 3; ++v)
+#pragma unroll
+                        for (int m = 0; m < NP; ++m)
+                            cp_async8(d + ROWW + (v * NP + m) * kLanes + lane, ur + (size_t)v * kp.vstride + m * kLanes);
+                }
+                const double *row = X + (size_t)r * kp.rstride;
+                double *nb = d + (HAS_U ? 2 : 1) * ROWW;
+                if (lft) {
+                    const double *b = row + (size_t)(eL >> 5) * NP * kLanes + (eL & 31);
+#pragma unroll
+                    for (int v = 0; v < 3; ++v)
+#pragma unroll
+                        for (int m = 0; m < NP; ++m) cp_async8(nb + v * NP + m, b + (size_t)v * kp.vstride + m * kLanes);
+                }
+                if (rgt) {
+                    const double *b = row + (size_t)(eR >> 5) * NP * kLanes + (eR & 31);
+#pragma unroll
+                    for (int v = 0; v < 3; ++v)
+#pragma unroll
+                        for (int m = 0; m < NP; ++m)
+                            cp_async8(nb + 3 * NP + v * NP + m, b + (size_t)v * kp.vstride + m * kLanes);
+                }
+            }
+        }
+        cp_commit();
+    };
+    auto xrow = [&](int slot, double (&u)[3][NP]) {
+        const double *d = ring + slot * SLOT;
+#pragma unroll
+        for (int v = 0; v < 3; ++v)
+#pragma unroll
+            for (int m = 0; m < NP; ++m) u[v][m] = d[(v * NP + m) * kLanes + lane];
+    };
+#pragma unroll 1
+    for (int k = 0; k < kLoDepth - 1; ++k) issue(jb + k, k);
+
     double cur[3][NP], nxt[3][NP];
     lo_load<P>(X + (size_t)jb * kp.rstride, kp.vstride, e, cur);
     // the face below row jb: row jb-1's top traces against row jb's bottom ones
@@ -176,23 +257,34 @@ __global__ void __launch_bounds__(kLoWarps * kLanes) lo_stage_kernel(StageParams
         }
     }
 
+    int slot = 0;                                                // ring slot of row j
     for (int j = jb; j < je; ++j) {
         const bool has_next = j + 1 <= r_last;
-        const bool lft = lane == 0, rgt = lane == nvalid - 1;
-        // every load of the row first (row j+1, u^n, the border neighbours):
-        // one burst of independent memory traffic per row and warp
-        if (has_next) lo_load<P>(X + (size_t)(j + 1) * kp.rstride, kp.vstride, e, nxt);
+        const int slot1 = slot + 1 == kLoDepth ? 0 : slot + 1;
+        const int slotD = slot == 0 ? kLoDepth - 1 : slot - 1;   // row j + kLoDepth - 1
+        issue(j + kLoDepth - 1, slotD);
+        cp_wait<kLoDepth - 2>();                                 // rows <= j + 1 have landed
+        if (has_next) xrow(slot1, nxt);
         double un[3][NP];
         if constexpr (HAS_U) {
-            const double *Ub = kp.U + lane_off + (size_t)j * kp.rstride;
+            const double *d = ring + slot * SLOT + ROWW;
 #pragma unroll
             for (int v = 0; v < 3; ++v)
 #pragma unroll
-                for (int m = 0; m < NP; ++m) un[v][m] = Ub[(size_t)v * kp.vstride + m * kLanes];
+                for (int m = 0; m < NP; ++m) un[v][m] = d[(v * NP + m) * kLanes + lane];
         }
         double nbl[3][NP], nbr[3][NP];   // lane 0's left / the last lane's right neighbour
-        if (lft) lo_load<P>(X + (size_t)j * kp.rstride, kp.vstride, eL, nbl);
-        if (rgt) lo_load<P>(X + (size_t)j * kp.rstride, kp.vstride, eR, nbr);
+        {
+            const double *nb = ring + slot * SLOT + (HAS_U ? 2 : 1) * ROWW;
+#pragma unroll
+            for (int v = 0; v < 3; ++v)
+#pragma unroll
+                for (int m = 0; m < NP; ++m) {
+                    nbl[v][m] = nb[v * NP + m];
+                    nbr[v][m] = nb[3 * NP + v * NP + m];
+                }
+        }
+        slot = slot1;
         const double *rw = kp.rowtab + (size_t)(kp.row0 + j) * RL::STRIDE;
         // traces of row j (and positivity of the h nodes and traces)
         double lt[3][N], rt[3][N], tt[3][N];
@@ -296,6 +388,7 @@ __global__ void __launch_bounds__(kLoWarps * kLanes) lo_stage_kernel(StageParams
             }
         }
     }
+    cp_wait_all();      // (every issued row <= je was consumed; empty groups remain)
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && lane == 0) {
         atomicOr(kp.status, bad);

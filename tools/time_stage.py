@@ -23,7 +23,7 @@ def main():
     cfg = default_config("williamson_tc6").override(nx=nx, ny=ny, p=p)
     setup = build_case(cfg)
     op = SpatialOperator(setup.mesh, p, setup.model)
-    st = op.project_state(setup.ic)
+    st = op.project_state(setup.ic, device=True)
     x0 = st.data.clone()
     best = 1e30
     for rep in range(3):
