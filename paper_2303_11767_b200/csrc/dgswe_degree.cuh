@@ -129,7 +129,8 @@ int launch_lo(dgswe_ctx *c, const StageParams &kp0, cudaStream_t s)
     }
     StageParams kp = kp0;
     const int rows = kp.j_end - kp.j_begin;
-    const long long cols = (long long)((c->nstrip + dgswe::kLoWarps - 1) / dgswe::kLoWarps) * c->cfg.nz;
+    const int segs = dgswe::lo_segments(c->cfg.nx);
+    const long long cols = (long long)((segs + dgswe::kLoWarps - 1) / dgswe::kLoWarps) * c->cfg.nz;
     const long long slots = (long long)c->sms * o;
     long long nch = slots / cols;                        // one full wave
     if (nch < 1) nch = (rows + 7) / 8;                   // wide grids: ~8-row chunks, several waves
@@ -141,7 +142,7 @@ int launch_lo(dgswe_ctx *c, const StageParams &kp0, cudaStream_t s)
     } else {
         kp.even = (int)nch;
     }
-    const dim3 grid((c->nstrip + dgswe::kLoWarps - 1) / dgswe::kLoWarps, (unsigned)nch, c->cfg.nz);
+    const dim3 grid((segs + dgswe::kLoWarps - 1) / dgswe::kLoWarps, (unsigned)nch, c->cfg.nz);
     dgswe::lo_stage_kernel<P, F><<<grid, dgswe::kLoWarps * dgswe::kLanes, smem, s>>>(kp);
     CUDA_TRY(cudaGetLastError());
     c->launches += 1;

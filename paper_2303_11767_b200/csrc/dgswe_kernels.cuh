@@ -258,18 +258,18 @@ __device__ __forceinline__ double rsqrt64(double x)
     return fma(y, e * fma(e, 0.375, 0.5), y);
 }
 
-// 1/hf with hf = max(h, floor) (models.py:161-166) and the celerity
-// sqrt(g max(h, 0)) (models.py:254-258) from ONE rsqrt of h: below the floor
-// 1/hf is the constant 1/floor.  h <= 0 or NaN at any trace node sets the
+// 1/hf with hf = max(h, floor) (models.py:161-166) and sqrt(max(h, 0)) --
+// the celerity is sqrt(g) times it (models.py:254-258), which the face
+// fuses explicitly into |w| + c -- from ONE rsqrt of h: below the floor 1/hf
+// is the constant 1/floor.  h <= 0 or NaN at any trace node sets the
 // positivity status bit, which discards the whole step (PositivityError,
-// dg.py:359-372), so c there only has to stay finite (it is <= 0 instead of
-// the reference's 0; the rsqrt argument is clamped to DBL_MIN).
-__device__ __forceinline__ void inv_and_celerity(double h, double h_floor, double inv_floor, double sqrt_g,
-                                                 double &r, double &c)
+// dg.py:359-372), so the root there only has to stay finite (it is <= 0
+// instead of the reference's 0; the rsqrt argument is clamped to DBL_MIN).
+__device__ __forceinline__ void inv_and_sqrt(double h, double h_floor, double inv_floor, double &r, double &sh)
 {
     const double y = rsqrt64(max_pos(h, 2.2250738585072014e-308));
     r = ge_pos(h, h_floor) ? y * y : inv_floor;   // branches compared on the integer pipe
-    c = sqrt_g * (h * y);
+    sh = h * y;
 }
 
 // --- TMA bulk copies and mbarriers (one elected lane per variable warp) ---
@@ -421,22 +421,24 @@ struct FaceArgs {
 // tangential momentum on the "in" / "out" side) into fh / fn / ft: shared
 // by the shared-memory face routine below and the low-order kernel
 // (dgswe_lo.cuh), so both give identical bits.
+// the face arithmetic from given reciprocals rin / rout and square roots
+// cin / cout of the two sides' h traces (inv_and_sqrt of hI / hO; the
+// celerity is sqrt(g) times it, fused explicitly): the low-order kernel
+// computes them once per element and shares them
 template <int P>
-__device__ __forceinline__ void face_core(const double (&hI)[P + 1], const double (&nI)[P + 1],
-                                          const double (&tI)[P + 1], const double (&hO)[P + 1],
-                                          const double (&nO)[P + 1], const double (&tO)[P + 1], const FaceArgs &fa,
-                                          double (&fh)[P + 1], double (&fn)[P + 1], double (&ft)[P + 1])
+__device__ __forceinline__ void face_core_rc(const double (&hI)[P + 1], const double (&nI)[P + 1],
+                                             const double (&tI)[P + 1], const double (&rin)[P + 1],
+                                             const double (&cin)[P + 1], const double (&hO)[P + 1],
+                                             const double (&nO)[P + 1], const double (&tO)[P + 1],
+                                             const double (&rout)[P + 1], const double (&cout)[P + 1],
+                                             const FaceArgs &fa, double (&fh)[P + 1], double (&fn)[P + 1],
+                                             double (&ft)[P + 1])
 {
     constexpr int N = P + 1;
-    double rin[N], rout[N];
     double am[N];
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-        double ci, co;
-        inv_and_celerity(hI[k], fa.h_floor, fa.inv_floor, fa.sqrt_g, rin[k], ci);
-        inv_and_celerity(hO[k], fa.h_floor, fa.inv_floor, fa.sqrt_g, rout[k], co);
-        am[k] = max_nn(fabs(nI[k] * rin[k]) + ci, fabs(nO[k] * rout[k]) + co);
-    }
+    for (int k = 0; k < N; ++k)
+        am[k] = max_nn(fma(fa.sqrt_g, cin[k], fabs(nI[k] * rin[k])), fma(fa.sqrt_g, cout[k], fabs(nO[k] * rout[k])));
 #pragma unroll
     for (int w = 1; w < N; w *= 2)
 #pragma unroll
@@ -459,6 +461,22 @@ __device__ __forceinline__ void face_core(const double (&hI)[P + 1], const doubl
         fn[k] = fma(hs, fni + fno, -ha * (nO[k] - nI[k]));
         ft[k] = fma(hs, ft_sum, -ha * (tO[k] - tI[k]));
     }
+}
+
+template <int P>
+__device__ __forceinline__ void face_core(const double (&hI)[P + 1], const double (&nI)[P + 1],
+                                          const double (&tI)[P + 1], const double (&hO)[P + 1],
+                                          const double (&nO)[P + 1], const double (&tO)[P + 1], const FaceArgs &fa,
+                                          double (&fh)[P + 1], double (&fn)[P + 1], double (&ft)[P + 1])
+{
+    constexpr int N = P + 1;
+    double rin[N], rout[N], cin[N], cout[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        inv_and_sqrt(hI[k], fa.h_floor, fa.inv_floor, rin[k], cin[k]);
+        inv_and_sqrt(hO[k], fa.h_floor, fa.inv_floor, rout[k], cout[k]);
+    }
+    face_core_rc<P>(hI, nI, tI, rin, cin, hO, nO, tO, rout, cout, fa, fh, fn, ft);
 }
 
 template <int P>

@@ -3,30 +3,37 @@
 // At p = 0 an element has one node per variable: the warp-specialised
 // kernel (dgswe_kernels.cuh) then spends its time on per-row barriers, ring
 // waits and one face evaluation per node, not on HBM (C5 sweep: 26% of the
-// roofline).  Here ONE thread owns one
-// element with all three variables in registers and there is no CTA
-// barrier: warp w of a CTA marches north through a chunk of rows of strip
-// 4 blockIdx.x + w, lane l = element 32 s + l.  Its loads go through a
-// per-warp ring of kLoDepth rows in shared memory filled by cp.async
-// (LDGSTS) kLoDepth - 1 rows ahead (each lane reads back only its own words:
-// no warp barrier); the first version loaded row j+1 into registers and
-// consumed it in the same iteration, one DRAM latency per row (C5 p = 0:
-// 0.29 of the roofline -> 0.35-0.39 with the ring).
+// roofline).  Here ONE thread owns one element with all three variables
+// in registers and there is no CTA barrier: warp w of a CTA marches north
+// through a chunk of rows of segment 4 blockIdx.x + w, 30 elements wide:
+// lanes 1..30 own elements 30 s .. 30 s + 29, lanes 0 and 31 hold their
+// periodic neighbours (read like the owned ones, never stored).  Its loads
+// go through a per-warp ring of kLoDepth rows in shared memory filled by
+// cp.async (LDGSTS) kLoDepth - 1 rows ahead (each lane reads back only its
+// own words: no warp barrier).  C5 p = 0 (1e9 DOF): 0.29 of the roofline
+// with one row loaded and consumed per iteration, 0.36 with the ring, 0.47
+// with the halo lanes and shared reciprocals (below).
 //
 // Per row j (nodal values; SAME arithmetic as the main kernel -- the traces
-// of dgswe_kernels.cuh, face_core, volume<> and the finalize order -- so
+// of dgswe_kernels.cuh, face_core_rc, volume<> and the finalize order -- so
 // both kernels give identical bits):
-//   * row j+1 (coalesced: one 256-byte line per variable and node) has
-//     landed in the ring while row j is computed; its bottom traces and row j's top traces give
-//     the y-face above row j, which is carried in registers as the next
-//     row's bottom face (each y-face evaluated once per strip);
-//   * x-faces: lane l evaluates its right face from its R trace and lane
-//     l+1's L trace (warp shuffles); its left face is lane l-1's (shuffle).
-//     The strip's border lanes load the neighbour strip's element and form
-//     its trace themselves: lane 0 of strip s+1 and the last lane of strip s
-//     then evaluate the same face from the same operands, in the same order.
+//   * at p = 0 all four traces of an element are its value (l_0 = 1), so
+//     1/h and sqrt(h) (inv_and_sqrt) are formed ONCE per element and row and
+//     shared: the right neighbour's by shuffle, the next row's computed for
+//     the y-face and carried up as that row's own (the main kernel forms
+//     them per face side: identical bits, the face fuses sqrt(g) sqrt(h)
+//     explicitly);
+//   * row j+1 (coalesced: one 256-byte line per variable) has landed in the
+//     ring while row j is computed; its traces and row j's give the y-face
+//     above row j, carried in registers as the next row's bottom face (each
+//     y-face evaluated once per segment);
+//   * x-faces: lane l (0..30) evaluates the face between lanes l and l+1
+//     (operands of lane l+1 by shuffle); an owned lane's left face is lane
+//     l-1's.  No lane evaluates an extra face alone: the neighbouring
+//     segments evaluate their shared border face from the same operands in
+//     the same order (2 of 32 lanes are halo work instead);
 //   * volume + source (models.py:161-252), lifts, diagonal mass and the
-//     stage combination (timestep.py:132-167), stores.
+//     stage combination (timestep.py:132-167), stores of the owned lanes.
 // Variants: plain nodal stages with and without the u^n term (kHasU) -- the
 // SSPRK3 / RK1 / RK2 steps of dgswe_rk_steps and the nodal stage entry
 // points.  Every other variant (modal, RK4's second output, band edges,
@@ -44,6 +51,10 @@ constexpr int kLoWarps = 4;   // strips per CTA
 // rings slower (more open DRAM pages per SM), 8 CTAs spill
 constexpr int kLoDepth = 4;
 constexpr int kLoMinBlocks = 6;
+constexpr int kLoOwn = kLanes - 2;   // elements a warp owns: lanes 1..30 (lanes 0 / 31: neighbours)
+
+// warp segments of kLoOwn elements covering a row
+__host__ __device__ constexpr int lo_segments(int nx) { return (nx + kLoOwn - 1) / kLoOwn; }
 
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -53,7 +64,7 @@ template <int P, bool HAS_U>
 constexpr int lo_smem_bytes()
 {
     constexpr int NP = (P + 1) * (P + 1);
-    return kLoWarps * kLoDepth * ((HAS_U ? 2 : 1) * 3 * NP * kLanes + 2 * 3 * NP) * (int)sizeof(double);
+    return kLoWarps * kLoDepth * (HAS_U ? 2 : 1) * 3 * NP * kLanes * (int)sizeof(double);
 }
 
 
@@ -97,33 +108,6 @@ __device__ __forceinline__ void lo_xtraces(const double (&u)[3][(P + 1) * (P + 1
     }
 }
 
-template <int P, bool LO>
-__device__ __forceinline__ void lo_ytraces(const double (&u)[3][(P + 1) * (P + 1)], double (&tr)[3][P + 1])
-{
-#pragma unroll
-    for (int v = 0; v < 3; ++v) {
-        double t[P + 1][P + 1];
-        lo_tile<P>(u[v], t);
-        ytrace<P, LO>(t, tr[v]);
-    }
-}
-
-// Rusanov flux of one face from [var][node] traces, back into [var][node]
-template <int P>
-__device__ __forceinline__ void lo_face(const double (&in)[3][P + 1], const double (&out)[3][P + 1],
-                                        const FaceArgs &fa, double (&f)[3][P + 1])
-{
-    const int vn = 1 + fa.dir, vt = 2 - fa.dir;
-    double fh[P + 1], fn[P + 1], ft[P + 1];
-    face_core<P>(in[0], in[vn], in[vt], out[0], out[vn], out[vt], fa, fh, fn, ft);
-#pragma unroll
-    for (int k = 0; k < P + 1; ++k) {
-        f[0][k] = fh[k];
-        f[vn][k] = fn[k];
-        f[vt][k] = ft[k];
-    }
-}
-
 template <int P>
 __device__ __forceinline__ unsigned lo_positive(const double *x, int n)
 {
@@ -133,30 +117,28 @@ __device__ __forceinline__ unsigned lo_positive(const double *x, int n)
     return bad;
 }
 
-template <int P>
-__device__ __forceinline__ double lo_shfl(double x, int delta, bool down)
-{
-    return down ? __shfl_down_sync(0xffffffffu, x, delta) : __shfl_up_sync(0xffffffffu, x, delta);
-}
-
 template <int P, int F>
 __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kernel(StageParams kp)
 {
-    static_assert(P <= 1, "low-order kernel");
+    static_assert(P == 0, "low-order kernel: one node per element");
     static_assert((F & ~kHasU) == 0, "low-order kernel: nodal stages with or without u^n only");
     constexpr bool HAS_U = (F & kHasU) != 0;
     constexpr int N = P + 1;
     constexpr int NP = N * N;
     using RL = RowLayout<P>;
     const int lane = threadIdx.x & 31;
-    const int strip = blockIdx.x * kLoWarps + (threadIdx.x >> 5);
-    if (strip >= kp.nstrip) return;                 // whole warps: no barrier below
     const int nx = kp.nx;
-    const int nvalid = min(kLanes, nx - strip * kLanes);
-    const bool owned = lane < nvalid;
-    const int e = strip * kLanes + (owned ? lane : nvalid - 1);   // padding lanes mirror a valid one
-    const int eL = (strip * kLanes - 1 + nx) % nx;                 // left neighbour of lane 0
-    const int eR = (strip * kLanes + nvalid) % nx;                 // right neighbour of the last lane
+    const int seg = blockIdx.x * kLoWarps + (threadIdx.x >> 5);
+    if (seg >= lo_segments(nx)) return;             // whole warps: no barrier below
+    // lanes 1..nvalid own elements first .. first + nvalid - 1; lane 0 and
+    // lane nvalid + 1 hold the neighbours (periodic), padding lanes mirror
+    // the right neighbour
+    const int first = seg * kLoOwn;
+    const int nvalid = min(kLoOwn, nx - first);
+    const bool owned = lane >= 1 && lane <= nvalid;
+    int g = first - 1 + min(lane, nvalid + 1);
+    g = g < 0 ? g + nx : (g >= nx ? g - nx : g);
+    const size_t eoff = (size_t)blockIdx.z * kp.zstride + (size_t)(g >> 5) * NP * kLanes + (g & 31);
     int jb, je;
     if (kp.even > 0) {
         const int rows = kp.j_end - kp.j_begin;
@@ -167,94 +149,81 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
         je = min(jb + kp.rc, kp.j_end);
     }
     if (jb >= je) return;
-    const double *X = kp.X + (size_t)blockIdx.z * kp.zstride;
-    const size_t lane_off = (size_t)blockIdx.z * kp.zstride + (size_t)strip * NP * kLanes + lane;
     const int r_last = min(kp.nrows - 1, kp.ny - 1 - kp.row0);      // local rows with coefficients
     const FaceArgs fx{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r, kp.alpha_mode, 0,
                       0.0, 0.0, kp.alpha_mode == 2 ? kp.alpha_dev[0] : kp.alpha, kp.bdy};
     const double alpha_y = kp.alpha_mode == 2 ? kp.alpha_dev[1] : kp.alpha;
     unsigned bad = 0;
 
-    // per-warp ring of kLoDepth rows in shared memory, filled with
-    // cp.async (LDGSTS) kLoDepth - 1 rows ahead: row j's X, u^n and border
-    // neighbours, one commit group per row.  Each lane reads back only the
-    // words it copied itself, so no warp barrier is needed.
+    // per-warp ring of kLoDepth rows in shared memory, filled with cp.async
+    // (LDGSTS) kLoDepth - 1 rows ahead: row r's X and u^n, one commit group
+    // per row; each lane reads back only the words it copied itself
     extern __shared__ __align__(16) double lo_smem[];
-    constexpr int ROWW = 3 * NP * kLanes;                       // one row of one variable set
-    constexpr int SLOT = (HAS_U ? 2 : 1) * ROWW + 2 * 3 * NP;   // X, u^n, left/right neighbour
+    constexpr int ROWW = 3 * NP * kLanes;
+    constexpr int SLOT = (HAS_U ? 2 : 1) * ROWW;
     double *ring = lo_smem + (threadIdx.x >> 5) * (kLoDepth * SLOT);
-    const bool lft = lane == 0, rgt = lane == nvalid - 1;
     const int x_last = min(je, r_last);                         // rows whose X is read
     auto issue = [&](int r, int slot) {
         double *d = ring + slot * SLOT;
         if (r <= x_last) {
-            const double *xr = X + (size_t)r * kp.rstride + (size_t)(e >> 5) * NP * kLanes + (e & 31);
+            const double *xr = kp.X + eoff + (size_t)r * kp.rstride;
 #pragma unroll
             for (int v = 0; v < 3; ++v)
 #pragma unroll
                 for (int m = 0; m < NP; ++m)
                     cp_async8(d + (v * NP + m) * kLanes + lane, xr + (size_t)v * kp.vstride + m * kLanes);
-            if (r < je) {
-                if constexpr (HAS_U) {
-                    const double *ur = kp.U + lane_off + (size_t)r * kp.rstride;
+            if constexpr (HAS_U) {
+                if (r < je && owned) {
+                    const double *ur = kp.U + eoff + (size_t)r * kp.rstride;
 #pragma unroll
                     for (int v = 0; v < 3; ++v)
 #pragma unroll
                         for (int m = 0; m < NP; ++m)
                             cp_async8(d + ROWW + (v * NP + m) * kLanes + lane, ur + (size_t)v * kp.vstride + m * kLanes);
                 }
-                const double *row = X + (size_t)r * kp.rstride;
-                double *nb = d + (HAS_U ? 2 : 1) * ROWW;
-                if (lft) {
-                    const double *b = row + (size_t)(eL >> 5) * NP * kLanes + (eL & 31);
-#pragma unroll
-                    for (int v = 0; v < 3; ++v)
-#pragma unroll
-                        for (int m = 0; m < NP; ++m) cp_async8(nb + v * NP + m, b + (size_t)v * kp.vstride + m * kLanes);
-                }
-                if (rgt) {
-                    const double *b = row + (size_t)(eR >> 5) * NP * kLanes + (eR & 31);
-#pragma unroll
-                    for (int v = 0; v < 3; ++v)
-#pragma unroll
-                        for (int m = 0; m < NP; ++m)
-                            cp_async8(nb + 3 * NP + v * NP + m, b + (size_t)v * kp.vstride + m * kLanes);
-                }
             }
         }
         cp_commit();
     };
-    auto xrow = [&](int slot, double (&u)[3][NP]) {
-        const double *d = ring + slot * SLOT;
-#pragma unroll
-        for (int v = 0; v < 3; ++v)
-#pragma unroll
-            for (int m = 0; m < NP; ++m) u[v][m] = d[(v * NP + m) * kLanes + lane];
-    };
 #pragma unroll 1
     for (int k = 0; k < kLoDepth - 1; ++k) issue(jb + k, k);
 
+    // row values, their (identical) traces and the reciprocal / celerity of
+    // the h trace, computed once per element and row: the x-face takes the
+    // right neighbour's by shuffle, the y-face the next row's, which is then
+    // carried up as the next row's own
+    auto traces = [&](const double (&u)[3][NP], double (&t)[3][N], double (&r)[N], double (&c)[N]) {
+        lo_xtraces<P, false>(u, t);
+#pragma unroll
+        for (int k = 0; k < N; ++k) inv_and_sqrt(t[0][k], kp.h_floor, kp.inv_floor, r[k], c[k]);
+    };
     double cur[3][NP], nxt[3][NP];
-    lo_load<P>(X + (size_t)jb * kp.rstride, kp.vstride, e, cur);
+    lo_load<P>(kp.X + (size_t)jb * kp.rstride + (size_t)blockIdx.z * kp.zstride, kp.vstride, g, cur);
+    double tr[3][N], rr[N], cc[N];
+    traces(cur, tr, rr, cc);
+    bad |= owned & lo_positive<P>(tr[0], N);
     // the face below row jb: row jb-1's top traces against row jb's bottom ones
     double fbot[3][N];
-    {
-        double bt[3][N];
-        lo_ytraces<P, true>(cur, bt);
-        bad |= owned & lo_positive<P>(bt[0], N);
-        if (kp.row0 + jb > 0) {
-            double below[3][NP], tt[3][N];
-            lo_load<P>(X + (size_t)(jb - 1) * kp.rstride, kp.vstride, e, below);
-            lo_ytraces<P, false>(below, tt);
-            const double *rw = kp.rowtab + (size_t)(kp.row0 + jb) * RL::STRIDE;
-            lo_face<P>(tt, bt, FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r, kp.alpha_mode,
-                                        1, rw[RL::CRB], rw[RL::COSB], alpha_y, kp.bdx}, fbot);
-        } else {
+    if (kp.row0 + jb > 0) {
+        double below[3][NP], tb[3][N], rb[N], cb[N];
+        lo_load<P>(kp.X + (size_t)(jb - 1) * kp.rstride + (size_t)blockIdx.z * kp.zstride, kp.vstride, g, below);
+        traces(below, tb, rb, cb);
+        const double *rw = kp.rowtab + (size_t)(kp.row0 + jb) * RL::STRIDE;
+        const FaceArgs fy{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r, kp.alpha_mode,
+                          1, rw[RL::CRB], rw[RL::COSB], alpha_y, kp.bdx};
+        double fh[N], fn[N], ft[N];
+        face_core_rc<P>(tb[0], tb[2], tb[1], rb, cb, tr[0], tr[2], tr[1], rr, cc, fy, fh, fn, ft);
 #pragma unroll
-            for (int v = 0; v < 3; ++v)
-#pragma unroll
-                for (int k = 0; k < N; ++k) fbot[v][k] = 0.0;   // a pole: no face (dg.py:483-495)
+        for (int k = 0; k < N; ++k) {
+            fbot[0][k] = fh[k];
+            fbot[2][k] = fn[k];
+            fbot[1][k] = ft[k];
         }
+    } else {
+#pragma unroll
+        for (int v = 0; v < 3; ++v)
+#pragma unroll
+            for (int k = 0; k < N; ++k) fbot[v][k] = 0.0;   // a pole: no face (dg.py:483-495)
     }
 
     int slot = 0;                                                // ring slot of row j
@@ -264,7 +233,13 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
         const int slotD = slot == 0 ? kLoDepth - 1 : slot - 1;   // row j + kLoDepth - 1
         issue(j + kLoDepth - 1, slotD);
         cp_wait<kLoDepth - 2>();                                 // rows <= j + 1 have landed
-        if (has_next) xrow(slot1, nxt);
+        if (has_next) {
+            const double *d = ring + slot1 * SLOT;
+#pragma unroll
+            for (int v = 0; v < 3; ++v)
+#pragma unroll
+                for (int m = 0; m < NP; ++m) nxt[v][m] = d[(v * NP + m) * kLanes + lane];
+        }
         double un[3][NP];
         if constexpr (HAS_U) {
             const double *d = ring + slot * SLOT + ROWW;
@@ -273,54 +248,52 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
 #pragma unroll
                 for (int m = 0; m < NP; ++m) un[v][m] = d[(v * NP + m) * kLanes + lane];
         }
-        double nbl[3][NP], nbr[3][NP];   // lane 0's left / the last lane's right neighbour
-        {
-            const double *nb = ring + slot * SLOT + (HAS_U ? 2 : 1) * ROWW;
-#pragma unroll
-            for (int v = 0; v < 3; ++v)
-#pragma unroll
-                for (int m = 0; m < NP; ++m) {
-                    nbl[v][m] = nb[v * NP + m];
-                    nbr[v][m] = nb[3 * NP + v * NP + m];
-                }
-        }
         slot = slot1;
         const double *rw = kp.rowtab + (size_t)(kp.row0 + j) * RL::STRIDE;
-        // traces of row j (and positivity of the h nodes and traces)
-        double lt[3][N], rt[3][N], tt[3][N];
-        lo_xtraces<P, true>(cur, lt);
-        lo_xtraces<P, false>(cur, rt);
-        lo_ytraces<P, false>(cur, tt);
-        bad |= owned & (lo_positive<P>(lt[0], N) | lo_positive<P>(rt[0], N) | lo_positive<P>(tt[0], N) |
-                        lo_positive<P>(cur[0], NP));
-        // x-faces: the right face of every lane from lane+1's L trace; the
-        // last valid lane's neighbour (and lane 0's left one) from memory
-        double nl[3][N];
-#pragma unroll
-        for (int v = 0; v < 3; ++v)
-#pragma unroll
-            for (int k = 0; k < N; ++k) nl[v][k] = lo_shfl<P>(lt[v][k], 1, true);
-        if (rgt) lo_xtraces<P, true>(nbr, nl);
+        bad |= owned & lo_positive<P>(cur[0], NP);
+        // x-faces: lane l (0..nvalid) evaluates the face between lanes l and
+        // l+1 from its own traces and lane l+1's (shuffled with its
+        // reciprocal and celerity); an owned lane's left face is lane l-1's
         double fr[3][N], fl[3][N];
-        lo_face<P>(rt, nl, fx, fr);
+        {
+            double ho[N], no[N], to[N], ro[N], co[N];
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                ho[k] = __shfl_down_sync(0xffffffffu, tr[0][k], 1);
+                no[k] = __shfl_down_sync(0xffffffffu, tr[1][k], 1);
+                to[k] = __shfl_down_sync(0xffffffffu, tr[2][k], 1);
+                ro[k] = __shfl_down_sync(0xffffffffu, rr[k], 1);
+                co[k] = __shfl_down_sync(0xffffffffu, cc[k], 1);
+            }
+            double fh[N], fn[N], ft[N];
+            face_core_rc<P>(tr[0], tr[1], tr[2], rr, cc, ho, no, to, ro, co, fx, fh, fn, ft);
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                fr[0][k] = fh[k];
+                fr[1][k] = fn[k];
+                fr[2][k] = ft[k];
+            }
+        }
 #pragma unroll
         for (int v = 0; v < 3; ++v)
 #pragma unroll
-            for (int k = 0; k < N; ++k) fl[v][k] = lo_shfl<P>(fr[v][k], 1, false);
-        if (lft) {
-            double nr[3][N];
-            lo_xtraces<P, false>(nbl, nr);
-            lo_face<P>(nr, lt, fx, fl);
-        }
+            for (int k = 0; k < N; ++k) fl[v][k] = __shfl_up_sync(0xffffffffu, fr[v][k], 1);
         // the y-face above row j (zero at the pole), carried to the next row
-        double ftop[3][N];
+        double ftop[3][N], trn[3][N], rn[N], cn[N];
         if (has_next) {
-            double bt[3][N];
-            lo_ytraces<P, true>(nxt, bt);
-            bad |= owned & lo_positive<P>(bt[0], N);
+            traces(nxt, trn, rn, cn);
+            bad |= owned & lo_positive<P>(trn[0], N);
             const double *ra = rw + RL::STRIDE;
-            lo_face<P>(tt, bt, FaceArgs{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r, kp.alpha_mode,
-                                        1, ra[RL::CRB], ra[RL::COSB], alpha_y, kp.bdx}, ftop);
+            const FaceArgs fy{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r, kp.alpha_mode,
+                              1, ra[RL::CRB], ra[RL::COSB], alpha_y, kp.bdx};
+            double fh[N], fn[N], ft[N];
+            face_core_rc<P>(tr[0], tr[2], tr[1], rr, cc, trn[0], trn[2], trn[1], rn, cn, fy, fh, fn, ft);
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                ftop[0][k] = fh[k];
+                ftop[2][k] = fn[k];
+                ftop[1][k] = ft[k];
+            }
         } else {
 #pragma unroll
             for (int v = 0; v < 3; ++v)
@@ -350,7 +323,7 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
                     acc[q][k] = fma(c_nod[P].mu[k], fbot[v][q], fma(-c_nod[P].mu[N - 1 - k], ftop[v][q], acc[q][k]));
                 }
             }
-            double *Yv = kp.Y + lane_off + (size_t)v * kp.vstride + (size_t)j * kp.rstride;
+            double *Yv = kp.Y + eoff + (size_t)v * kp.vstride + (size_t)j * kp.rstride;
 #pragma unroll
             for (int jj = 0; jj < N; ++jj) {
                 const double gr = kp.g * rw[RL::RJ + jj];
@@ -377,14 +350,22 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
             if (kp.check_finite) bad |= fexp == 0x7ff00000 ? 2u : 0u;
             if (kp.check_mean) bad |= !(mean > 0.0) ? 4u : 0u;
         }
-        // slide the window: the next row's bottom face is this row's top face
+        // slide the window: the next row's values, traces and bottom face
         if (has_next) {
 #pragma unroll
             for (int v = 0; v < 3; ++v) {
 #pragma unroll
                 for (int m = 0; m < NP; ++m) cur[v][m] = nxt[v][m];
 #pragma unroll
-                for (int k = 0; k < N; ++k) fbot[v][k] = ftop[v][k];
+                for (int k = 0; k < N; ++k) {
+                    fbot[v][k] = ftop[v][k];
+                    tr[v][k] = trn[v][k];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                rr[k] = rn[k];
+                cc[k] = cn[k];
             }
         }
     }
