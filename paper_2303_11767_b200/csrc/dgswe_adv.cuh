@@ -5,15 +5,19 @@
 // A one-variable scalar model outside the shallow-water hot path, so the
 // kernel is plain: one thread per element, the state in the reference's
 // modal coefficients with layout [nz][ny][nphi][nx] (a warp reads 32
-// consecutive elements of one mode), the element's and its four
-// neighbours' tiles converted to the Gauss nodes in registers, the nodal
-// form of the same operator as the shallow-water kernel (DESIGN.md
-// section 3): weak derivatives with the tables of dgswe_params.h NodTab,
-// Rusanov faces with alpha = |beta . n| (the model's wavespeed,
-// models.py:129-135), the diagonal nodal mass, and
+// consecutive elements of one mode).  Face traces come straight from the
+// modes (Legendre P_a(+-1) = (+-1)^a: a signed sum over one index, then the
+// Gauss-node values of the other, the same formula for an element's own
+// trace and for its neighbour's, so both sides of a face use identical
+// operands and the face flux is bit-identical); each neighbour is streamed
+// through two N-vectors instead of a converted tile, which keeps p <= 5
+// free of spills.  Then the nodal form of the same operator as the
+// shallow-water kernel: Rusanov faces with
+// alpha = |beta . n| (the model's wavespeed, models.py:129-135) lifted with
+// mu, weak derivatives with the tables of dgswe_params.h NodTab, the
+// diagonal nodal mass, and
 //   Y = a U + b X + g RHS(X)
-// with the nodal RHS converted back to modes.  Each face is evaluated by
-// both elements from the same operands in the same order (bit-identical).
+// with the nodal RHS converted back to modes.
 #pragma once
 
 #include "dgswe_kernels.cuh"
@@ -28,6 +32,33 @@ __device__ __forceinline__ double adv_flux(double in, double out, double bn, dou
     return scale * fma(0.5 * bn, in + out, -0.5 * fabs(bn) * (out - in));
 }
 
+// trace of element (ii, jj) at the Gauss nodes of one side, from its
+// modes c[a][b] (a: x degree, b: y degree): X side (xi = SGN) or Y side
+template <int P, bool XSIDE, int SGN>
+__device__ __forceinline__ void adv_trace(const double *c, long long mstride, double (&tr)[P + 1])
+{
+    constexpr int N = P + 1;
+    double s[N];
+#pragma unroll
+    for (int o = 0; o < N; ++o) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            const int a = XSIDE ? k : o, b = XSIDE ? o : k;
+            const double v = c[(size_t)(a * N + b) * mstride];
+            acc = (SGN < 0 && (k & 1)) ? acc - v : acc + v;
+        }
+        s[o] = acc;
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+        double t = 0.0;
+#pragma unroll
+        for (int o = 0; o < N; ++o) t = fma(c_nod[P].leg[o][q], s[o], t);
+        tr[q] = t;
+    }
+}
+
 template <int P>
 __global__ void __launch_bounds__(128) adv_stage_kernel(AdvParams ap)
 {
@@ -37,57 +68,61 @@ __global__ void __launch_bounds__(128) adv_stage_kernel(AdvParams ap)
     const int j = blockIdx.y;
     if (i >= ap.nx) return;
     const size_t zoff = (size_t)blockIdx.z * ap.zstride;
-    // nodal tile of element (ii, jj), periodic in both directions
-    auto tile = [&](int ii, int jj, double (&u)[N][N]) {
-        ii = (ii + ap.nx) % ap.nx;
-        jj = (jj + ap.ny) % ap.ny;
-        const double *c = ap.X + zoff + (size_t)jj * NP * ap.nx + ii;
+    const long long ms = ap.nx;                                  // mode stride
+    auto elem = [&](int ii, int jj) {                            // periodic in both directions
+        ii = ii < 0 ? ii + ap.nx : (ii >= ap.nx ? ii - ap.nx : ii);
+        jj = jj < 0 ? jj + ap.ny : (jj >= ap.ny ? jj - ap.ny : jj);
+        return ap.X + zoff + (size_t)jj * NP * ap.nx + ii;
+    };
+    const double *self = elem(i, j);
+    // the four face fluxes (lower / left element = "in"), scaled by the face Jacobian
+    double fl[N], fr[N], fb[N], ft[N];
+    {
+        double own[N], nb[N];
+        adv_trace<P, true, -1>(self, ms, own);
+        adv_trace<P, true, 1>(elem(i - 1, j), ms, nb);
+#pragma unroll
+        for (int q = 0; q < N; ++q) fl[q] = adv_flux(nb[q], own[q], ap.bx, ap.bdy);
+        adv_trace<P, true, 1>(self, ms, own);
+        adv_trace<P, true, -1>(elem(i + 1, j), ms, nb);
+#pragma unroll
+        for (int q = 0; q < N; ++q) fr[q] = adv_flux(own[q], nb[q], ap.bx, ap.bdy);
+        adv_trace<P, false, -1>(self, ms, own);
+        adv_trace<P, false, 1>(elem(i, j - 1), ms, nb);
+#pragma unroll
+        for (int q = 0; q < N; ++q) fb[q] = adv_flux(nb[q], own[q], ap.by, ap.bdx);
+        adv_trace<P, false, 1>(self, ms, own);
+        adv_trace<P, false, -1>(elem(i, j + 1), ms, nb);
+#pragma unroll
+        for (int q = 0; q < N; ++q) ft[q] = adv_flux(own[q], nb[q], ap.by, ap.bdx);
+    }
+    // lifts (x faces along xi, y faces along eta), then the volume:
+    // sum_k Dx[ii][k] F[k][jj] + sum_k dh[jj][k] G[ii][k]
+    double acc[N][N];
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+        for (int b = 0; b < N; ++b)
+            acc[a][b] = fma(c_nod[P].mu[a], fl[b], -c_nod[P].mu[N - 1 - a] * fr[b]) +
+                        fma(c_nod[P].mu[b], fb[a], -c_nod[P].mu[N - 1 - b] * ft[a]);
+    {
+        double u[N][N];
 #pragma unroll
         for (int a = 0; a < N; ++a)
 #pragma unroll
-            for (int b = 0; b < N; ++b) u[a][b] = c[(size_t)(a * N + b) * ap.nx];
+            for (int b = 0; b < N; ++b) u[a][b] = self[(size_t)(a * N + b) * ms];
         to_nodal<P>(u);
-    };
-    double u[N][N], nb[N][N];
-    tile(i, j, u);
-    double lt[N], rt[N], bt[N], tt[N], nr[N], nl[N], nt[N], nbt[N];
-    xtrace<P, true>(u, lt);
-    xtrace<P, false>(u, rt);
-    ytrace<P, true>(u, bt);
-    ytrace<P, false>(u, tt);
-    tile(i - 1, j, nb);
-    xtrace<P, false>(nb, nr);        // left neighbour's R trace
-    tile(i + 1, j, nb);
-    xtrace<P, true>(nb, nl);         // right neighbour's L trace
-    tile(i, j - 1, nb);
-    ytrace<P, false>(nb, nt);        // lower neighbour's top trace
-    tile(i, j + 1, nb);
-    ytrace<P, true>(nb, nbt);        // upper neighbour's bottom trace
-    // volume: sum_k Dx[i][k] F[k][j] + sum_k dh[j][k] G[i][k]
-    double acc[N][N];
 #pragma unroll
-    for (int ii = 0; ii < N; ++ii)
+        for (int ii = 0; ii < N; ++ii)
 #pragma unroll
-        for (int jj = 0; jj < N; ++jj) {
-            double e = 0.0;
+            for (int jj = 0; jj < N; ++jj) {
+                double e = acc[ii][jj];
 #pragma unroll
-            for (int k = 0; k < N; ++k) e = fma(ap.cx * c_nod[P].dh[ii][k], ap.bx * u[k][jj], e);
+                for (int k = 0; k < N; ++k) e = fma(ap.cx * c_nod[P].dh[ii][k], ap.bx * u[k][jj], e);
 #pragma unroll
-            for (int k = 0; k < N; ++k) e = fma(c_nod[P].dh[jj][k], ap.cy * ap.by * u[ii][k], e);
-            acc[ii][jj] = e;
-        }
-    // faces (lower / left element = "in"), lifted along xi / eta with mu
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-        const double fl = adv_flux(nr[q], lt[q], ap.bx, ap.bdy);
-        const double fr = adv_flux(rt[q], nl[q], ap.bx, ap.bdy);
-        const double fb = adv_flux(nt[q], bt[q], ap.by, ap.bdx);
-        const double ft = adv_flux(tt[q], nbt[q], ap.by, ap.bdx);
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-            acc[k][q] = fma(c_nod[P].mu[k], fl, fma(-c_nod[P].mu[N - 1 - k], fr, acc[k][q]));
-            acc[q][k] = fma(c_nod[P].mu[k], fb, fma(-c_nod[P].mu[N - 1 - k], ft, acc[q][k]));
-        }
+                for (int k = 0; k < N; ++k) e = fma(c_nod[P].dh[jj][k], ap.cy * ap.by * u[ii][k], e);
+                acc[ii][jj] = e;
+            }
     }
     // RHS at the nodes (diagonal mass), back to modes, stage combination
 #pragma unroll
@@ -95,15 +130,14 @@ __global__ void __launch_bounds__(128) adv_stage_kernel(AdvParams ap)
 #pragma unroll
         for (int jj = 0; jj < N; ++jj) acc[ii][jj] *= ap.inv_determ;
     to_modal<P>(acc);
-    const double *xm = ap.X + zoff + (size_t)j * NP * ap.nx + i;
     const double *um = ap.U ? ap.U + zoff + (size_t)j * NP * ap.nx + i : nullptr;
     double *ym = ap.Y + zoff + (size_t)j * NP * ap.nx + i;
 #pragma unroll
     for (int a = 0; a < N; ++a)
 #pragma unroll
         for (int b = 0; b < N; ++b) {
-            const size_t o = (size_t)(a * N + b) * ap.nx;
-            double y = fma(ap.b, xm[o], ap.g * acc[a][b]);
+            const size_t o = (size_t)(a * N + b) * ms;
+            double y = fma(ap.b, self[o], ap.g * acc[a][b]);
             if (um) y = fma(ap.a, um[o], y);
             ym[o] = y;
         }
