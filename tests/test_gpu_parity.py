@@ -541,12 +541,13 @@ def test_host_state_step_pipelined(P, case, nx, ny, p, nz, chunks):
 
 
 @pytest.mark.parametrize("p", [0, 1])
-@pytest.mark.parametrize("nx", [31, 32, 33, 64, 97])
+@pytest.mark.parametrize("nx", [1, 2, 29, 30, 31, 32, 33, 60, 61, 64, 97])
 def test_low_order_kernel_bitwise(P, p, nx, monkeypatch):
     """p <= 1 nodal stages run on the barrier-free low-order kernel
     (csrc/dgswe_lo.cuh); it must give the main kernel's bits: same traces,
     face arithmetic, volume and stage combination, different data path
-    (partial strips, strip borders, poles, check_mean)."""
+    (partial strips, the low-order kernel's 30-element segments and their
+    halo lanes, periodic wrap at nx = 1, 2, poles, check_mean)."""
     ny = 12
     setup = P.build_case(P.default_config("williamson_tc6").override(nx=nx, ny=ny, p=p))
     out = []
@@ -559,5 +560,20 @@ def test_low_order_kernel_bitwise(P, p, nx, monkeypatch):
         op.rk_steps(st, 20.0, 1, order=1)
         flags, _ = op.status()
         assert flags == 0
+        out.append(st.to_numpy())
+    assert np.array_equal(out[0], out[1])
+
+
+def test_low_order_kernel_levels_bitwise(P, monkeypatch):
+    """nz = 2 levels (blockIdx.z) on the low-order kernel, against the main kernel."""
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=45, ny=10, p=0))
+    out = []
+    for no_lo in ("1", "0"):
+        monkeypatch.setenv("DGSWE_NO_LO", no_lo)
+        op = P.SpatialOperator(setup.mesh, 0, setup.model, nz=2)
+        st = op.project_state(setup.ic)
+        st.data[1] *= 1.5
+        op.ssprk3_steps(st, 20.0, 3, check_mean=True)
+        assert op.status()[0] == 0
         out.append(st.to_numpy())
     assert np.array_equal(out[0], out[1])
