@@ -9,10 +9,12 @@
 // lanes 1..30 own elements 30 s .. 30 s + 29, lanes 0 and 31 hold their
 // periodic neighbours (read like the owned ones, never stored).  Its loads
 // go through a per-warp ring of kLoDepth rows in shared memory filled by
-// cp.async (LDGSTS) kLoDepth - 1 rows ahead (each lane reads back only its
-// own words: no warp barrier).  C5 p = 0 (1e9 DOF): 0.29 of the roofline
+// cp.async (LDGSTS) kLoDepth - 1 rows ahead, the row's table included
+// (X and u^n are read back only by the lane that copied them; the table by
+// all lanes after a __syncwarp).  C5 p = 0 (1e9 DOF): 0.29 of the roofline
 // with one row loaded and consumed per iteration, 0.36 with the ring, 0.47
-// with the halo lanes and shared reciprocals (below).
+// with the halo lanes and shared reciprocals (below), 0.58 with the staged
+// row tables at 4 CTAs per SM.
 //
 // Per row j (nodal values; SAME arithmetic as the main kernel -- the traces
 // of dgswe_kernels.cuh, face_core_rc, volume<> and the finalize order -- so
@@ -46,11 +48,12 @@ namespace dgswe {
 
 constexpr int kLoWarps = 4;   // strips per CTA
 // rows per warp in the shared-memory ring (kLoDepth - 1 in flight) and
-// resident CTAs per SM: measured at C5 p = 0 (1e9 DOF), depth 3..8 with
-// 1 / 6 / 8 CTAs: 4 rows with 6 CTAs (78 registers, no spill) best, deeper
-// rings slower (more open DRAM pages per SM), 8 CTAs spill
+// resident CTAs per SM, measured at C5 p = 0 (1e9 DOF, halo-lane kernel
+// with staged row tables): 6 CTAs (80 registers, small spills) 0.45, 5
+// (no spill) 0.49-0.51, 4 (104 registers) 0.57-0.59, 3 0.57; ring depth 3
+// 0.56, 4 and 6 equal
 constexpr int kLoDepth = 4;
-constexpr int kLoMinBlocks = 6;
+constexpr int kLoMinBlocks = 4;
 constexpr int kLoOwn = kLanes - 2;   // elements a warp owns: lanes 1..30 (lanes 0 / 31: neighbours)
 
 // warp segments of kLoOwn elements covering a row
@@ -64,11 +67,11 @@ template <int P, bool HAS_U>
 constexpr int lo_smem_bytes()
 {
     constexpr int NP = (P + 1) * (P + 1);
-    return kLoWarps * kLoDepth * (HAS_U ? 2 : 1) * 3 * NP * kLanes * (int)sizeof(double);
+    return kLoWarps * kLoDepth * ((HAS_U ? 2 : 1) * 3 * NP * kLanes + RowLayout<P>::SSTRIDE) * (int)sizeof(double);
 }
 
 
-// the degrees the low-order kernel serves: p = 0 (1.7x the main kernel);
+// the degrees the low-order kernel serves: p = 0 (2.2x the main kernel at C5);
 // at p = 1 the main kernel is faster (the one-thread element carries 4x the
 // registers and the per-row dependency chain gets 4x longer)
 template <int P>
@@ -156,11 +159,14 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
     unsigned bad = 0;
 
     // per-warp ring of kLoDepth rows in shared memory, filled with cp.async
-    // (LDGSTS) kLoDepth - 1 rows ahead: row r's X and u^n, one commit group
-    // per row; each lane reads back only the words it copied itself
+    // (LDGSTS) kLoDepth - 1 rows ahead: row r's X, u^n and row table, one
+    // commit group per row; X and u^n are read back only by the lane that
+    // copied them, the row table by all lanes (after a __syncwarp)
     extern __shared__ __align__(16) double lo_smem[];
     constexpr int ROWW = 3 * NP * kLanes;
-    constexpr int SLOT = (HAS_U ? 2 : 1) * ROWW;
+    constexpr int TBL = (HAS_U ? 2 : 1) * ROWW;                 // row table [RL::SSTRIDE]
+    constexpr int SLOT = TBL + RL::SSTRIDE;
+    static_assert(RL::SSTRIDE <= kLanes, "one row-table word per lane");
     double *ring = lo_smem + (threadIdx.x >> 5) * (kLoDepth * SLOT);
     const int x_last = min(je, r_last);                         // rows whose X is read
     auto issue = [&](int r, int slot) {
@@ -172,6 +178,7 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
 #pragma unroll
                 for (int m = 0; m < NP; ++m)
                     cp_async8(d + (v * NP + m) * kLanes + lane, xr + (size_t)v * kp.vstride + m * kLanes);
+            if (lane < RL::SSTRIDE) cp_async8(d + TBL + lane, kp.rowtab + (size_t)(kp.row0 + r) * RL::STRIDE + lane);
             if constexpr (HAS_U) {
                 if (r < je && owned) {
                     const double *ur = kp.U + eoff + (size_t)r * kp.rstride;
@@ -231,8 +238,12 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
         const bool has_next = j + 1 <= r_last;
         const int slot1 = slot + 1 == kLoDepth ? 0 : slot + 1;
         const int slotD = slot == 0 ? kLoDepth - 1 : slot - 1;   // row j + kLoDepth - 1
+        __syncwarp();                                            // every lane is done with row j-1's slot
         issue(j + kLoDepth - 1, slotD);
         cp_wait<kLoDepth - 2>();                                 // rows <= j + 1 have landed
+        __syncwarp();                                            // (the row tables: other lanes' copies)
+        const double *rw = ring + slot * SLOT + TBL;             // row j's table, row j+1's next
+        const double *ra = ring + slot1 * SLOT + TBL;
         if (has_next) {
             const double *d = ring + slot1 * SLOT;
 #pragma unroll
@@ -249,7 +260,6 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
                 for (int m = 0; m < NP; ++m) un[v][m] = d[(v * NP + m) * kLanes + lane];
         }
         slot = slot1;
-        const double *rw = kp.rowtab + (size_t)(kp.row0 + j) * RL::STRIDE;
         bad |= owned & lo_positive<P>(cur[0], NP);
         // x-faces: lane l (0..nvalid) evaluates the face between lanes l and
         // l+1 from its own traces and lane l+1's (shuffled with its
@@ -283,7 +293,6 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
         if (has_next) {
             traces(nxt, trn, rn, cn);
             bad |= owned & lo_positive<P>(trn[0], N);
-            const double *ra = rw + RL::STRIDE;
             const FaceArgs fy{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r, kp.alpha_mode,
                               1, ra[RL::CRB], ra[RL::COSB], alpha_y, kp.bdx};
             double fh[N], fn[N], ft[N];
