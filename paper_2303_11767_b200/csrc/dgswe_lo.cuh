@@ -1,30 +1,31 @@
-// dgswe_lo.cuh -- low-order (p = 0) stage kernel for sm_100a.
+// dgswe_lo.cuh -- low-order (p = 0, 1) stage kernel for sm_100a.
 //
-// At p = 0 an element has one node per variable: the warp-specialised
+// At p <= 1 an element has 1-4 nodes per variable: the warp-specialised
 // kernel (dgswe_kernels.cuh) then spends its time on per-row barriers, ring
-// waits and one face evaluation per node, not on HBM (C5 sweep: 26% of the
-// roofline).  Here ONE thread owns one element with all three variables
+// waits and one face evaluation per 1-2 nodes, not on HBM (C5 sweep: 26% /
+// 51% of the roofline).  Here ONE thread owns one element with all three variables
 // in registers and there is no CTA barrier: warp w of a CTA marches north
 // through a chunk of rows of segment 4 blockIdx.x + w, 30 elements wide:
 // lanes 1..30 own elements 30 s .. 30 s + 29, lanes 0 and 31 hold their
 // periodic neighbours (read like the owned ones, never stored).  Its loads
-// go through a per-warp ring of kLoDepth rows in shared memory filled by
-// cp.async (LDGSTS) kLoDepth - 1 rows ahead, the row's table included
+// go through a per-warp ring of lo_depth<P>() rows in shared memory filled by
+// cp.async (LDGSTS) depth - 1 rows ahead, the row's table included
 // (X and u^n are read back only by the lane that copied them; the table by
 // all lanes after a __syncwarp).  C5 p = 0 (1e9 DOF): 0.29 of the roofline
 // with one row loaded and consumed per iteration, 0.36 with the ring, 0.47
 // with the halo lanes and shared reciprocals (below), 0.58 with the staged
-// row tables at 4 CTAs per SM.
+// row tables at 4 CTAs per SM; p = 1: 0.65 (the main kernel 0.51).
 //
 // Per row j (nodal values; SAME arithmetic as the main kernel -- the traces
 // of dgswe_kernels.cuh, face_core_rc, volume<> and the finalize order -- so
 // both kernels give identical bits):
-//   * at p = 0 all four traces of an element are its value (l_0 = 1), so
-//     1/h and sqrt(h) (inv_and_sqrt) are formed ONCE per element and row and
-//     shared: the right neighbour's by shuffle, the next row's computed for
-//     the y-face and carried up as that row's own (the main kernel forms
-//     them per face side: identical bits, the face fuses sqrt(g) sqrt(h)
-//     explicitly);
+//   * each trace node's 1/h and sqrt(h) (inv_and_sqrt) is formed once, by
+//     its own element (lo_side): the x-face takes lane l+1's L side with
+//     them by shuffle, the y-face the next row's B side (the main kernel
+//     forms them inside each face: identical bits, the face fuses
+//     sqrt(g) sqrt(h) explicitly).  At p = 0 all four sides of an element
+//     are its value (l_0 = 1): one set per element and row, the next row's
+//     carried up as that row's own;
 //   * row j+1 (coalesced: one 256-byte line per variable) has landed in the
 //     ring while row j is computed; its traces and row j's give the y-face
 //     above row j, carried in registers as the next row's bottom face (each
@@ -47,13 +48,20 @@
 namespace dgswe {
 
 constexpr int kLoWarps = 4;   // strips per CTA
-// rows per warp in the shared-memory ring (kLoDepth - 1 in flight) and
-// resident CTAs per SM, measured at C5 p = 0 (1e9 DOF, halo-lane kernel
-// with staged row tables): 6 CTAs (80 registers, small spills) 0.45, 5
-// (no spill) 0.49-0.51, 4 (104 registers) 0.57-0.59, 3 0.57; ring depth 3
-// 0.56, 4 and 6 equal
-constexpr int kLoDepth = 4;
-constexpr int kLoMinBlocks = 4;
+// rows per warp in the shared-memory ring (depth - 1 in flight) and
+// resident CTAs per SM (register cap), per degree and variant, measured at
+// C5 (1e9 DOF):
+//   p = 0: depth 4, 4 CTAs (104 registers): 0.57-0.59 of the roofline (6
+//          CTAs at 80 registers spilled: 0.45; 5: 0.49-0.51; 3: 0.57;
+//          depth 3: 0.56, 6: equal);
+//   p = 1: depth 3; the stage without u^n 3 CTAs (166 registers), with u^n
+//          2 (212; its ring takes 75 KB): 0.65 (both at 2: 0.63, both at 3:
+//          0.58; depth 4: 0.47), the main kernel 0.51.
+template <int P> __host__ __device__ constexpr int lo_depth() { return P == 0 ? 4 : 3; }
+template <int P, int F> __host__ __device__ constexpr int lo_min_blocks()
+{
+    return P == 0 ? 4 : ((F & kHasU) ? 2 : 3);
+}
 constexpr int kLoOwn = kLanes - 2;   // elements a warp owns: lanes 1..30 (lanes 0 / 31: neighbours)
 
 // warp segments of kLoOwn elements covering a row
@@ -67,15 +75,14 @@ template <int P, bool HAS_U>
 constexpr int lo_smem_bytes()
 {
     constexpr int NP = (P + 1) * (P + 1);
-    return kLoWarps * kLoDepth * ((HAS_U ? 2 : 1) * 3 * NP * kLanes + RowLayout<P>::SSTRIDE) * (int)sizeof(double);
+    return kLoWarps * lo_depth<P>() * ((HAS_U ? 2 : 1) * 3 * NP * kLanes + RowLayout<P>::SSTRIDE) * (int)sizeof(double);
 }
 
 
-// the degrees the low-order kernel serves: p = 0 (2.2x the main kernel at C5);
-// at p = 1 the main kernel is faster (the one-thread element carries 4x the
-// registers and the per-row dependency chain gets 4x longer)
+// the degrees the low-order kernel serves: p = 0 (2.2x the main kernel at
+// C5) and p = 1 (1.27x); p = 2 would need 255 registers and spill
 template <int P>
-__host__ __device__ constexpr bool lo_kernel_degree() { return P == 0; }
+__host__ __device__ constexpr bool lo_kernel_degree() { return P <= 1; }
 
 // all three variables of element e of a row (row pointer: level and row
 // applied), nodal slots m = i N + j
@@ -111,6 +118,26 @@ __device__ __forceinline__ void lo_xtraces(const double (&u)[3][(P + 1) * (P + 1
     }
 }
 
+// one side's traces of all three variables (SIDE 0 / 1: xi = -1 / +1,
+// 2 / 3: eta = -1 / +1) with 1/h and sqrt(h) of its h nodes (inv_and_sqrt)
+template <int P, int SIDE>
+__device__ __forceinline__ void lo_side(const double (&u)[3][(P + 1) * (P + 1)], double (&t)[3][P + 1],
+                                        double (&r)[P + 1], double (&c)[P + 1], double h_floor, double inv_floor)
+{
+    if constexpr (SIDE <= 1) {
+        lo_xtraces<P, SIDE == 0>(u, t);
+    } else {
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+            double tile[P + 1][P + 1];
+            lo_tile<P>(u[v], tile);
+            ytrace<P, SIDE == 2>(tile, t[v]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < P + 1; ++k) inv_and_sqrt(t[0][k], h_floor, inv_floor, r[k], c[k]);
+}
+
 template <int P>
 __device__ __forceinline__ unsigned lo_positive(const double *x, int n)
 {
@@ -121,9 +148,9 @@ __device__ __forceinline__ unsigned lo_positive(const double *x, int n)
 }
 
 template <int P, int F>
-__global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kernel(StageParams kp)
+__global__ void __launch_bounds__(kLoWarps * kLanes, lo_min_blocks<P, F>()) lo_stage_kernel(StageParams kp)
 {
-    static_assert(P == 0, "low-order kernel: one node per element");
+    static_assert(P <= 1, "low-order kernel");
     static_assert((F & ~kHasU) == 0, "low-order kernel: nodal stages with or without u^n only");
     constexpr bool HAS_U = (F & kHasU) != 0;
     constexpr int N = P + 1;
@@ -158,8 +185,8 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
     const double alpha_y = kp.alpha_mode == 2 ? kp.alpha_dev[1] : kp.alpha;
     unsigned bad = 0;
 
-    // per-warp ring of kLoDepth rows in shared memory, filled with cp.async
-    // (LDGSTS) kLoDepth - 1 rows ahead: row r's X, u^n and row table, one
+    // per-warp ring of lo_depth<P>() rows in shared memory, filled with cp.async
+    // (LDGSTS) depth - 1 rows ahead: row r's X, u^n and row table, one
     // commit group per row; X and u^n are read back only by the lane that
     // copied them, the row table by all lanes (after a __syncwarp)
     extern __shared__ __align__(16) double lo_smem[];
@@ -167,7 +194,7 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
     constexpr int TBL = (HAS_U ? 2 : 1) * ROWW;                 // row table [RL::SSTRIDE]
     constexpr int SLOT = TBL + RL::SSTRIDE;
     static_assert(RL::SSTRIDE <= kLanes, "one row-table word per lane");
-    double *ring = lo_smem + (threadIdx.x >> 5) * (kLoDepth * SLOT);
+    double *ring = lo_smem + (threadIdx.x >> 5) * (lo_depth<P>() * SLOT);
     const int x_last = min(je, r_last);                         // rows whose X is read
     auto issue = [&](int r, int slot) {
         double *d = ring + slot * SLOT;
@@ -193,28 +220,24 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
         cp_commit();
     };
 #pragma unroll 1
-    for (int k = 0; k < kLoDepth - 1; ++k) issue(jb + k, k);
+    for (int k = 0; k < lo_depth<P>() - 1; ++k) issue(jb + k, k);
 
-    // row values, their (identical) traces and the reciprocal / celerity of
-    // the h trace, computed once per element and row: the x-face takes the
-    // right neighbour's by shuffle, the y-face the next row's, which is then
-    // carried up as the next row's own
-    auto traces = [&](const double (&u)[3][NP], double (&t)[3][N], double (&r)[N], double (&c)[N]) {
-        lo_xtraces<P, false>(u, t);
-#pragma unroll
-        for (int k = 0; k < N; ++k) inv_and_sqrt(t[0][k], kp.h_floor, kp.inv_floor, r[k], c[k]);
-    };
+    // traces with 1/h and sqrt(h) of their h nodes, computed once per
+    // element side and row: the x-face takes the right neighbour's L side
+    // by shuffle, the y-face the next row's B side.  At p = 0 all four
+    // sides are the element's value (l_0 = 1): one set per element, the
+    // next row's carried up as that row's own (tr / rr / cc)
     double cur[3][NP], nxt[3][NP];
     lo_load<P>(kp.X + (size_t)jb * kp.rstride + (size_t)blockIdx.z * kp.zstride, kp.vstride, g, cur);
-    double tr[3][N], rr[N], cc[N];
-    traces(cur, tr, rr, cc);
+    double tr[3][N], rr[N], cc[N];                               // row jb's B side (p = 0: every side)
+    lo_side<P, 2>(cur, tr, rr, cc, kp.h_floor, kp.inv_floor);
     bad |= owned & lo_positive<P>(tr[0], N);
     // the face below row jb: row jb-1's top traces against row jb's bottom ones
     double fbot[3][N];
     if (kp.row0 + jb > 0) {
         double below[3][NP], tb[3][N], rb[N], cb[N];
         lo_load<P>(kp.X + (size_t)(jb - 1) * kp.rstride + (size_t)blockIdx.z * kp.zstride, kp.vstride, g, below);
-        traces(below, tb, rb, cb);
+        lo_side<P, 3>(below, tb, rb, cb, kp.h_floor, kp.inv_floor);
         const double *rw = kp.rowtab + (size_t)(kp.row0 + jb) * RL::STRIDE;
         const FaceArgs fy{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r, kp.alpha_mode,
                           1, rw[RL::CRB], rw[RL::COSB], alpha_y, kp.bdx};
@@ -236,11 +259,11 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
     int slot = 0;                                                // ring slot of row j
     for (int j = jb; j < je; ++j) {
         const bool has_next = j + 1 <= r_last;
-        const int slot1 = slot + 1 == kLoDepth ? 0 : slot + 1;
-        const int slotD = slot == 0 ? kLoDepth - 1 : slot - 1;   // row j + kLoDepth - 1
+        const int slot1 = slot + 1 == lo_depth<P>() ? 0 : slot + 1;
+        const int slotD = slot == 0 ? lo_depth<P>() - 1 : slot - 1;   // row j + lo_depth<P>() - 1
         __syncwarp();                                            // every lane is done with row j-1's slot
-        issue(j + kLoDepth - 1, slotD);
-        cp_wait<kLoDepth - 2>();                                 // rows <= j + 1 have landed
+        issue(j + lo_depth<P>() - 1, slotD);
+        cp_wait<lo_depth<P>() - 2>();                                 // rows <= j + 1 have landed
         __syncwarp();                                            // (the row tables: other lanes' copies)
         const double *rw = ring + slot * SLOT + TBL;             // row j's table, row j+1's next
         const double *ra = ring + slot1 * SLOT + TBL;
@@ -261,6 +284,23 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
         }
         slot = slot1;
         bad |= owned & lo_positive<P>(cur[0], NP);
+        // row j's R side (x-face in), L side (the left neighbour's out) and
+        // T side (y-face in)
+        double tR[3][N], rR[N], cR[N], tL[3][N], rL[N], cL[N], tT[3][N], rT[N], cT[N];
+        if constexpr (P == 0) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+#pragma unroll
+                for (int v = 0; v < 3; ++v) tR[v][k] = tL[v][k] = tT[v][k] = tr[v][k];
+                rR[k] = rL[k] = rT[k] = rr[k];
+                cR[k] = cL[k] = cT[k] = cc[k];
+            }
+        } else {
+            lo_side<P, 1>(cur, tR, rR, cR, kp.h_floor, kp.inv_floor);
+            lo_side<P, 0>(cur, tL, rL, cL, kp.h_floor, kp.inv_floor);
+            lo_side<P, 3>(cur, tT, rT, cT, kp.h_floor, kp.inv_floor);
+            bad |= owned & (lo_positive<P>(tR[0], N) | lo_positive<P>(tL[0], N) | lo_positive<P>(tT[0], N));
+        }
         // x-faces: lane l (0..nvalid) evaluates the face between lanes l and
         // l+1 from its own traces and lane l+1's (shuffled with its
         // reciprocal and celerity); an owned lane's left face is lane l-1's
@@ -269,14 +309,14 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
             double ho[N], no[N], to[N], ro[N], co[N];
 #pragma unroll
             for (int k = 0; k < N; ++k) {
-                ho[k] = __shfl_down_sync(0xffffffffu, tr[0][k], 1);
-                no[k] = __shfl_down_sync(0xffffffffu, tr[1][k], 1);
-                to[k] = __shfl_down_sync(0xffffffffu, tr[2][k], 1);
-                ro[k] = __shfl_down_sync(0xffffffffu, rr[k], 1);
-                co[k] = __shfl_down_sync(0xffffffffu, cc[k], 1);
+                ho[k] = __shfl_down_sync(0xffffffffu, tL[0][k], 1);
+                no[k] = __shfl_down_sync(0xffffffffu, tL[1][k], 1);
+                to[k] = __shfl_down_sync(0xffffffffu, tL[2][k], 1);
+                ro[k] = __shfl_down_sync(0xffffffffu, rL[k], 1);
+                co[k] = __shfl_down_sync(0xffffffffu, cL[k], 1);
             }
             double fh[N], fn[N], ft[N];
-            face_core_rc<P>(tr[0], tr[1], tr[2], rr, cc, ho, no, to, ro, co, fx, fh, fn, ft);
+            face_core_rc<P>(tR[0], tR[1], tR[2], rR, cR, ho, no, to, ro, co, fx, fh, fn, ft);
 #pragma unroll
             for (int k = 0; k < N; ++k) {
                 fr[0][k] = fh[k];
@@ -291,12 +331,12 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, kLoMinBlocks) lo_stage_kern
         // the y-face above row j (zero at the pole), carried to the next row
         double ftop[3][N], trn[3][N], rn[N], cn[N];
         if (has_next) {
-            traces(nxt, trn, rn, cn);
+            lo_side<P, 2>(nxt, trn, rn, cn, kp.h_floor, kp.inv_floor);
             bad |= owned & lo_positive<P>(trn[0], N);
             const FaceArgs fy{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r, kp.alpha_mode,
                               1, ra[RL::CRB], ra[RL::COSB], alpha_y, kp.bdx};
             double fh[N], fn[N], ft[N];
-            face_core_rc<P>(tr[0], tr[2], tr[1], rr, cc, trn[0], trn[2], trn[1], rn, cn, fy, fh, fn, ft);
+            face_core_rc<P>(tT[0], tT[2], tT[1], rT, cT, trn[0], trn[2], trn[1], rn, cn, fy, fh, fn, ft);
 #pragma unroll
             for (int k = 0; k < N; ++k) {
                 ftop[0][k] = fh[k];
