@@ -126,6 +126,7 @@ struct AdvParams {
     double bdx, bdy;                   // face Jacobians dx/2, dy/2
     double cx, cy;                     // determ / bd_det_x, determ / bd_det_y (dg.py:199-202)
     double inv_determ;                 // the nodal mass 1 / determ
+    int rc;                            // rows per CTA (row-marching kernel)
 };
 
 // strided view of a state for the diagnostics / projection kernels
