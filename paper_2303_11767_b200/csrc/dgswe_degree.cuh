@@ -153,7 +153,7 @@ template <int P, int F>
 int launch_variant(dgswe_ctx *c, const StageParams &kp0, cudaStream_t s)
 {
     if constexpr (dgswe::lo_kernel_degree<P>() && (F & ~dgswe::kHasU) == 0) {
-        if (!c->no_lo && !kp0.periodic_y && kp0.j_end2 <= kp0.j_begin2) return launch_lo<P, F>(c, kp0, s);
+        if (!c->no_lo && kp0.j_end2 <= kp0.j_begin2) return launch_lo<P, F>(c, kp0, s);
     }
     const int o = occupancy<P, F>(c);
     if (o < 0) return o;

@@ -179,7 +179,10 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, lo_min_blocks<P, F>()) lo_s
         je = min(jb + kp.rc, kp.j_end);
     }
     if (jb >= je) return;
-    const int r_last = min(kp.nrows - 1, kp.ny - 1 - kp.row0);      // local rows with coefficients
+    // the plane (periodic_y, one context per grid): rows wrap, no pole faces
+    const bool yper = kp.periodic_y != 0;
+    auto wrap = [&](int r) { return yper ? (r + kp.ny) % kp.ny : r; };
+    const int r_last = yper ? je : min(kp.nrows - 1, kp.ny - 1 - kp.row0);   // local rows with coefficients
     const FaceArgs fx{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r, kp.alpha_mode, 0,
                       0.0, 0.0, kp.alpha_mode == 2 ? kp.alpha_dev[0] : kp.alpha, kp.bdy};
     const double alpha_y = kp.alpha_mode == 2 ? kp.alpha_dev[1] : kp.alpha;
@@ -199,13 +202,13 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, lo_min_blocks<P, F>()) lo_s
     auto issue = [&](int r, int slot) {
         double *d = ring + slot * SLOT;
         if (r <= x_last) {
-            const double *xr = kp.X + eoff + (size_t)r * kp.rstride;
+            const double *xr = kp.X + eoff + (size_t)wrap(r) * kp.rstride;
 #pragma unroll
             for (int v = 0; v < 3; ++v)
 #pragma unroll
                 for (int m = 0; m < NP; ++m)
                     cp_async8(d + (v * NP + m) * kLanes + lane, xr + (size_t)v * kp.vstride + m * kLanes);
-            if (lane < RL::SSTRIDE) cp_async8(d + TBL + lane, kp.rowtab + (size_t)(kp.row0 + r) * RL::STRIDE + lane);
+            if (lane < RL::SSTRIDE) cp_async8(d + TBL + lane, kp.rowtab + (size_t)wrap(kp.row0 + r) * RL::STRIDE + lane);
             if constexpr (HAS_U) {
                 if (r < je && owned) {
                     const double *ur = kp.U + eoff + (size_t)r * kp.rstride;
@@ -234,9 +237,9 @@ __global__ void __launch_bounds__(kLoWarps * kLanes, lo_min_blocks<P, F>()) lo_s
     bad |= owned & lo_positive<P>(tr[0], N);
     // the face below row jb: row jb-1's top traces against row jb's bottom ones
     double fbot[3][N];
-    if (kp.row0 + jb > 0) {
+    if (yper || kp.row0 + jb > 0) {
         double below[3][NP], tb[3][N], rb[N], cb[N];
-        lo_load<P>(kp.X + (size_t)(jb - 1) * kp.rstride + (size_t)blockIdx.z * kp.zstride, kp.vstride, g, below);
+        lo_load<P>(kp.X + (size_t)wrap(jb - 1) * kp.rstride + (size_t)blockIdx.z * kp.zstride, kp.vstride, g, below);
         lo_side<P, 3>(below, tb, rb, cb, kp.h_floor, kp.inv_floor);
         const double *rw = kp.rowtab + (size_t)(kp.row0 + jb) * RL::STRIDE;
         const FaceArgs fy{kp.h_floor, kp.inv_floor, kp.sqrt_g, kp.half_g, kp.inv_r, kp.alpha_mode,

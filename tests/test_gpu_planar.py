@@ -110,3 +110,20 @@ def test_planar_device_projection(P, gold):
     got = op.project_state(setup.ic, device=True).to_numpy()
     ref = gold[f"{name}/x0"]
     assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("p", [0, 1])
+@pytest.mark.parametrize("nx", [29, 33])
+def test_planar_low_order_kernel_bitwise(P, monkeypatch, p, nx):
+    """The low-order kernel on the plane (rows wrap) against the main kernel."""
+    setup = P.build_case(P.default_config("geostrophic_adjustment").override(nx=nx, ny=9, p=p))
+    out = []
+    for no_lo in ("1", "0"):
+        monkeypatch.setenv("DGSWE_NO_LO", no_lo)
+        op = P.SpatialOperator(setup.mesh, p, setup.model)
+        st = op.project_state(setup.ic)
+        op.ssprk3_steps(st, 400.0, 4, check_mean=True)
+        op.rk_steps(st, 400.0, 1, order=2)
+        assert op.status()[0] == 0
+        out.append(st.to_numpy())
+    assert np.array_equal(out[0], out[1])
