@@ -205,14 +205,15 @@ def test_row_chunk_invariance(P, golden, oracle_mod, rc):
     assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("p", [0, 1, 3])
 @pytest.mark.parametrize("world", [2, 3, 5])
-def test_band_decomposition_bitwise(P, oracle_mod, world):
+def test_band_decomposition_bitwise(P, oracle_mod, world, p):
     """Latitude bands with halo rows (one context per band, as on one GPU of
     a multi-GPU run) reproduce the single-band stage bit for bit, including
     the interior/boundary split used to overlap the halo exchange."""
     from paper_2303_11767_b200.bands import BandLayout, BandOperator
-    setup = P.build_case(P.default_config("williamson_tc6").override(nx=64, ny=21, p=3, nz=2))
-    op = P.SpatialOperator(setup.mesh, 3, setup.model, nz=2)
+    setup = P.build_case(P.default_config("williamson_tc6").override(nx=64, ny=21, p=p, nz=2))
+    op = P.SpatialOperator(setup.mesh, p, setup.model, nz=2)
     st = op.project_state(setup.ic)
     st.data[1] *= 1.0001
     full = st.data.cpu().numpy()
