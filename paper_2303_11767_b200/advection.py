@@ -85,7 +85,9 @@ class AdvectionOperator:
         if not torch.cuda.is_available():
             raise RuntimeError("AdvectionOperator needs a CUDA device (no CPU fallback)")
         self.mesh, self.p, self.model, self.nz = mesh, int(p), model, int(nz)
-        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.device = torch.device("cuda") if device is None else torch.device(device)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.quad = gauss_legendre(self.p + 1)
         self.vander = build_vander(self.p, self.quad)
         self.nphi = self.vander.nphi
@@ -133,12 +135,17 @@ class AdvectionOperator:
         return self.state_from_coeffs({"u": project_initial(ic_funcs["u"], self.mesh, self.vander)})
 
     def stage(self, a: float, U: AdvState | None, b: float, X: AdvState, g: float, Y: AdvState):
-        """Y = a U + b X + g RHS(X) in one launch."""
-        _lib.check(self.lib.dgswe_adv_stage(self._h, float(a), ctypes.c_void_p(U.data.data_ptr() if U else 0),
-                                            float(b), ctypes.c_void_p(X.data.data_ptr()), float(g),
-                                            ctypes.c_void_p(Y.data.data_ptr()),
-                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
-                   "dgswe_adv_stage")
+        """Y = a U + b X + g RHS(X) in one launch (U may alias Y, X may not)."""
+        for s in (U, X, Y):
+            if s is not None and (tuple(s.data.shape) != self.state_shape or s.data.device != self.device
+                                  or not s.data.is_contiguous()):
+                raise ValueError(f"states must be contiguous {self.state_shape} float64 tensors on {self.device}")
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.dgswe_adv_stage(self._h, float(a), ctypes.c_void_p(U.data.data_ptr() if U else 0),
+                                                float(b), ctypes.c_void_p(X.data.data_ptr()), float(g),
+                                                ctypes.c_void_p(Y.data.data_ptr()),
+                                                ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                       "dgswe_adv_stage")
 
     def assemble_rhs(self, state: AdvState, out: AdvState | None = None) -> AdvState:
         """M^-1 (volume - boundary) of the advection operator (dg.py:504-523)."""
