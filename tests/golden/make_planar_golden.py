@@ -10,7 +10,9 @@ It imports ``dgswe`` from /root/reference/pkg/src read-only and writes
 coefficients, the right-hand side there, the state after N reference
 ``rk_step(tableau(3))`` steps (momentum non-zero by then) and the
 right-hand side of that state, and the right-hand sides of both states
-scaled by (1 + 2^-52) (the reference's own rounding sensitivity).  Arrays
+scaled by (1 + 2^-52) (the reference's own rounding sensitivity); for the
+first case also the RHS and 3 more steps from the N-step state with the
+global and a pinned Rusanov alpha.  Arrays
 are (3, nx, ny, nz, nphi) interior
 coefficients.  Nothing here is imported by the product.
 """
@@ -68,6 +70,31 @@ def main():
             out[f"{name}/rhs{tag}_ulp"] = coeffs_of(op.assemble_rhs(sp))
         out[f"{name}/meta"] = np.array([nx, ny, p, dt, nsteps])
         print(name, "done", flush=True)
+    # global Rusanov alpha (dg.py:385-421, mode "global") and a pinned one,
+    # on the state after N steps of the first case: RHS and 3 further steps
+    name, nx, ny, p, dt, nsteps = CASES[0]
+    for tag, rus in (("global", dg.RusanovParams("global")), ("pinned", dg.RusanovParams("global", 250.0))):
+        cfg = cases.default_config("geostrophic_adjustment").override(nx=nx, ny=ny, p=p)
+        setup = cases.build_case(cfg)
+        op = dg.SpatialOperator(setup.mesh, p, setup.model, rusanov=rus)
+        st = op.zero_state()
+        for v, nm in enumerate(st.names):
+            st.fields[nm].data[1:-1, 1:-1] = out[f"{name}/xn"][v]
+        out[f"{name}/{tag}/rhs"] = coeffs_of(op.assemble_rhs(st))
+        tab = timestep.tableau(3)
+        ws = timestep._RKWorkspace(st, tab.s)
+        for _ in range(3):
+            timestep.rk_step(st, op.assemble_rhs, dt, tab, ws)
+        out[f"{name}/{tag}/x3"] = coeffs_of(st)
+        # the reference's own 1-ulp sensitivity of those 3 steps (the gate's scale)
+        st = op.zero_state()
+        for v, nm in enumerate(st.names):
+            st.fields[nm].data[1:-1, 1:-1] = out[f"{name}/xn"][v] * (1.0 + 2.0 ** -52)
+        ws = timestep._RKWorkspace(st, tab.s)
+        for _ in range(3):
+            timestep.rk_step(st, op.assemble_rhs, dt, tab, ws)
+        out[f"{name}/{tag}/x3_ulp"] = coeffs_of(st)
+        print(name, tag, "done", flush=True)
     np.savez_compressed(os.path.join(HERE, "planar.npz"), **out)
 
 

@@ -127,3 +127,29 @@ def test_planar_low_order_kernel_bitwise(P, monkeypatch, p, nx):
         assert op.status()[0] == 0
         out.append(st.to_numpy())
     assert np.array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("tag", ["global", "pinned"])
+def test_planar_global_alpha_vs_reference(P, gold, tag):
+    """The reference's global Rusanov alpha (dg.py:385-421) and a pinned one
+    on the plane: one RHS and 3 Butcher-form steps from the N-step state."""
+    name = "adj_16x12_p3"
+    rus = P.RusanovParams("global") if tag == "global" else P.RusanovParams("global", 250.0)
+    setup, op, dt, nsteps = make(P, gold, name, rusanov=rus)
+    x = op.state_from_array(gold[f"{name}/xn"])
+    got = op.assemble_rhs(x).to_numpy()
+    ref = gold[f"{name}/{tag}/rhs"]
+    for v in range(3):
+        err = np.linalg.norm(got[v] - ref[v])
+        assert err <= 1e-10 * np.linalg.norm(ref[v]) + 1e-13 * np.linalg.norm(ref), (v, err)
+    tab = P.tableau(3)
+    ws = P.stepping._RKWorkspace(x, tab.s)
+    for _ in range(3):
+        P.rk_step(x, op.assemble_rhs, dt, tab, ws)
+    # within 20x the reference's own 1-ulp sensitivity of the same 3 steps
+    # (pinned alpha = 250: ~1.3e-10 relative in the momenta in the reference itself)
+    got, ref, ulp = x.to_numpy(), gold[f"{name}/{tag}/x3"], gold[f"{name}/{tag}/x3_ulp"]
+    for v in range(3):
+        err = np.linalg.norm(got[v] - ref[v])
+        sens = np.linalg.norm(ulp[v] - ref[v])
+        assert err <= 20.0 * sens + 1e-13 * np.linalg.norm(ref[v]), (v, err, sens)
