@@ -158,6 +158,10 @@ int dgswe_adv_create(const dgswe_adv_cfg *cfg, const double *leg, const double *
                      dgswe_adv_ctx **out);
 int dgswe_adv_stage(dgswe_adv_ctx *ctx, double a, const double *U, double b, const double *X, double g, double *Y,
                     void *stream);
+/* Pinned global Rusanov alpha for both directions (RusanovParams("global",
+ * alpha), dg.py:47-57, 389-392); default: |beta_x|, |beta_y| (the model's
+ * wavespeed: local and global modes coincide for constant beta). */
+int dgswe_adv_set_alpha(dgswe_adv_ctx *ctx, double alpha);
 void dgswe_adv_destroy(dgswe_adv_ctx *ctx);
 
 int dgswe_abi_version(void);

@@ -58,6 +58,7 @@ SIGNATURES = {
     "dgswe_destroy": (None, [_VP]),
     "dgswe_adv_create": (_I, [ctypes.POINTER(AdvCfg), _PD, _PD, _PD, ctypes.POINTER(_VP)]),
     "dgswe_adv_stage": (_I, [_VP, _D, _VP, _D, _VP, _D, _VP, _VP]),
+    "dgswe_adv_set_alpha": (_I, [_VP, _D]),
     "dgswe_adv_destroy": (None, [_VP]),
     "dgswe_state_elems": (ctypes.c_int64, [_VP]),
     "dgswe_rhs": (_I, [_VP, _VP, _VP, _VP]),

@@ -79,9 +79,14 @@ class AdvectionOperator:
     """DG operator of linear advection on a periodic planar mesh
     (the reference's SpatialOperator with an advection model, dg.py:166-543)."""
 
-    def __init__(self, mesh: Mesh, p: int, model: AdvectionModel, nz: int = 1, device=None):
+    def __init__(self, mesh: Mesh, p: int, model: AdvectionModel, rusanov=None, nz: int = 1, device=None):
+        """``rusanov``: RusanovParams (dg.py:47-57); "local" and "global" coincide
+        for constant beta (alpha = |beta_d| on every face), a pinned global
+        alpha replaces it in both directions."""
+        from .operator import RusanovParams
         if mesh.kind != "planar" or not isinstance(model, AdvectionModel):
             raise ValueError("linear advection runs on the periodic planar mesh")
+        self.rusanov = rusanov if rusanov is not None else RusanovParams()
         if not torch.cuda.is_available():
             raise RuntimeError("AdvectionOperator needs a CUDA device (no CPU fallback)")
         self.mesh, self.p, self.model, self.nz = mesh, int(p), model, int(nz)
@@ -104,6 +109,8 @@ class AdvectionOperator:
                        "dgswe_adv_create")
         self._h = handle
         self._ws = None
+        if self.rusanov.mode == "global" and self.rusanov.alpha is not None:
+            _lib.check(self.lib.dgswe_adv_set_alpha(self._h, float(self.rusanov.alpha)), "dgswe_adv_set_alpha")
 
     def __del__(self):
         h = getattr(self, "_h", None)

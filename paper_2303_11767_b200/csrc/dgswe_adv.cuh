@@ -25,11 +25,12 @@
 namespace dgswe {
 
 
-// Rusanov flux of u across a face with normal velocity bn, scaled by the
-// face Jacobian: scale (bn (in + out) / 2 - |bn| (out - in) / 2)
-__device__ __forceinline__ double adv_flux(double in, double out, double bn, double scale)
+// Rusanov flux of u across a face with normal velocity bn and
+// stabilisation alpha (|bn|, or a pinned global value), scaled by the face
+// Jacobian: scale (bn (in + out) / 2 - alpha (out - in) / 2)
+__device__ __forceinline__ double adv_flux(double in, double out, double bn, double alpha, double scale)
 {
-    return scale * fma(0.5 * bn, in + out, -0.5 * fabs(bn) * (out - in));
+    return scale * fma(0.5 * bn, in + out, -0.5 * alpha * (out - in));
 }
 
 // trace of element (ii, jj) at the Gauss nodes of one side, from its
@@ -82,19 +83,19 @@ __global__ void __launch_bounds__(128) adv_elem_kernel(AdvParams ap)
         adv_trace<P, true, -1>(self, ms, own);
         adv_trace<P, true, 1>(elem(i - 1, j), ms, nb);
 #pragma unroll
-        for (int q = 0; q < N; ++q) fl[q] = adv_flux(nb[q], own[q], ap.bx, ap.bdy);
+        for (int q = 0; q < N; ++q) fl[q] = adv_flux(nb[q], own[q], ap.bx, ap.ax, ap.bdy);
         adv_trace<P, true, 1>(self, ms, own);
         adv_trace<P, true, -1>(elem(i + 1, j), ms, nb);
 #pragma unroll
-        for (int q = 0; q < N; ++q) fr[q] = adv_flux(own[q], nb[q], ap.bx, ap.bdy);
+        for (int q = 0; q < N; ++q) fr[q] = adv_flux(own[q], nb[q], ap.bx, ap.ax, ap.bdy);
         adv_trace<P, false, -1>(self, ms, own);
         adv_trace<P, false, 1>(elem(i, j - 1), ms, nb);
 #pragma unroll
-        for (int q = 0; q < N; ++q) fb[q] = adv_flux(nb[q], own[q], ap.by, ap.bdx);
+        for (int q = 0; q < N; ++q) fb[q] = adv_flux(nb[q], own[q], ap.by, ap.ay, ap.bdx);
         adv_trace<P, false, 1>(self, ms, own);
         adv_trace<P, false, -1>(elem(i, j + 1), ms, nb);
 #pragma unroll
-        for (int q = 0; q < N; ++q) ft[q] = adv_flux(own[q], nb[q], ap.by, ap.bdx);
+        for (int q = 0; q < N; ++q) ft[q] = adv_flux(own[q], nb[q], ap.by, ap.ay, ap.bdx);
     }
     // lifts (x faces along xi, y faces along eta), then the volume:
     // sum_k Dx[ii][k] F[k][jj] + sum_k dh[jj][k] G[ii][k]
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(128) adv_stage_kernel(AdvParams ap)
         adv_trace_r<P, false, 1>(nxt, tT);
         adv_trace_r<P, false, -1>(cur, tB);
 #pragma unroll
-        for (int q = 0; q < N; ++q) fb[q] = adv_flux(tT[q], tB[q], ap.by, ap.bdx);
+        for (int q = 0; q < N; ++q) fb[q] = adv_flux(tT[q], tB[q], ap.by, ap.ay, ap.bdx);
     }
     for (int j = jb; j < je; ++j) {
         load(j + 1, nxt);
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(128) adv_stage_kernel(AdvParams ap)
             adv_trace_r<P, true, 1>(cur, tR);
             adv_trace_r<P, true, -1>(cur, tL);
 #pragma unroll
-            for (int q = 0; q < N; ++q) fr[q] = adv_flux(tR[q], __shfl_down_sync(0xffffffffu, tL[q], 1), ap.bx, ap.bdy);
+            for (int q = 0; q < N; ++q) fr[q] = adv_flux(tR[q], __shfl_down_sync(0xffffffffu, tL[q], 1), ap.bx, ap.ax, ap.bdy);
 #pragma unroll
             for (int q = 0; q < N; ++q) fl[q] = __shfl_up_sync(0xffffffffu, fr[q], 1);
         }
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(128) adv_stage_kernel(AdvParams ap)
             double tB[N];
             adv_trace_r<P, false, -1>(nxt, tB);
 #pragma unroll
-            for (int q = 0; q < N; ++q) fb[q] = adv_flux(tT[q], tB[q], ap.by, ap.bdx);
+            for (int q = 0; q < N; ++q) fb[q] = adv_flux(tT[q], tB[q], ap.by, ap.ay, ap.bdx);
 #pragma unroll
             for (int a = 0; a < N; ++a)
 #pragma unroll

@@ -765,12 +765,23 @@ int dgswe_adv_create(const dgswe_adv_cfg *cfg, const double *leg, const double *
     ap.zstride = (long long)c.nx * c.ny * n * n;
     ap.bx = c.beta_x;
     ap.by = c.beta_y;
+    ap.ax = std::fabs(c.beta_x);   // the model's wavespeed (models.py:129-131), local = global
+    ap.ay = std::fabs(c.beta_y);
     ap.bdx = c.dx / 2.0;
     ap.bdy = c.dy / 2.0;
     ap.cx = determ / ap.bdx;
     ap.cy = determ / ap.bdy;
     ap.inv_determ = 1.0 / determ;
     *out = ctx;
+    return DGSWE_OK;
+}
+
+int dgswe_adv_set_alpha(dgswe_adv_ctx *ctx, double alpha)
+{
+    if (!ctx) return dgswe_fail(DGSWE_EINVAL, "null context");
+    if (!(alpha >= 0.0) || !std::isfinite(alpha)) return dgswe_fail(DGSWE_EINVAL, "alpha must be finite and >= 0");
+    ctx->ap.ax = alpha;
+    ctx->ap.ay = alpha;
     return DGSWE_OK;
 }
 

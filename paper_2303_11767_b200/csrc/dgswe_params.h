@@ -123,6 +123,7 @@ struct AdvParams {
     int nx, ny;
     long long zstride;                 // nx * ny * nphi
     double bx, by;                     // advection velocity
+    double ax, ay;                     // Rusanov alpha per direction: |bx|, |by| or a pinned value
     double bdx, bdy;                   // face Jacobians dx/2, dy/2
     double cx, cy;                     // determ / bd_det_x, determ / bd_det_y (dg.py:199-202)
     double inv_determ;                 // the nodal mass 1 / determ

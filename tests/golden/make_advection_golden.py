@@ -70,6 +70,20 @@ def main():
                                         diagnostics.l2_error(st2, setup.exact(T_FINAL), op, relative=True)])
         out[f"{name}/meta"] = np.array([nx, ny, p, rk, dt, nsteps, log.steps, log.dt])
         print(name, "done", flush=True)
+    # a pinned global Rusanov alpha (dg.py:389-392) on the first case: RHS of
+    # the N-step state and 3 more steps
+    name, nx, ny, p, rk, dt, nsteps = CASES[0]
+    cfg = cases.default_config("advection_sine").override(nx=nx, ny=ny, p=p, rk=rk)
+    setup = cases.build_case(cfg)
+    op = dg.SpatialOperator(setup.mesh, p, setup.model, rusanov=dg.RusanovParams("global", 2.5))
+    st = op.zero_state()
+    st.fields["u"].data[1:-1, 1:-1] = out[f"{name}/xn"][0]
+    out[f"{name}/pinned/rhs"] = coeffs_of(op.assemble_rhs(st))
+    tab = timestep.tableau(rk)
+    ws = timestep._RKWorkspace(st, tab.s)
+    for _ in range(3):
+        timestep.rk_step(st, op.assemble_rhs, dt, tab, ws)
+    out[f"{name}/pinned/x3"] = coeffs_of(st)
     np.savez_compressed(os.path.join(HERE, "advection.npz"), **out)
 
 

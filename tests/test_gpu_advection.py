@@ -137,3 +137,21 @@ def test_advection_convergence(P):
         errs.append(P.l2_error(st, setup.exact(0.05), op))
     rate = P.convergence_rate(errs[0], 1.0 / 8, errs[1], 1.0 / 16)
     assert rate > 2.7, (errs, rate)
+
+
+def test_advection_pinned_alpha_vs_reference(P, gold):
+    """RusanovParams("global", 2.5) (dg.py:389-392): one RHS and 3 steps."""
+    name = "sine_20x20_p2"
+    nx, ny, p, rk, dt, nsteps, n_int, dt_int = gold[f"{name}/meta"]
+    setup = P.build_case(P.default_config("advection_sine").override(nx=int(nx), ny=int(ny), p=int(p), rk=int(rk)))
+    op = P.AdvectionOperator(setup.mesh, int(p), setup.model, rusanov=P.RusanovParams("global", 2.5))
+    x = op.state_from_coeffs({"u": gold[f"{name}/xn"][0][:, :, 0, :]})
+    assert rel(op.assemble_rhs(x).to_numpy(), gold[f"{name}/pinned/rhs"]) <= 1e-13
+    tab = P.tableau(int(rk))
+    ws = P.stepping._RKWorkspace(x, tab.s)
+    for _ in range(3):
+        P.rk_step(x, op.assemble_rhs, float(dt), tab, ws)
+    assert rel(x.to_numpy(), gold[f"{name}/pinned/x3"]) <= 1e-12
+    default = P.AdvectionOperator(setup.mesh, int(p), setup.model, rusanov=P.RusanovParams("global"))
+    assert rel(default.assemble_rhs(x).to_numpy(), P.AdvectionOperator(setup.mesh, int(p), setup.model)
+               .assemble_rhs(x).to_numpy()) == 0.0           # global == local for constant beta
