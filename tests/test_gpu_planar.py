@@ -153,3 +153,20 @@ def test_planar_global_alpha_vs_reference(P, gold, tag):
         err = np.linalg.norm(got[v] - ref[v])
         sens = np.linalg.norm(ulp[v] - ref[v])
         assert err <= 20.0 * sens + 1e-13 * np.linalg.norm(ref[v]), (v, err, sens)
+
+
+def test_planar_default_run_vs_reference(P):
+    """The reference's default f-plane run (50x50, p = 3, RK4, dt = 100 s,
+    360 steps to t = 36000 s) through integrate(): the final state within
+    1e-10 relative of the unmodified reference's own run
+    (tests/golden/planar_default.npz), mass conserved like the reference's."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "planar_default.npz"))
+    cfg = P.default_config("geostrophic_adjustment")
+    setup = P.build_case(cfg)
+    op = P.SpatialOperator(setup.mesh, cfg.p, setup.model)
+    st = op.project_state(setup.ic)
+    st, log = P.integrate(st, op, P.TimeControls(t_final=cfg.t_final, dt=cfg.dt), P.tableau(cfg.rk))
+    assert log.steps == int(g["steps"][0])
+    state_gate(st.to_numpy(), g["xT"], tol=1e-10)
+    m0, mT = g["mass"]
+    assert abs(P.mass_integral(st, op) - m0) <= 1e-13 * abs(m0)
