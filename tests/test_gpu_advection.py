@@ -155,3 +155,21 @@ def test_advection_pinned_alpha_vs_reference(P, gold):
     default = P.AdvectionOperator(setup.mesh, int(p), setup.model, rusanov=P.RusanovParams("global"))
     assert rel(default.assemble_rhs(x).to_numpy(), P.AdvectionOperator(setup.mesh, int(p), setup.model)
                .assemble_rhs(x).to_numpy()) == 0.0           # global == local for constant beta
+
+
+def test_advection_default_run_vs_reference(P):
+    """The reference's default advection run (20x20, p = 2, RK4, Courant
+    0.2, one period) through integrate(): final state within 1e-12 relative
+    of the reference's own run, its L2 error against the exact solution
+    within 1e-9 relative (tests/golden/advection_default.npz)."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "advection_default.npz"))
+    cfg = P.default_config("advection_sine")
+    setup = P.build_case(cfg)
+    op = P.AdvectionOperator(setup.mesh, cfg.p, setup.model)
+    st = op.project_state(setup.ic)
+    st, log = P.integrate(st, op, P.TimeControls(t_final=cfg.t_final, courant=cfg.courant), P.tableau(cfg.rk))
+    assert log.steps == int(g["steps"][0]) and log.dt == float(g["dt"][0])
+    assert rel(st.to_numpy(), g["xT"]) <= 1e-12
+    err, err_rel = g["err"]
+    assert abs(P.l2_error(st, setup.exact(cfg.t_final), op) - err) <= 1e-9 * err
+    assert abs(P.l2_error(st, setup.exact(cfg.t_final), op, relative=True) - err_rel) <= 1e-9 * err_rel
