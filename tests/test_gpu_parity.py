@@ -578,3 +578,26 @@ def test_low_order_kernel_levels_bitwise(P, monkeypatch):
         assert op.status()[0] == 0
         out.append(st.to_numpy())
     assert np.array_equal(out[0], out[1])
+
+
+def test_tc2_default_config_fails_like_reference(P):
+    """The reference's own default TC2 configuration (20x20, p = 3, RK4,
+    Courant 0.2) is unstable: its integrate() raises DivergenceError at step
+    7, t = 596.22 s (a PositivityError in the RHS) and leaves u after step
+    6.  The fused integrate reports the same step and time and leaves that
+    state up to the run's own rounding amplification
+    (tests/golden/tc2_default_failure.npz)."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "tc2_default_failure.npz"))
+    cfg = P.default_config("williamson_tc2")
+    setup = P.build_case(cfg)
+    op = P.SpatialOperator(setup.mesh, cfg.p, setup.model)
+    st = op.project_state(setup.ic)
+    with pytest.raises(P.DivergenceError) as ei:
+        P.integrate(st, op, P.TimeControls(t_final=cfg.t_final, courant=cfg.courant), P.tableau(cfg.rk))
+    assert ei.value.step == int(g["step"][0]) and ei.value.t == float(g["t"][0])
+    # six steps at 7x the stable dt amplify rounding ~100x per step: the
+    # reference's own state moves by 8e-4 / 1e-2 / 7e-2 (h / hu / hv) under a
+    # 1-ulp change of the initial state; ours stays within 50x that spread
+    got, ref, ulp = st.to_numpy(), g["x"], g["x_ulp"]
+    for v in range(3):
+        assert np.linalg.norm(got[v] - ref[v]) <= 50.0 * np.linalg.norm(ulp[v] - ref[v]), v
