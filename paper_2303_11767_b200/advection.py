@@ -18,7 +18,7 @@ import ctypes
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, tracing
 from .geometry import Mesh, build_vander, gauss_legendre, project_initial, row_mass_matrices
 
 
@@ -153,6 +153,10 @@ class AdvectionOperator:
                                                 ctypes.c_void_p(Y.data.data_ptr()),
                                                 ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
                        "dgswe_adv_stage")
+        if tracing.get_op_recorder() is not None:
+            rgn = tracing.LaunchRegion((self.mesh.nx, self.mesh.ny, self.nz), self.p, nvars=1)
+            tracing.record("stage", "dgswe_adv_stage", rgn, 24.0 if (U is not None and a != 0.0) else 16.0,
+                           tracing.adv_stage_flops_per_dof(self.p))
 
     def assemble_rhs(self, state: AdvState, out: AdvState | None = None) -> AdvState:
         """M^-1 (volume - boundary) of the advection operator (dg.py:504-523)."""

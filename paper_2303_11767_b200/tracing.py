@@ -34,15 +34,17 @@ def get_op_recorder():
 
 @dataclass(frozen=True)
 class LaunchRegion:
-    """The work of one launch: ``domain`` = (nx, rows, nz) elements, degree p."""
+    """The work of one launch: ``domain`` = (nx, rows, nz) elements, degree
+    p, ``nvars`` variables (3 for shallow water, 1 for linear advection)."""
 
     domain: tuple
     p: int
+    nvars: int = 3
 
     @property
     def dofs(self) -> int:
         nx, rows, nz = self.domain
-        return nx * rows * nz * 3 * (self.p + 1) ** 2
+        return nx * rows * nz * self.nvars * (self.p + 1) ** 2
 
 
 def stage_flops_per_dof(p: int) -> float:
@@ -54,6 +56,16 @@ def stage_flops_per_dof(p: int) -> float:
     over n DOFs, the four face lifts 8, mass and stage combination 4."""
     n = p + 1
     return 4.0 * (2 * n - 1) / n + 4.0 * n + 10.0 + 20.0 / n + 8.0 + 4.0
+
+
+def adv_stage_flops_per_dof(p: int) -> float:
+    """Analytic FP64 flops per DOF-update of one linear-advection stage
+    (dgswe_adv.cuh, n = p+1, FMA = 2): modal <-> nodal conversions 8n, the
+    two weak derivatives 4n, traces of the element and its neighbours from
+    the modes ~16 over n^2 nodes per face pair, fluxes and lifts ~12,
+    mass and stage combination 4."""
+    n = p + 1
+    return 12.0 * n + 16.0 / n + 16.0
 
 
 def record(kind: str, op: str, rgn: LaunchRegion, bytes_per_dof: float, flops_per_dof: float) -> None:

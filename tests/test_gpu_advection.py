@@ -173,3 +173,25 @@ def test_advection_default_run_vs_reference(P):
     err, err_rel = g["err"]
     assert abs(P.l2_error(st, setup.exact(cfg.t_final), op) - err) <= 1e-9 * err
     assert abs(P.l2_error(st, setup.exact(cfg.t_final), op, relative=True) - err_rel) <= 1e-9 * err_rel
+
+
+def test_advection_op_recorder(P, gold):
+    """set_op_recorder (fields.py:66-76) sees one record per advection launch,
+    with the one-variable DOF count."""
+    name = "sine_16x12_p3"
+    setup, op, cfg, dt, nsteps = make(P, gold, name)
+    st = op.project_state(setup.ic)
+    seen = []
+
+    class Rec:
+        def record(self, kind, opname, rgn, flops, nbytes):
+            seen.append((kind, opname, rgn.dofs, nbytes))
+
+    P.set_op_recorder(Rec())
+    try:
+        op.rk_steps(st, dt, 2, 3)
+    finally:
+        P.set_op_recorder(None)
+    dofs = 16 * 12 * 16
+    assert len(seen) == 6 and all(s[1] == "dgswe_adv_stage" and s[2] == dofs for s in seen)
+    assert [s[3] for s in seen[:3]] == [16 * dofs, 24 * dofs, 24 * dofs]
