@@ -601,3 +601,22 @@ def test_tc2_default_config_fails_like_reference(P):
     got, ref, ulp = st.to_numpy(), g["x"], g["x_ulp"]
     for v in range(3):
         assert np.linalg.norm(got[v] - ref[v]) <= 50.0 * np.linalg.norm(ulp[v] - ref[v]), v
+
+
+def test_tc6_default_config_first_hour_vs_reference(P):
+    """The reference's default TC6 configuration (40x20, p = 3, RK4,
+    dt = 4 s) through integrate() for its first hour (900 steps): the final
+    state within 1e-11 relative per variable of the unmodified reference's
+    own run, mass conserved like the reference's (tests/golden/tc6_default_1h.npz)."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "tc6_default_1h.npz"))
+    cfg = P.default_config("williamson_tc6")
+    setup = P.build_case(cfg)
+    op = P.SpatialOperator(setup.mesh, cfg.p, setup.model)
+    st = op.project_state(setup.ic)
+    st, log = P.integrate(st, op, P.TimeControls(t_final=3600.0, dt=cfg.dt), P.tableau(cfg.rk))
+    assert log.steps == int(g["steps"][0])
+    got, ref = st.to_numpy(), g["xT"]
+    for v in range(3):
+        assert np.linalg.norm(got[v] - ref[v]) <= 1e-11 * np.linalg.norm(ref[v]), v
+    m0, mT = g["mass"]
+    assert abs(P.mass_integral(st, op) - m0) <= 1e-13 * abs(m0)
