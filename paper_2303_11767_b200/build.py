@@ -21,7 +21,8 @@ SRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(os.path.dirname(HERE), "build", "dgswe_obj")
 OUT = os.path.join(HERE, "libdgswe_b200.so")
 SOURCES = ["dgswe_b200.cu"] + [f"deg_p{p}.cu" for p in range(7)]
-HEADERS = ["dgswe_kernels.cuh", "dgswe_diag.cuh", "dgswe_degree.cuh", "dgswe_params.h", "dgswe_ctx.h"]
+HEADERS = ["dgswe_kernels.cuh", "dgswe_lo.cuh", "dgswe_adv.cuh", "dgswe_diag.cuh", "dgswe_degree.cuh", "dgswe_params.h",
+           "dgswe_ctx.h"]
 DEPS = SOURCES + HEADERS
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
